@@ -1,0 +1,137 @@
+/*
+ * dprt_cuda.h -- C ABI of libdprt_cuda.so, the B200 (sm_100a) data path for per-rank direct volume
+ * rendering of a brick and sort-last compositing of the RGBA partials.
+ *
+ * The reference (arxiv/paper_2501_01628, Python package `dprt`) has no native code; its per-rank compute
+ * slot is a numba call with flat contiguous arrays, outputs mutated in place, no return value and the GIL
+ * released (pkg/src/dprt/engine.py:254-279 -> bvh.py:284-311, `@njit(nogil=True)` bvh.py:160).  Each entry
+ * point below takes that slot's place in the same style: plain pointers and sizes, no torch types,
+ * results written in place into caller-owned buffers, stream ordered, and errors returned as status codes
+ * (never thrown across the ABI).  The host wrapper (paper_2501_01628_b200/_lib.py) maps the codes onto the
+ * reference's exception taxonomy (pkg/src/dprt/errors.py:4-29).
+ *
+ * Ownership: the caller (Python / torch) owns every image, transfer-function and frame buffer; the library
+ * borrows device pointers until the stream work completes.  Opaque handles (DprtBrick) are owned by the
+ * library and released by *_destroy, mirroring RefCounted.release (pkg/src/dprt/refcount.py:39-48).
+ * Threading: every call binds `device` itself; calls on different devices may run concurrently from
+ * different host threads (one thread per rank, as run_collective does, transport.py:545-548).
+ */
+#ifndef DPRT_CUDA_H
+#define DPRT_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPRT_ABI_VERSION 1
+
+/* status codes -> Python exceptions (errors.py:4-29) */
+#define DPRT_OK 0
+#define DPRT_E_USAGE -1     /* UsageError: bad argument, dead handle */
+#define DPRT_E_CUDA -2      /* TransportError subclass DeviceError: CUDA runtime failure */
+#define DPRT_E_NOMEM -3     /* DeviceError: allocation failed */
+#define DPRT_E_TRANSPORT -4 /* TransportError: peer memory (IPC) failure */
+
+#define DPRT_MAX_BLOBS 64
+#define DPRT_MAX_PARTS 64
+
+/* Brick descriptor: a vertex-centred f32 field of dims[0] x dims[1] x dims[2] voxels (x fastest);
+ * voxel (i, j, k) sits at origin + (i, j, k) * spacing.  The brick OWNS cells [lo, hi) (0 <= lo < hi <=
+ * dims - 1) and stores voxels [max(lo - ghost, 0), min(hi + ghost, dims - 1)].
+ * Replaces the per-rank triangle set a Partition hands each rank (pkg/src/dprt/scene.py:52-58). */
+typedef struct DprtBrickDesc {
+    int64_t dims[3];
+    int64_t lo[3];
+    int64_t hi[3];
+    int32_t ghost;
+    int32_t reserved;
+    double origin[3];
+    double spacing[3];
+} DprtBrickDesc;
+
+/* Pinhole camera, host-evaluated exactly as CameraSpec.basis() (geom.py:163-168) and
+ * camera_primary_ray's half extents (geom.py:250-251). */
+typedef struct DprtCamera {
+    double pos[3];
+    double fwd[3];
+    double right[3];
+    double up[3];
+    double half_w;
+    double half_h;
+} DprtCamera;
+
+/* Synthetic field: kind 0 = blob mixture, `blobs` = host array of n_blobs x {cx, cy, cz, inv_rho2, amp}
+ * in unit-cube coordinates (parameters drawn as scene.py:258-262). */
+typedef struct DprtFieldSpec {
+    int32_t kind;
+    int32_t n_blobs;
+    const double* blobs;
+} DprtFieldSpec;
+
+/* March parameters.  tf_rgba: DEVICE pointer to n_tf x {r, g, b, a} f32. */
+typedef struct DprtMarchParams {
+    const float* tf_rgba;
+    int32_t n_tf;
+    int32_t flags; /* DPRT_MARCH_* */
+    double vmin;
+    double vmax;
+    double dt;
+    double ert;
+} DprtMarchParams;
+
+#define DPRT_MARCH_NO_SKIP 1      /* disable exact empty-space skipping (macrocell min/max grid) */
+#define DPRT_MARCH_FULL_FRAME 2   /* march every pixel instead of the brick's screen footprint */
+
+#define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
+#define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */
+
+typedef struct DprtBrick DprtBrick;
+
+int dprt_cuda_version(void);
+const char* dprt_last_error(void); /* thread-local message of the last failing call on this thread */
+int dprt_device_count(int* n);
+
+/* Brick lifecycle.  Replaces World._on_commit's accel build (pkg/src/dprt/api.py:146-171) and
+ * build_bvh (bvh.py:105-157): the brick's device storage is the per-rank acceleration state. */
+int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out);
+int dprt_brick_stored(const DprtBrick* b, int64_t stored_lo[3], int64_t stored_dims[3]);
+int dprt_brick_upload(DprtBrick* b, const float* src, int src_is_device, void* stream);
+int dprt_brick_download(const DprtBrick* b, float* dst, int dst_is_device, void* stream);
+int dprt_brick_generate(DprtBrick* b, const DprtFieldSpec* spec, void* stream);
+/* Rebuild the macrocell min/max grid used for exact empty-space skipping (called by upload/generate). */
+int dprt_brick_build_macrocells(DprtBrick* b, void* stream);
+int dprt_brick_destroy(DprtBrick* b);
+
+/* Screen footprint [x0, y0, x1, y1) of the owned box under `cam` (whole frame if the eye is too close). */
+int dprt_brick_footprint(const DprtBrick* b, const DprtCamera* cam, int W, int H, int32_t rect[4]);
+
+/* Per-rank local work: replaces trace_local_round -> trace_nearest_batch (engine.py:254-279,
+ * bvh.py:284-296).  Writes the full-frame premultiplied RGBA partial (W*H*4 f32, zero outside the
+ * footprint) and, if `samples` is non-NULL, the owned lattice sample count per pixel (W*H u32). */
+int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
+               uint32_t* samples, int W, int H, void* stream);
+
+/* Sort-last 'over' of P contiguous fragments of npix pixels each, already in front-to-back order
+ * (DESIGN.md §2.8).  Replaces the reference's order-independent (t, gid) min (bvh.py:246-248) plus
+ * the final tone map (engine.py:500-502) for the pixels a rank owns (engine.py:216-221).  `inputs`
+ * is a HOST array of P device pointers -- local buffers, received fragments or mapped peer pointers
+ * (NVLink P2P), so the same kernel is the single-GPU, NCCL and fused-P2P compositor.  rgb8 (npix*3) and
+ * rgba_out (npix*4) may also be peer pointers (fused gather into rank 0's frame). */
+int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, const float bg[3], int flags,
+                   uint8_t* rgb8, float* rgba_out, void* stream);
+
+/* Peer memory over NVLink for the fused direct-send compositor (one process per GPU). */
+int dprt_ipc_handle(int device, const void* dev_ptr, uint8_t handle[64]);
+int dprt_ipc_open(int device, const uint8_t handle[64], void** out_ptr);
+int dprt_ipc_close(int device, void* ptr);
+int dprt_enable_peer(int device, int peer);
+
+/* Stream-ordered helpers for the host driver (no torch types): device sync and an event timer. */
+int dprt_device_synchronize(int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPRT_CUDA_H */

@@ -1,0 +1,134 @@
+"""ctypes binding of libdprt_cuda.so (the C ABI in include/dprt_cuda.h).
+
+The data path has no CPU fallback: if the library is missing or unloadable every entry point raises
+``NativeLibraryMissing``.  ctypes releases the GIL for the duration of each foreign call, which is what
+the reference relies on numba's ``nogil=True`` for (pkg/src/dprt/bvh.py:160) so rank threads overlap.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+from typing import Optional
+
+from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
+
+LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
+ABI_VERSION = 1
+
+DPRT_OK = 0
+DPRT_E_USAGE = -1
+DPRT_E_CUDA = -2
+DPRT_E_NOMEM = -3
+DPRT_E_TRANSPORT = -4
+
+MAX_BLOBS = 64
+MAX_PARTS = 64
+
+MARCH_NO_SKIP = 1
+MARCH_FULL_FRAME = 2
+COMPOSITE_TONEMAP = 1
+COMPOSITE_RGBA = 2
+
+EXPORTS = (
+    "dprt_cuda_version", "dprt_last_error", "dprt_device_count", "dprt_device_synchronize",
+    "dprt_brick_create", "dprt_brick_stored", "dprt_brick_upload", "dprt_brick_download",
+    "dprt_brick_generate", "dprt_brick_build_macrocells", "dprt_brick_destroy", "dprt_brick_footprint",
+    "dprt_march", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
+    "dprt_enable_peer",
+)
+
+c_double3 = ctypes.c_double * 3
+c_int64_3 = ctypes.c_int64 * 3
+
+
+class BrickDesc(ctypes.Structure):
+    _fields_ = [("dims", c_int64_3), ("lo", c_int64_3), ("hi", c_int64_3), ("ghost", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("origin", c_double3), ("spacing", c_double3)]
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("pos", c_double3), ("fwd", c_double3), ("right", c_double3), ("up", c_double3),
+                ("half_w", ctypes.c_double), ("half_h", ctypes.c_double)]
+
+
+class FieldSpec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("n_blobs", ctypes.c_int32), ("blobs", ctypes.c_void_p)]
+
+
+class MarchParams(ctypes.Structure):
+    _fields_ = [("tf_rgba", ctypes.c_void_p), ("n_tf", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("vmin", ctypes.c_double), ("vmax", ctypes.c_double), ("dt", ctypes.c_double),
+                ("ert", ctypes.c_double)]
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def _declare(lib: ctypes.CDLL) -> None:
+    P = ctypes.c_void_p
+    I = ctypes.c_int
+    sig = {
+        "dprt_cuda_version": ([], I),
+        "dprt_last_error": ([], ctypes.c_char_p),
+        "dprt_device_count": ([P], I),
+        "dprt_device_synchronize": ([I], I),
+        "dprt_brick_create": ([I, P, P], I),
+        "dprt_brick_stored": ([P, P, P], I),
+        "dprt_brick_upload": ([P, P, I, P], I),
+        "dprt_brick_download": ([P, P, I, P], I),
+        "dprt_brick_generate": ([P, P, P], I),
+        "dprt_brick_build_macrocells": ([P, P], I),
+        "dprt_brick_destroy": ([P], I),
+        "dprt_brick_footprint": ([P, P, I, I, P], I),
+        "dprt_march": ([P, P, P, P, P, I, I, P], I),
+        "dprt_composite": ([I, P, I, ctypes.c_int64, P, I, P, P, P], I),
+        "dprt_ipc_handle": ([I, P, P], I),
+        "dprt_ipc_open": ([I, P, P], I),
+        "dprt_ipc_close": ([I, P], I),
+        "dprt_enable_peer": ([I, I], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library; raises NativeLibraryMissing (no fallback) if it cannot be loaded."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("DPRT_CUDA_LIB", str(LIB_PATH)))
+    if not path.exists():
+        raise NativeLibraryMissing(
+            f"{path} not built: run `python -m paper_2501_01628_b200.build` (there is no CPU fallback)")
+    try:
+        handle = ctypes.CDLL(str(path))
+    except OSError as exc:
+        raise NativeLibraryMissing(f"cannot load {path}: {exc}") from exc
+    _declare(handle)
+    if handle.dprt_cuda_version() != ABI_VERSION:
+        raise NativeLibraryMissing(f"{path} ABI {handle.dprt_cuda_version()} != expected {ABI_VERSION}; rebuild")
+    _lib = handle
+    return handle
+
+
+def check(rc: int, what: str) -> None:
+    """Map a status code onto the reference's exception taxonomy (errors.py:4-29)."""
+    if rc == DPRT_OK:
+        return
+    msg = (lib().dprt_last_error() or b"").decode("utf-8", "replace")
+    text = f"{what}: {msg}" if msg else what
+    if rc == DPRT_E_USAGE:
+        raise UsageError(text)
+    if rc == DPRT_E_TRANSPORT:
+        raise TransportError(text)
+    raise DeviceError(text)
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    rc = lib().dprt_device_count(ctypes.byref(n))
+    return int(n.value) if rc == DPRT_OK else 0

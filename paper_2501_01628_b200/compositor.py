@@ -1,0 +1,267 @@
+"""Sort-last compositing of per-rank RGBA partials: direct-send, binary-swap and fused peer-memory.
+
+The reference resolves cross-rank visibility by cycling every ray through every rank and reducing with
+the commutative (t, gid) min (pkg/src/dprt/engine.py:282-310, bvh.py:246-248), then gathers disjoint
+row tiles to rank 0 (engine.py:443-456, 485; transport.py:465-475).  Volume partials need the
+non-commutative 'over' in brick visibility order instead, so this module exchanges image fragments:
+
+* ``direct_send``: one round; rank j receives row block j (``assign_pixels``, engine.py:216-221) of every
+  other rank's partial, blends the P fragments in visibility order with the fused tone map, and sends
+  its RGB8 tile to rank 0.  On NVSwitch every peer is one hop at full bandwidth, so this is the default.
+* ``binary_swap``: log2(P) rounds; in round k rank r trades half of its current row range with
+  r XOR 2^k and blends the two group composites (front group first).  Needs P a power of two and a
+  visibility order in which every aligned rank group is contiguous (true for kd decompositions).
+* ``p2p``: one kernel per rank reads the P fragments of its row block straight out of the peers'
+  partial buffers over NVLink (CUDA IPC mappings), blends, tone-maps and writes the RGB8 tile directly
+  into rank 0's frame -- the exchange, the blend and the gather fused.
+
+Fragment bytes per rank per frame are (1 - 1/P)*W*H*16 in both exchange modes.  The
+blend itself always runs in libdprt_cuda.so (``CudaBlender``); there is no CPU blend in the product.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from .errors import UsageError
+from .transport import RankEndpoint
+
+
+def assign_rows(height: int, P: int) -> List[Tuple[int, int]]:
+    """Row blocks [b*H//P, (b+1)*H//P) -- engine.py:216-221."""
+    return [(b * height // P, (b + 1) * height // P) for b in range(P)]
+
+
+@dataclass(frozen=True)
+class DirectSendPlan:
+    rank: int
+    own_rows: Tuple[int, int]
+    sends: Tuple[Tuple[int, Tuple[int, int]], ...]   # (peer, rows of MY partial that peer owns)
+    recvs: Tuple[int, ...]                           # peers whose fragment of own_rows I receive
+
+
+def direct_send_plan(height: int, P: int, rank: int) -> DirectSendPlan:
+    blocks = assign_rows(height, P)
+    sends = tuple((j, blocks[j]) for j in range(P) if j != rank)
+    recvs = tuple(j for j in range(P) if j != rank)
+    return DirectSendPlan(rank, blocks[rank], sends, recvs)
+
+
+@dataclass(frozen=True)
+class SwapRound:
+    k: int
+    partner: int
+    keep: Tuple[int, int]   # block range kept after the round
+    give: Tuple[int, int]   # block range sent to the partner
+    my_group: Tuple[int, int]       # rank range [g0, g1) my current composite covers
+    partner_group: Tuple[int, int]
+
+
+def binary_swap_plan(P: int, rank: int) -> Tuple[List[SwapRound], int]:
+    """Rounds for ``rank`` and the final row block it ends up owning (bit-reversed rank)."""
+    if P < 1 or P & (P - 1):
+        raise UsageError(f"binary-swap needs a power-of-two rank count, got {P}")
+    rounds: List[SwapRound] = []
+    b0, b1 = 0, P
+    k = 0
+    while (1 << k) < P:
+        partner = rank ^ (1 << k)
+        mid = (b0 + b1) // 2
+        lower, upper = (b0, mid), (mid, b1)
+        keep, give = (lower, upper) if not (rank >> k) & 1 else (upper, lower)
+        size = 1 << k
+        g0 = (rank >> k) << k
+        p0 = (partner >> k) << k
+        rounds.append(SwapRound(k, partner, keep, give, (g0, g0 + size), (p0, p0 + size)))
+        b0, b1 = keep
+        k += 1
+    return rounds, b0
+
+
+class CudaBlender:
+    """The product blender: libdprt_cuda.so's composite kernel."""
+
+    def over(self, frags: Sequence[torch.Tensor], out_rgba: torch.Tensor) -> None:
+        from . import device as dev
+        dev.composite(frags, None, rgba=out_rgba)
+
+    def over_tonemap(self, frags: Sequence[torch.Tensor], background, out_rgb8: torch.Tensor,
+                     out_rgba: Optional[torch.Tensor] = None) -> None:
+        from . import device as dev
+        dev.composite(frags, background, rgb8=out_rgb8, rgba=out_rgba)
+
+
+@dataclass
+class CompositeOutput:
+    rgb8: Optional[torch.Tensor]   # rank 0: (H, W, 3) uint8
+    rgba: Optional[torch.Tensor]   # rank 0 with keep_float: (H*W*4) f32 blended, no background
+
+
+class Compositor:
+    """Per-rank compositing state for one frame size (scratch buffers persist across frames)."""
+
+    def __init__(self, ep: RankEndpoint, width: int, height: int, mode: str, device: torch.device,
+                 blender=None):
+        self.ep = ep
+        self.W = width
+        self.H = height
+        self.device = device
+        self.mode_requested = mode
+        self.mode = self.resolve_mode(mode, ep.R)
+        self.blender = blender if blender is not None else CudaBlender()
+        self.last_bytes = 0
+        self._frame = None
+        self._frame_rgba = None
+        self._scratch: Dict[str, torch.Tensor] = {}
+
+    @staticmethod
+    def resolve_mode(mode: str, P: int) -> str:
+        if P == 1:
+            return "single"
+        if mode == "auto":
+            return "direct_send"
+        if mode == "binary_swap" and P & (P - 1):
+            raise UsageError(f"binary_swap needs a power-of-two rank count, got {P}")
+        if mode not in ("direct_send", "binary_swap", "p2p"):
+            raise UsageError(f"unknown composite mode {mode!r}")
+        return mode
+
+    def _buf(self, name: str, numel: int, dtype=torch.float32) -> torch.Tensor:
+        t = self._scratch.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(numel, dtype=dtype, device=self.device)
+            self._scratch[name] = t
+        return t[:numel]
+
+    def _frame_buffers(self, keep_float: bool):
+        if self._frame is None:
+            self._frame = torch.empty((self.H, self.W, 3), dtype=torch.uint8, device=self.device)
+        if keep_float and self._frame_rgba is None:
+            self._frame_rgba = torch.empty(self.H * self.W * 4, dtype=torch.float32, device=self.device)
+        return self._frame, (self._frame_rgba if keep_float else None)
+
+    def _rows(self, flat: torch.Tensor, rows: Tuple[int, int], ch: int) -> torch.Tensor:
+        return flat[rows[0] * self.W * ch: rows[1] * self.W * ch]
+
+    # ------------------------------------------------------------------------------------------
+    def composite(self, partial: torch.Tensor, order: Sequence[int], background, keep_float: bool = False,
+                  solo: bool = False) -> CompositeOutput:
+        order = list(order)
+        if sorted(order) != list(range(self.ep.R)):
+            raise UsageError(f"visibility order {order} is not a permutation of {self.ep.R} ranks")
+        self.last_bytes = 0
+        if self.mode == "single" or solo:
+            return self._single(partial, background, keep_float)
+        if self.mode == "direct_send":
+            return self._direct_send(partial, order, background, keep_float)
+        if self.mode == "binary_swap":
+            return self._binary_swap(partial, order, background, keep_float)
+        return self._p2p(partial, order, background, keep_float)
+
+    def _single(self, partial, background, keep_float) -> CompositeOutput:
+        if self.ep.rank != 0:
+            return CompositeOutput(None, None)
+        frame, rgba = self._frame_buffers(keep_float)
+        self.blender.over_tonemap([partial], background, frame.view(-1), rgba)
+        return CompositeOutput(frame, rgba)
+
+    def _gather_tiles(self, rows: Tuple[int, int], tile_rgb8: torch.Tensor, tile_rgba: Optional[torch.Tensor],
+                      all_rows: Sequence[Tuple[int, int]], keep_float: bool) -> CompositeOutput:
+        """Final gather of RGB8 (and optionally RGBA) row tiles to rank 0 (engine.py:485-487)."""
+        ep = self.ep
+        if ep.rank == 0:
+            frame, frame_rgba = self._frame_buffers(keep_float)
+            flat = frame.view(-1)
+            recvs = []
+            for src in range(1, ep.R):
+                r = all_rows[src]
+                if r[1] > r[0]:
+                    recvs.append((src, self._rows(flat, r, 3)))
+                    if keep_float:
+                        recvs.append((src, self._rows(frame_rgba, r, 4)))
+            own = self._rows(flat, rows, 3)
+            if tile_rgb8.data_ptr() != own.data_ptr():
+                own.copy_(tile_rgb8)
+            if keep_float:
+                own_f = self._rows(frame_rgba, rows, 4)
+                if tile_rgba.data_ptr() != own_f.data_ptr():
+                    own_f.copy_(tile_rgba)
+            ep.exchange([], recvs)
+            return CompositeOutput(frame, frame_rgba)
+        sends = []
+        if rows[1] > rows[0]:
+            sends.append((0, tile_rgb8))
+            if keep_float:
+                sends.append((0, tile_rgba))
+        ep.exchange(sends, [])
+        self.last_bytes += sum(t.numel() * t.element_size() for _, t in sends)
+        return CompositeOutput(None, None)
+
+    def _direct_send(self, partial, order, background, keep_float) -> CompositeOutput:
+        ep = self.ep
+        P, r = ep.R, ep.rank
+        plan = direct_send_plan(self.H, P, r)
+        rows = plan.own_rows
+        n_own = (rows[1] - rows[0]) * self.W
+        inbox = {j: self._buf(f"in{j}", n_own * 4) for j in plan.recvs}
+        sends = [(j, self._rows(partial, rr, 4)) for j, rr in plan.sends if rr[1] > rr[0]]
+        recvs = [(j, inbox[j]) for j in plan.recvs] if n_own else []
+        ep.exchange(sends, recvs)
+        self.last_bytes += sum(t.numel() * 4 for _, t in sends)
+        frags = [self._rows(partial, rows, 4) if s == r else inbox[s] for s in order]
+        tile = self._buf("tile8", n_own * 3, torch.uint8)
+        tile_f = self._buf("tilef", n_own * 4) if keep_float else None
+        if n_own:
+            self.blender.over_tonemap(frags, background, tile, tile_f)
+        return self._gather_tiles(rows, tile, tile_f, assign_rows(self.H, P), keep_float)
+
+    def _binary_swap(self, partial, order, background, keep_float) -> CompositeOutput:
+        ep = self.ep
+        P, r = ep.R, ep.rank
+        pos = {s: i for i, s in enumerate(order)}
+        rounds, final_block = binary_swap_plan(P, r)
+        blocks = assign_rows(self.H, P)
+
+        def rows_of(br):
+            return (blocks[br[0]][0], blocks[br[1] - 1][1])
+
+        cur = partial          # full-frame-indexed buffer holding my current group composite
+        work = [self._buf("swapA", self.H * self.W * 4), self._buf("swapB", self.H * self.W * 4)]
+        for i, rd in enumerate(rounds):
+            keep_rows, give_rows = rows_of(rd.keep), rows_of(rd.give)
+            n_keep = (keep_rows[1] - keep_rows[0]) * self.W
+            inbox = self._buf("swapIn", max(n_keep, 1) * 4)[: n_keep * 4]
+            send = self._rows(cur, give_rows, 4)
+            ep.exchange([(rd.partner, send)] if send.numel() else [], [(rd.partner, inbox)] if n_keep else [])
+            self.last_bytes += send.numel() * 4
+            mine = self._rows(cur, keep_rows, 4)
+            mine_front = min(pos[s] for s in range(*rd.my_group)) < min(pos[s] for s in range(*rd.partner_group))
+            frags = [mine, inbox] if mine_front else [inbox, mine]
+            last = i == len(rounds) - 1
+            if not last:
+                out = work[i % 2]
+                if n_keep:
+                    self.blender.over(frags, self._rows(out, keep_rows, 4))
+                cur = out
+            else:
+                tile = self._buf("tile8", n_keep * 3, torch.uint8)
+                tile_f = self._buf("tilef", n_keep * 4) if keep_float else None
+                if n_keep:
+                    self.blender.over_tonemap(frags, background, tile, tile_f)
+                final_rows = rows_of((final_block, final_block + 1))
+                assert final_rows == keep_rows
+                finals = [binary_swap_plan(P, s)[1] for s in range(P)]
+                all_rows = [rows_of((b, b + 1)) for b in finals]
+                return self._gather_tiles(keep_rows, tile, tile_f, all_rows, keep_float)
+        raise AssertionError("binary swap with P > 1 always has a last round")
+
+    def _p2p(self, partial, order, background, keep_float) -> CompositeOutput:
+        from .p2p import P2PCompositor
+        if not hasattr(self, "_p2p_impl"):
+            self._p2p_impl = P2PCompositor(self.ep, self.W, self.H, self.device)
+        out = self._p2p_impl.composite(partial, order, background, keep_float)
+        self.last_bytes = self._p2p_impl.last_bytes
+        return out

@@ -1,0 +1,378 @@
+// extern "C" entry points of libdprt_cuda.so (declared in include/dprt_cuda.h).
+//
+// Host-side glue only: argument validation, device binding, allocation, kernel-argument packing.  No
+// exception crosses the ABI; failures return a negative status and leave a thread-local message that
+// the Python wrapper maps onto the reference's error taxonomy (pkg/src/dprt/errors.py:4-29).
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "common.cuh"
+
+namespace dprt {
+cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream);
+cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cudaStream_t stream);
+cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream);
+cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream);
+}  // namespace dprt
+
+struct DprtBrick : dprt::DeviceBrick {};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    cudaGetLastError();  // clear sticky-free errors
+    int code = (e == cudaErrorMemoryAllocation) ? DPRT_E_NOMEM : DPRT_E_CUDA;
+    return fail(code, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CK(call, what)                                  \
+    do {                                                \
+        cudaError_t _e = (call);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+int bind(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0 || device >= n) return fail(DPRT_E_USAGE, "device %d outside [0, %d)", device, n);
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    return DPRT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dprt_cuda_version(void) { return DPRT_ABI_VERSION; }
+
+const char* dprt_last_error(void) { return g_err.c_str(); }
+
+int dprt_device_count(int* n) {
+    if (!n) return fail(DPRT_E_USAGE, "null output");
+    cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+        *n = 0;
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    return DPRT_OK;
+}
+
+int dprt_device_synchronize(int device) {
+    int rc = bind(device);
+    if (rc) return rc;
+    CK(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    return DPRT_OK;
+}
+
+int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
+    if (!desc || !out) return fail(DPRT_E_USAGE, "null brick descriptor or output");
+    *out = nullptr;
+    for (int a = 0; a < 3; ++a) {
+        if (desc->dims[a] < 2) return fail(DPRT_E_USAGE, "dims[%d] = %lld: need >= 2 voxels", a, (long long)desc->dims[a]);
+        if (!(0 <= desc->lo[a] && desc->lo[a] < desc->hi[a] && desc->hi[a] <= desc->dims[a] - 1))
+            return fail(DPRT_E_USAGE, "owned cells [%lld, %lld) invalid on axis %d for %lld voxels",
+                        (long long)desc->lo[a], (long long)desc->hi[a], a, (long long)desc->dims[a]);
+        if (!(desc->spacing[a] > 0.0) || !isfinite(desc->spacing[a]) || !isfinite(desc->origin[a]))
+            return fail(DPRT_E_USAGE, "spacing/origin on axis %d must be finite, spacing > 0", a);
+    }
+    if (desc->ghost < 0) return fail(DPRT_E_USAGE, "ghost must be >= 0");
+    int rc = bind(device);
+    if (rc) return rc;
+    DprtBrick* b = new DprtBrick();
+    b->device = device;
+    b->desc = *desc;
+    long long nvox = 1, nmc = 1;
+    for (int a = 0; a < 3; ++a) {
+        long long lo = desc->lo[a] - desc->ghost;
+        long long hi = desc->hi[a] + desc->ghost;
+        if (lo < 0) lo = 0;
+        if (hi > desc->dims[a] - 1) hi = desc->dims[a] - 1;
+        b->s_lo[a] = lo;
+        b->sd[a] = hi - lo + 1;
+        b->mcd[a] = (b->sd[a] - 1 + dprt::kMacro - 1) / dprt::kMacro;
+        nvox *= b->sd[a];
+        nmc *= b->mcd[a];
+    }
+    b->vox = nullptr;
+    b->macro = nullptr;
+    cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
+    if (e != cudaSuccess) {
+        if (b->vox) cudaFree(b->vox);
+        delete b;
+        return cuda_fail(e, "brick allocation");
+    }
+    *out = b;
+    return DPRT_OK;
+}
+
+int dprt_brick_stored(const DprtBrick* b, int64_t stored_lo[3], int64_t stored_dims[3]) {
+    if (!b) return fail(DPRT_E_USAGE, "null brick");
+    for (int a = 0; a < 3; ++a) {
+        if (stored_lo) stored_lo[a] = b->s_lo[a];
+        if (stored_dims) stored_dims[a] = b->sd[a];
+    }
+    return DPRT_OK;
+}
+
+static size_t brick_bytes(const DprtBrick* b) { return (size_t)b->sd[0] * b->sd[1] * b->sd[2] * sizeof(float); }
+
+int dprt_brick_build_macrocells(DprtBrick* b, void* stream) {
+    if (!b) return fail(DPRT_E_USAGE, "null brick");
+    int rc = bind(b->device);
+    if (rc) return rc;
+    CK(dprt::launch_macrocells(*b, (cudaStream_t)stream), "macrocell kernel launch");
+    return DPRT_OK;
+}
+
+int dprt_brick_upload(DprtBrick* b, const float* src, int src_is_device, void* stream) {
+    if (!b || !src) return fail(DPRT_E_USAGE, "null brick or source");
+    int rc = bind(b->device);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(b->vox, src, brick_bytes(b), src_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       (cudaStream_t)stream),
+       "brick upload");
+    return dprt_brick_build_macrocells(b, stream);
+}
+
+int dprt_brick_download(const DprtBrick* b, float* dst, int dst_is_device, void* stream) {
+    if (!b || !dst) return fail(DPRT_E_USAGE, "null brick or destination");
+    int rc = bind(b->device);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(dst, b->vox, brick_bytes(b), dst_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       (cudaStream_t)stream),
+       "brick download");
+    if (!dst_is_device) CK(cudaStreamSynchronize((cudaStream_t)stream), "brick download sync");
+    return DPRT_OK;
+}
+
+int dprt_brick_generate(DprtBrick* b, const DprtFieldSpec* spec, void* stream) {
+    if (!b || !spec) return fail(DPRT_E_USAGE, "null brick or field spec");
+    if (spec->kind != 0) return fail(DPRT_E_USAGE, "unknown field kind %d", spec->kind);
+    if (spec->n_blobs < 0 || spec->n_blobs > DPRT_MAX_BLOBS || (spec->n_blobs > 0 && !spec->blobs))
+        return fail(DPRT_E_USAGE, "n_blobs %d outside [0, %d]", spec->n_blobs, DPRT_MAX_BLOBS);
+    int rc = bind(b->device);
+    if (rc) return rc;
+    CK(dprt::launch_generate(*b, *spec, (cudaStream_t)stream), "generate kernel launch");
+    return dprt_brick_build_macrocells(b, stream);
+}
+
+int dprt_brick_destroy(DprtBrick* b) {
+    if (!b) return DPRT_OK;
+    int rc = bind(b->device);
+    if (rc) return rc;
+    cudaFree(b->vox);
+    cudaFree(b->macro);
+    delete b;
+    return DPRT_OK;
+}
+
+static void owned_box(const DprtBrick* b, double lo[3], double hi[3]) {
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = b->desc.origin[a] + (double)b->desc.lo[a] * b->desc.spacing[a];
+        hi[a] = b->desc.origin[a] + (double)b->desc.hi[a] * b->desc.spacing[a];
+    }
+}
+
+int dprt_brick_footprint(const DprtBrick* b, const DprtCamera* cam, int W, int H, int32_t rect[4]) {
+    if (!b || !cam || !rect || W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "bad footprint arguments");
+    double lo[3], hi[3];
+    owned_box(b, lo, hi);
+    double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+    bool full = false;
+    for (int c = 0; c < 8 && !full; ++c) {
+        double p[3] = {(c & 1) ? hi[0] : lo[0], (c & 2) ? hi[1] : lo[1], (c & 4) ? hi[2] : lo[2]};
+        double v[3] = {p[0] - cam->pos[0], p[1] - cam->pos[1], p[2] - cam->pos[2]};
+        double z = v[0] * cam->fwd[0] + v[1] * cam->fwd[1] + v[2] * cam->fwd[2];
+        double len = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        if (!(z > 1e-6 * (len + 1.0))) {
+            full = true;
+            break;
+        }
+        double x = (v[0] * cam->right[0] + v[1] * cam->right[1] + v[2] * cam->right[2]) / z;
+        double y = (v[0] * cam->up[0] + v[1] * cam->up[1] + v[2] * cam->up[2]) / z;
+        // invert geom.py:252-253 for the pixel coordinate of the film point
+        double px = (x / cam->half_w + 1.0) * 0.5 * W - 0.5;
+        double py = (1.0 - y / cam->half_h) * 0.5 * H - 0.5;
+        xmin = fmin(xmin, px);
+        xmax = fmax(xmax, px);
+        ymin = fmin(ymin, py);
+        ymax = fmax(ymax, py);
+    }
+    if (full) {
+        rect[0] = 0;
+        rect[1] = 0;
+        rect[2] = W;
+        rect[3] = H;
+        return DPRT_OK;
+    }
+    // one pixel of slack on every side keeps the rectangle conservative under rounding
+    double x0 = floor(xmin) - 1.0, x1 = ceil(xmax) + 2.0, y0 = floor(ymin) - 1.0, y1 = ceil(ymax) + 2.0;
+    rect[0] = (int32_t)fmax(0.0, fmin((double)W, x0));
+    rect[1] = (int32_t)fmax(0.0, fmin((double)H, y0));
+    rect[2] = (int32_t)fmax(0.0, fmin((double)W, x1));
+    rect[3] = (int32_t)fmax(0.0, fmin((double)H, y1));
+    return DPRT_OK;
+}
+
+int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
+               uint32_t* samples, int W, int H, void* stream) {
+    if (!b || !cam || !p || !partial_rgba) return fail(DPRT_E_USAGE, "null march argument");
+    if (W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "frame size %dx%d must be positive", W, H);
+    if (p->n_tf < 2 || p->n_tf > dprt::kMaxTf || !p->tf_rgba)
+        return fail(DPRT_E_USAGE, "transfer function needs 2..%d entries (got %d)", dprt::kMaxTf, p->n_tf);
+    if (!(p->vmax > p->vmin)) return fail(DPRT_E_USAGE, "transfer function range needs vmax > vmin");
+    if (!(p->dt > 0.0) || !isfinite(p->dt)) return fail(DPRT_E_USAGE, "dt must be finite and > 0");
+    if (!(cam->half_w > 0.0) || !(cam->half_h > 0.0)) return fail(DPRT_E_USAGE, "camera half extents must be > 0");
+    int rc = bind(b->device);
+    if (rc) return rc;
+    dprt::MarchArgs a;
+    memset(&a, 0, sizeof(a));
+    for (int i = 0; i < 3; ++i) {
+        a.o[i] = cam->pos[i];
+        a.f[i] = cam->fwd[i];
+        a.r[i] = cam->right[i];
+        a.u[i] = cam->up[i];
+        a.origin[i] = b->desc.origin[i];
+        a.spacing[i] = b->desc.spacing[i];
+        a.inv_spacing[i] = (float)(1.0 / b->desc.spacing[i]);
+        a.stored_lo_d[i] = (double)b->s_lo[i];
+        a.clo[i] = 0;
+        a.chi[i] = (int)(b->sd[i] - 2);
+        a.sd[i] = (int)b->sd[i];
+        a.mcd[i] = (int)b->mcd[i];
+    }
+    owned_box(b, a.blo, a.bhi);
+    a.half_w = cam->half_w;
+    a.half_h = cam->half_h;
+    a.dt = p->dt;
+    a.sy = (long long)b->sd[0];
+    a.sz = (long long)b->sd[0] * b->sd[1];
+    a.vox = b->vox;
+    a.macro = b->macro;
+    a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
+    a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
+    a.n_tf = p->n_tf;
+    a.vmin = (float)p->vmin;
+    a.tf_scale = (float)((double)(p->n_tf - 1) / (p->vmax - p->vmin));
+    a.ert = (float)p->ert;
+    a.out = reinterpret_cast<float4*>(partial_rgba);
+    a.samples = samples;
+    a.W = W;
+    a.H = H;
+    if (p->flags & DPRT_MARCH_FULL_FRAME) {
+        a.rect[0] = 0;
+        a.rect[1] = 0;
+        a.rect[2] = W;
+        a.rect[3] = H;
+    } else {
+        rc = dprt_brick_footprint(b, cam, W, H, a.rect);
+        if (rc) return rc;
+    }
+    CK(dprt::launch_march(a, (cudaStream_t)stream), "march kernel launch");
+    return DPRT_OK;
+}
+
+int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, const float bg[3], int flags,
+                   uint8_t* rgb8, float* rgba_out, void* stream) {
+    if (!inputs || P < 1 || P > DPRT_MAX_PARTS) return fail(DPRT_E_USAGE, "need 1..%d fragments (got %d)", DPRT_MAX_PARTS, P);
+    if (npix < 0) return fail(DPRT_E_USAGE, "negative pixel count");
+    if ((flags & DPRT_COMPOSITE_TONEMAP) && (!rgb8 || !bg)) return fail(DPRT_E_USAGE, "tone map needs rgb8 and bg");
+    if ((flags & DPRT_COMPOSITE_RGBA) && !rgba_out) return fail(DPRT_E_USAGE, "RGBA output requested but null");
+    if (!(flags & (DPRT_COMPOSITE_TONEMAP | DPRT_COMPOSITE_RGBA))) return fail(DPRT_E_USAGE, "no composite output selected");
+    int rc = bind(device);
+    if (rc) return rc;
+    dprt::CompositeArgs a;
+    memset(&a, 0, sizeof(a));
+    for (int i = 0; i < P; ++i) {
+        if (!inputs[i]) return fail(DPRT_E_USAGE, "fragment %d is null", i);
+        if (reinterpret_cast<uintptr_t>(inputs[i]) & 15) return fail(DPRT_E_USAGE, "fragment %d not 16-byte aligned", i);
+        a.in[i] = reinterpret_cast<const float4*>(inputs[i]);
+    }
+    a.P = P;
+    a.npix = npix;
+    if (bg) {
+        a.bg[0] = bg[0];
+        a.bg[1] = bg[1];
+        a.bg[2] = bg[2];
+    }
+    a.flags = flags;
+    a.rgb8 = rgb8;
+    a.rgba = reinterpret_cast<float4*>(rgba_out);
+    CK(dprt::launch_composite(a, (cudaStream_t)stream), "composite kernel launch");
+    return DPRT_OK;
+}
+
+int dprt_ipc_handle(int device, const void* dev_ptr, uint8_t handle[64]) {
+    if (!dev_ptr || !handle) return fail(DPRT_E_USAGE, "null IPC argument");
+    int rc = bind(device);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaIpcGetMemHandle");
+        return DPRT_E_TRANSPORT;
+    }
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    memcpy(handle, &h, 64);
+    return DPRT_OK;
+}
+
+int dprt_ipc_open(int device, const uint8_t handle[64], void** out_ptr) {
+    if (!handle || !out_ptr) return fail(DPRT_E_USAGE, "null IPC argument");
+    int rc = bind(device);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    cudaError_t e = cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaIpcOpenMemHandle");
+        return DPRT_E_TRANSPORT;
+    }
+    return DPRT_OK;
+}
+
+int dprt_ipc_close(int device, void* ptr) {
+    int rc = bind(device);
+    if (rc) return rc;
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaIpcCloseMemHandle");
+        return DPRT_E_TRANSPORT;
+    }
+    return DPRT_OK;
+}
+
+int dprt_enable_peer(int device, int peer) {
+    int rc = bind(device);
+    if (rc) return rc;
+    int can = 0;
+    CK(cudaDeviceCanAccessPeer(&can, device, peer), "cudaDeviceCanAccessPeer");
+    if (!can) return fail(DPRT_E_TRANSPORT, "device %d cannot access peer %d", device, peer);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    cudaGetLastError();
+    return DPRT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// Shared definitions for the sm_100a kernels of libdprt_cuda.so (see include/dprt_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dprt_cuda.h"
+
+namespace dprt {
+
+constexpr int kMacro = 8;          // macrocell edge in cells (empty-space skipping granularity)
+constexpr int kMacroShift = 3;
+constexpr int kTileX = 16;         // marcher CTA screen tile: 16 x 16 pixels, warps are 8 x 4 pixel tiles
+constexpr int kTileY = 16;
+constexpr int kMaxTf = 1024;       // transfer-function entries held in shared memory
+
+struct DeviceBrick {
+    int device;
+    DprtBrickDesc desc;
+    int64_t s_lo[3];   // first stored voxel (global index)
+    int64_t sd[3];     // stored voxel dims
+    float* vox;        // sd[0]*sd[1]*sd[2] f32, x fastest
+    int64_t mcd[3];    // macrocell grid dims
+    float2* macro;     // per macrocell (min, max) over its dilated voxel range
+};
+
+// Everything the marcher needs, by value (kernel parameter space).
+struct MarchArgs {
+    // camera (f64, host-evaluated basis)
+    double o[3], f[3], r[3], u[3];
+    double half_w, half_h;
+    // owned box in world space, field origin and spacing (f64, exact ray setup)
+    double blo[3], bhi[3];
+    double origin[3], spacing[3];
+    double dt;
+    // f32 march state
+    float inv_spacing[3];
+    double stored_lo_d[3];  // s_lo (local coordinate shift)
+    int clo[3], chi[3];    // local clamp range of the cell index
+    int sd[3];
+    long long sy, sz;      // voxel strides
+    const float* __restrict__ vox;
+    const float2* __restrict__ macro;
+    int mcd[3];
+    int skip;
+    // transfer function
+    const float4* __restrict__ tf;
+    int n_tf;
+    float vmin, tf_scale, ert;
+    // output
+    float4* __restrict__ out;
+    uint32_t* __restrict__ samples;
+    int W, H;
+    int rect[4];
+};
+
+struct CompositeArgs {
+    const float4* in[DPRT_MAX_PARTS];
+    int P;
+    long long npix;
+    float bg[3];
+    int flags;
+    uint8_t* rgb8;
+    float4* rgba;
+};
+
+}  // namespace dprt

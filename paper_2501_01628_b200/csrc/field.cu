@@ -1,0 +1,88 @@
+// Brick storage kernels: synthetic field generation and the macrocell min/max grid.
+//
+// The generator evaluates the blob mixture of DESIGN.md §2.2 in float64 with explicitly rounded ops in
+// the same order as oracle/dvr_oracle.c (field_value), so GPU voxels are bit-identical to the CPU ones --
+// the device-side counterpart of the reference's seeded, bit-reproducible scene generator
+// (pkg/src/dprt/scene.py:250-289: "identical seeds give bit-identical scenes").
+
+#include "common.cuh"
+
+namespace dprt {
+
+struct GenArgs {
+    long long N[3];
+    long long s_lo[3];
+    long long sd[3];
+    int nb;
+    double blobs[DPRT_MAX_BLOBS * 5];
+};
+
+__global__ void generate_kernel(const GenArgs g, float* __restrict__ out) {
+    const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long y = blockIdx.y;
+    const long long z = blockIdx.z;
+    if (x >= g.sd[0]) return;
+    const long long i = g.s_lo[0] + x, j = g.s_lo[1] + y, k = g.s_lo[2] + z;
+    const double ux = g.N[0] > 1 ? __ddiv_rn((double)i, (double)(g.N[0] - 1)) : 0.0;
+    const double uy = g.N[1] > 1 ? __ddiv_rn((double)j, (double)(g.N[1] - 1)) : 0.0;
+    const double uz = g.N[2] > 1 ? __ddiv_rn((double)k, (double)(g.N[2] - 1)) : 0.0;
+    double f = 0.0;
+    for (int b = 0; b < g.nb; ++b) {
+        const double* p = g.blobs + 5 * b;
+        const double dx = __dsub_rn(ux, p[0]), dy = __dsub_rn(uy, p[1]), dz = __dsub_rn(uz, p[2]);
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        const double q = __dsub_rn(1.0, __dmul_rn(r2, p[3]));
+        if (q > 0.0) f = __dadd_rn(f, __dmul_rn(p[4], __dmul_rn(__dmul_rn(q, q), q)));
+    }
+    if (f > 1.0) f = 1.0;
+    out[(z * g.sd[1] + y) * g.sd[0] + x] = __double2float_rn(f);
+}
+
+cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cudaStream_t stream) {
+    GenArgs g;
+    for (int a = 0; a < 3; ++a) {
+        g.N[a] = b.desc.dims[a];
+        g.s_lo[a] = b.s_lo[a];
+        g.sd[a] = b.sd[a];
+    }
+    g.nb = spec.n_blobs;
+    for (int i = 0; i < 5 * spec.n_blobs; ++i) g.blobs[i] = spec.blobs[i];
+    dim3 block(256);
+    dim3 grid((unsigned)((b.sd[0] + 255) / 256), (unsigned)b.sd[1], (unsigned)b.sd[2]);
+    generate_kernel<<<grid, block, 0, stream>>>(g, b.vox);
+    return cudaGetLastError();
+}
+
+// Macrocell m covers local cells [8m, 8m + 8) per axis, i.e. voxels [8m, 8m + 8]; its (min, max) is
+// taken over the 1-voxel dilation [8m - 1, 8m + 9] so that samples whose f32 position rounds across a
+// macrocell face are still bounded by it (skipping is exact, not approximate).
+__global__ void macrocell_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
+                                 int mc0, int mc1, int mc2, float2* __restrict__ macro) {
+    const int mx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int my = blockIdx.y, mz = blockIdx.z;
+    if (mx >= mc0) return;
+    const long long x0 = max(0LL, (long long)mx * kMacro - 1), x1 = min(sd0 - 1, (long long)mx * kMacro + kMacro + 1);
+    const long long y0 = max(0LL, (long long)my * kMacro - 1), y1 = min(sd1 - 1, (long long)my * kMacro + kMacro + 1);
+    const long long z0 = max(0LL, (long long)mz * kMacro - 1), z1 = min(sd2 - 1, (long long)mz * kMacro + kMacro + 1);
+    float lo = INFINITY, hi = -INFINITY;
+    for (long long z = z0; z <= z1; ++z)
+        for (long long y = y0; y <= y1; ++y) {
+            const float* row = vox + (z * sd1 + y) * sd0;
+            for (long long x = x0; x <= x1; ++x) {
+                const float v = __ldg(row + x);
+                lo = fminf(lo, v);
+                hi = fmaxf(hi, v);
+            }
+        }
+    macro[((long long)mz * mc1 + my) * mc0 + mx] = make_float2(lo, hi);
+}
+
+cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream) {
+    dim3 block(64);
+    dim3 grid((unsigned)((b.mcd[0] + 63) / 64), (unsigned)b.mcd[1], (unsigned)b.mcd[2]);
+    macrocell_kernel<<<grid, block, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], (int)b.mcd[0], (int)b.mcd[1],
+                                                 (int)b.mcd[2], b.macro);
+    return cudaGetLastError();
+}
+
+}  // namespace dprt

@@ -1,0 +1,232 @@
+"""Torch-facing wrappers of the C ABI: device bricks, the marcher and the compositor kernel.
+
+PyTorch is plumbing here: it owns the device buffers (partials, TF table, frames) and supplies the
+current stream; all compute is in libdprt_cuda.so.  Every call checks its status code and raises the
+reference's exception classes (errors.py); there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import UsageError
+from .geom import CameraSpec
+from .volume import BrickDesc, FieldSpec, TransferFunction1D
+
+
+def _stream(device: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype) -> None:
+    if not t.is_cuda:
+        raise UsageError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise UsageError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise UsageError(f"{name} must be contiguous")
+
+
+def camera_struct(cam: CameraSpec) -> _lib.Camera:
+    """Host-evaluated basis and film half extents (geom.py:163-168, 250-251)."""
+    f, r, u = cam.basis()
+    half_w, half_h = cam.film_half_extents()
+    c = _lib.Camera()
+    c.pos[:] = [float(v) for v in cam.position]
+    c.fwd[:] = list(f)
+    c.right[:] = list(r)
+    c.up[:] = list(u)
+    c.half_w = half_w
+    c.half_h = half_h
+    return c
+
+
+class DeviceBrick:
+    """A rank's brick resident in HBM (stored voxels incl. ghost + macrocell min/max grid).
+
+    Lifetime mirrors the reference's RefCounted objects (refcount.py:10-63): ``close()`` releases the
+    native handle; using a closed brick raises UsageError."""
+
+    def __init__(self, desc: BrickDesc, device: torch.device):
+        if device.type != "cuda":
+            raise UsageError("DeviceBrick needs a CUDA device")
+        self.desc = desc
+        self.device = device
+        self.index = device.index if device.index is not None else torch.cuda.current_device()
+        d = _lib.BrickDesc()
+        d.dims[:] = list(desc.dims)
+        d.lo[:] = list(desc.lo)
+        d.hi[:] = list(desc.hi)
+        d.ghost = desc.ghost
+        d.origin[:] = [float(v) for v in desc.origin]
+        d.spacing[:] = [float(v) for v in desc.spacing]
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().dprt_brick_create(self.index, ctypes.byref(d), ctypes.byref(h)), "dprt_brick_create")
+        self._h = h
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._h is None:
+            raise UsageError("brick was released")
+        return self._h
+
+    def generate(self, f: FieldSpec) -> "DeviceBrick":
+        if tuple(f.dims) != tuple(self.desc.dims):
+            raise UsageError(f"field dims {f.dims} != brick grid {self.desc.dims}")
+        blobs = np.ascontiguousarray(f.blobs, np.float64)
+        spec = _lib.FieldSpec(0, blobs.shape[0], ctypes.c_void_p(blobs.ctypes.data))
+        _lib.check(_lib.lib().dprt_brick_generate(self.handle, ctypes.byref(spec), _stream(self.device)),
+                   "dprt_brick_generate")
+        return self
+
+    def upload(self, voxels) -> "DeviceBrick":
+        """Stored voxels (z, y, x) from a host numpy array or a device tensor."""
+        shape = tuple(reversed(self.desc.stored_dims))
+        if isinstance(voxels, torch.Tensor):
+            if tuple(voxels.shape) != shape:
+                raise UsageError(f"voxel tensor {tuple(voxels.shape)} != stored {shape}")
+            if voxels.is_cuda:
+                _require_cuda(voxels, "voxels", torch.float32)
+                rc = _lib.lib().dprt_brick_upload(self.handle, ctypes.c_void_p(voxels.data_ptr()), 1, _stream(self.device))
+                _lib.check(rc, "dprt_brick_upload")
+                return self
+            voxels = voxels.numpy()
+        arr = np.ascontiguousarray(voxels, np.float32)
+        if arr.shape != shape:
+            raise UsageError(f"voxel array {arr.shape} != stored {shape}")
+        rc = _lib.lib().dprt_brick_upload(self.handle, ctypes.c_void_p(arr.ctypes.data), 0, _stream(self.device))
+        _lib.check(rc, "dprt_brick_upload")
+        torch.cuda.current_stream(self.device).synchronize()  # host array must outlive the copy
+        return self
+
+    def download(self) -> np.ndarray:
+        out = np.empty(tuple(reversed(self.desc.stored_dims)), np.float32)
+        rc = _lib.lib().dprt_brick_download(self.handle, ctypes.c_void_p(out.ctypes.data), 0, _stream(self.device))
+        _lib.check(rc, "dprt_brick_download")
+        return out
+
+    def footprint(self, cam: CameraSpec, width: int, height: int):
+        rect = (ctypes.c_int32 * 4)()
+        c = camera_struct(cam)
+        _lib.check(_lib.lib().dprt_brick_footprint(self.handle, ctypes.byref(c), width, height, rect),
+                   "dprt_brick_footprint")
+        return tuple(rect)
+
+    def close(self) -> None:
+        if self._h is not None:
+            _lib.check(_lib.lib().dprt_brick_destroy(self._h), "dprt_brick_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+class DeviceTF:
+    """A transfer function table resident on one device (4 KiB for 256 entries)."""
+
+    def __init__(self, tf: TransferFunction1D, device: torch.device):
+        self.tf = tf
+        self.table = torch.from_numpy(tf.as_f32().reshape(-1)).to(device)
+
+    def params(self, dt: float, ert: float, flags: int = 0) -> _lib.MarchParams:
+        return _lib.MarchParams(ctypes.c_void_p(self.table.data_ptr()), self.tf.n, flags, float(self.tf.vmin),
+                                float(self.tf.vmax), float(dt), float(ert))
+
+
+def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, partial: torch.Tensor,
+          width: int, height: int, samples: Optional[torch.Tensor] = None, skip: bool = True,
+          footprint: bool = True) -> None:
+    """dprt_march: the brick's full-frame premultiplied RGBA partial into ``partial`` (H*W*4 f32)."""
+    _require_cuda(partial, "partial", torch.float32)
+    if partial.numel() != width * height * 4:
+        raise UsageError(f"partial holds {partial.numel()} floats, need {width * height * 4}")
+    sp = ctypes.c_void_p(0)
+    if samples is not None:
+        _require_cuda(samples, "samples", torch.int32)
+        if samples.numel() != width * height:
+            raise UsageError("samples buffer must hold one count per pixel")
+        sp = ctypes.c_void_p(samples.data_ptr())
+    flags = (0 if skip else _lib.MARCH_NO_SKIP) | (0 if footprint else _lib.MARCH_FULL_FRAME)
+    p = tf.params(dt, ert, flags)
+    c = camera_struct(cam)
+    rc = _lib.lib().dprt_march(brick.handle, ctypes.byref(c), ctypes.byref(p), ctypes.c_void_p(partial.data_ptr()),
+                               sp, width, height, _stream(brick.device))
+    _lib.check(rc, "dprt_march")
+
+
+def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[torch.Tensor] = None,
+              rgba: Optional[torch.Tensor] = None) -> None:
+    """dprt_composite: front-to-back 'over' of equally sized RGBA fragments (already in visibility
+    order); writes tone-mapped RGB8 (needs ``background``) and/or the blended RGBA."""
+    if not frags:
+        raise UsageError("nothing to composite")
+    n = frags[0].numel()
+    if n % 4:
+        raise UsageError("fragments must hold whole RGBA pixels")
+    for i, f in enumerate(frags):
+        _require_cuda(f, f"fragment {i}", torch.float32)
+        if f.numel() != n:
+            raise UsageError("fragments differ in size")
+    npix = n // 4
+    flags = 0
+    bg_arr = None
+    rgb_ptr = ctypes.c_void_p(0)
+    rgba_ptr = ctypes.c_void_p(0)
+    if rgb8 is not None:
+        _require_cuda(rgb8, "rgb8", torch.uint8)
+        if rgb8.numel() != npix * 3:
+            raise UsageError("rgb8 output must hold 3 bytes per pixel")
+        if background is None:
+            raise UsageError("tone mapping needs a background colour")
+        flags |= _lib.COMPOSITE_TONEMAP
+        rgb_ptr = ctypes.c_void_p(rgb8.data_ptr())
+    if background is not None:
+        bg_arr = (ctypes.c_float * 3)(*[float(c) for c in background])
+    if rgba is not None:
+        _require_cuda(rgba, "rgba", torch.float32)
+        if rgba.numel() != n:
+            raise UsageError("rgba output must match the fragments")
+        flags |= _lib.COMPOSITE_RGBA
+        rgba_ptr = ctypes.c_void_p(rgba.data_ptr())
+    ptrs = (ctypes.c_void_p * len(frags))(*[f.data_ptr() for f in frags])
+    dev = frags[0].device
+    rc = _lib.lib().dprt_composite(dev.index if dev.index is not None else torch.cuda.current_device(), ptrs,
+                                   len(frags), npix, bg_arr, flags, rgb_ptr, rgba_ptr, _stream(dev))
+    _lib.check(rc, "dprt_composite")
+
+
+def composite_ptrs(device_index: int, ptrs: Sequence[int], npix: int, background, rgb8_ptr: int = 0,
+                   rgba_ptr: int = 0, stream: Optional[int] = None) -> None:
+    """Raw-pointer form for peer (IPC-mapped) fragments and outputs: the fused NVLink compositor."""
+    flags = (_lib.COMPOSITE_TONEMAP if rgb8_ptr else 0) | (_lib.COMPOSITE_RGBA if rgba_ptr else 0)
+    bg_arr = (ctypes.c_float * 3)(*[float(c) for c in background]) if background is not None else None
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    s = ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream(device_index).cuda_stream)
+    rc = _lib.lib().dprt_composite(device_index, arr, len(ptrs), npix, bg_arr, flags, ctypes.c_void_p(rgb8_ptr),
+                                   ctypes.c_void_p(rgba_ptr), s)
+    _lib.check(rc, "dprt_composite")
+
+
+def ipc_handle(device_index: int, ptr: int) -> bytes:
+    buf = (ctypes.c_uint8 * 64)()
+    _lib.check(_lib.lib().dprt_ipc_handle(device_index, ctypes.c_void_p(ptr), buf), "dprt_ipc_handle")
+    return bytes(buf)
+
+
+def ipc_open(device_index: int, handle: bytes) -> int:
+    buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    out = ctypes.c_void_p()
+    _lib.check(_lib.lib().dprt_ipc_open(device_index, buf, ctypes.byref(out)), "dprt_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(device_index: int, ptr: int) -> None:
+    _lib.check(_lib.lib().dprt_ipc_close(device_index, ctypes.c_void_p(ptr)), "dprt_ipc_close")

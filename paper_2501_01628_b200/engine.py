@@ -1,0 +1,201 @@
+"""Per-rank sort-last DVR frame driver: march this rank's brick, composite in visibility order, gather.
+
+Counterpart of the reference's wavefront driver (pkg/src/dprt/engine.py): ``render_volume_with``
+replaces ``render_with`` (engine.py:459-488) and ``render_volume_frame`` replaces ``render_frame``
+(engine.py:491-497).  The collective contract is unchanged: the render digest is verified on every rank
+before any GPU work (engine.py:410-440), pixel ownership is ``assign_pixels``' row blocks
+(engine.py:216-221), the frame lands on rank 0, and ``tone_map_rgb8`` is the same formula
+(engine.py:500-502) -- fused into the last compositing kernel.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import device as dev
+from .compositor import Compositor
+from .errors import ContractError, UsageError
+from .geom import CameraSpec, Vec3
+from .transport import RankEndpoint
+from .volume import Decomposition, TransferFunction1D, visibility_order
+
+COMPOSITE_MODES = ("auto", "direct_send", "binary_swap", "p2p")
+
+# Distinct colours for rank-ownership visualisation, one per rank modulo 8 (engine.py:41-44).
+RANK_PALETTE = np.array([
+    (0.90, 0.15, 0.15), (0.15, 0.55, 0.90), (0.95, 0.75, 0.10), (0.15, 0.80, 0.35),
+    (0.60, 0.30, 0.85), (0.95, 0.45, 0.10), (0.20, 0.25, 0.95), (0.80, 0.80, 0.80),
+], dtype=np.float64)
+
+
+def assign_pixels(width: int, height: int, num_ranks: int) -> List[Tuple[int, int]]:
+    """Row blocks: rank r owns rows [r*H//R, (r+1)*H//R) (engine.py:216-221)."""
+    if num_ranks < 1:
+        raise ValueError(f"num_ranks must be >= 1, got {num_ranks}")
+    return [(r * height // num_ranks, (r + 1) * height // num_ranks) for r in range(num_ranks)]
+
+
+def tone_map_rgb8(image: np.ndarray) -> np.ndarray:
+    """Host twin of the fused device tone map: clamp to [0, 1], quantize half up (engine.py:500-502)."""
+    return np.floor(np.clip(image, 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+
+
+@dataclass(frozen=True)
+class RenderOptions:
+    """DVR render options (the reference's RenderOptions, engine.py:167-174, re-scoped to volumes)."""
+
+    dt: float = 1.0                    # lattice spacing along the ray, world units
+    ert: float = 0.99                  # early ray termination threshold (per brick)
+    composite: str = "auto"            # auto | direct_send | binary_swap | p2p
+    skip_empty: bool = True            # exact empty-space skipping
+    disable_compositing: bool = False  # debug: root shows only its own brick (negative test, engine.py:172)
+    frame_index: int = 0
+    keep_float: bool = False           # also return the float RGB image before quantisation (rank 0)
+    collect_samples: bool = False      # also return per-pixel owned sample counts (this rank)
+
+
+@dataclass
+class RankStats:
+    """Per-rank counters plus line records in the reference's schema (engine.py:177-193)."""
+
+    samples: int = 0
+    bytes_exchanged: int = 0
+    rounds: int = 0
+    records: List[str] = field(default_factory=list)
+
+    def record(self, frame: int, rays: int, nbytes: int, millis: float, **extra) -> None:
+        tail = "".join(f" {k}={v}" for k, v in extra.items())
+        self.records.append(f"frame={frame} round={self.rounds} raysTraced={rays} "
+                            f"bytesExchanged={nbytes} millis={millis:.3f}{tail}")
+        self.rounds += 1
+
+
+@dataclass
+class RenderResult:
+    rgb8: Optional[torch.Tensor]          # rank 0: (H, W, 3) uint8 on the device; None elsewhere
+    stats: RankStats
+    image: Optional[np.ndarray] = None    # rank 0 with keep_float: (H, W, 3) float64
+    samples: Optional[torch.Tensor] = None  # with collect_samples: (H, W) int32, this rank's brick
+    partial: Optional[torch.Tensor] = None  # this rank's RGBA partial (H, W, 4) f32 (device)
+    order: Optional[List[int]] = None
+
+
+def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptions, tf: TransferFunction1D,
+                  background: Vec3, decomposition: Decomposition) -> bytes:
+    """sha256 of every collective render parameter (engine.py:410-424), extended with the transfer
+    function bytes, lattice, ERT, field geometry, brick table and composite mode."""
+    f = decomposition.field
+    doc = {
+        "cam": [list(cam.position), list(cam.view_dir), list(cam.up), cam.fov_y, cam.aspect],
+        "size": [width, height],
+        "dt": options.dt, "ert": options.ert, "composite": options.composite,
+        "skip": options.skip_empty, "disableCompositing": options.disable_compositing,
+        "tf": [hashlib.sha256(tf.as_f32().tobytes()).hexdigest(), tf.vmin, tf.vmax],
+        "field": [list(f.dims), list(f.origin), list(f.spacing)],
+        "bricks": [[list(lo), list(hi)] for lo, hi in decomposition.boxes],
+        "background": list(background),
+    }
+    return hashlib.sha256(json.dumps(doc, separators=(",", ":")).encode("utf-8")).digest()
+
+
+def verify_collective_digest(ep: RankEndpoint, digest: bytes) -> None:
+    """Fail on every rank, before any GPU work, if digests diverge (engine.py:427-440)."""
+    root_digest = ep.broadcast_from_root(digest if ep.rank == 0 else None)
+    votes = ep.gather_to_root(b"\x01" if root_digest == digest else b"\x00")
+    verdict = json.dumps([r for r, v in enumerate(votes) if v != b"\x01"]).encode() if ep.rank == 0 else None
+    bad = json.loads(ep.broadcast_from_root(verdict))
+    if bad:
+        raise ContractError(f"collective render parameters diverge from rank 0 on ranks {bad}")
+
+
+class VolumeRenderer:
+    """Per-rank state that persists across frames: device TF, partial buffer, compositor scratch.
+
+    One instance per rank/GPU.  ``render`` is the collective frame (all ranks call it in the same
+    order with the same committed parameters)."""
+
+    def __init__(self, ep: RankEndpoint, brick: dev.DeviceBrick, decomposition: Decomposition,
+                 tf: TransferFunction1D, background: Vec3 = (0.0, 0.0, 0.0)):
+        if decomposition.P != ep.R:
+            raise UsageError(f"decomposition has {decomposition.P} bricks for {ep.R} ranks")
+        self.ep = ep
+        self.brick = brick
+        self.decomposition = decomposition
+        self.device = brick.device
+        self.set_tf(tf)
+        self.background = tuple(float(c) for c in background)
+        self._size = None
+        self.partial = None
+        self.samples = None
+        self.compositor: Optional[Compositor] = None
+
+    def set_tf(self, tf: TransferFunction1D) -> None:
+        self.tf = tf
+        self.dtf = dev.DeviceTF(tf, self.brick.device)
+
+    def _ensure(self, width: int, height: int, mode: str) -> None:
+        if self._size != (width, height):
+            self.partial = torch.empty(height * width * 4, dtype=torch.float32, device=self.device)
+            self.samples = torch.empty(height * width, dtype=torch.int32, device=self.device)
+            self.compositor = None
+            self._size = (width, height)
+        if self.compositor is None or self.compositor.mode_requested != mode:
+            self.compositor = Compositor(self.ep, width, height, mode, self.device)
+
+    def render(self, cam: CameraSpec, width: int, height: int, options: RenderOptions = RenderOptions(),
+               verify: bool = True) -> RenderResult:
+        if options.composite not in COMPOSITE_MODES:
+            raise UsageError(f"unknown composite mode {options.composite!r}; choose from {COMPOSITE_MODES}")
+        stats = RankStats()
+        if verify:
+            verify_collective_digest(self.ep, render_digest(cam, width, height, options, self.tf,
+                                                            self.background, self.decomposition))
+        self._ensure(width, height, options.composite)
+        order = visibility_order(self.decomposition, cam.position)
+        t0 = time.perf_counter()
+        dev.march(self.brick, cam, self.dtf, options.dt, options.ert, self.partial, width, height,
+                  samples=self.samples if options.collect_samples else None, skip=options.skip_empty)
+        if options.disable_compositing:
+            order = [self.ep.rank] if self.ep.R == 1 else order
+        out = self.compositor.composite(self.partial, order, self.background,
+                                        keep_float=options.keep_float, solo=options.disable_compositing)
+        nbytes = self.compositor.last_bytes
+        stats.bytes_exchanged += nbytes
+        stats.record(options.frame_index, width * height, nbytes, (time.perf_counter() - t0) * 1e3)
+        res = RenderResult(rgb8=out.rgb8, stats=stats, order=order,
+                           partial=self.partial.view(height, width, 4))
+        if options.keep_float and out.rgba is not None:
+            rgba = out.rgba.view(height, width, 4).double().cpu().numpy()
+            bg = np.asarray(self.background, np.float64)
+            res.image = rgba[..., :3] + (1.0 - rgba[..., 3:4]) * bg
+        if options.collect_samples:
+            res.samples = self.samples.view(height, width)
+        return res
+
+
+def render_volume_with(ep: RankEndpoint, brick: dev.DeviceBrick, decomposition: Decomposition,
+                       tf: TransferFunction1D, cam: CameraSpec, width: int, height: int,
+                       options: RenderOptions = RenderOptions(), background: Vec3 = (0.0, 0.0, 0.0)) -> RenderResult:
+    """Collective render given this rank's resident brick (the render_with slot, engine.py:459-488)."""
+    return VolumeRenderer(ep, brick, decomposition, tf, background).render(cam, width, height, options)
+
+
+def render_volume_frame(ep: RankEndpoint, decomposition: Decomposition, tf: TransferFunction1D,
+                        cam: CameraSpec, width: int, height: int, options: RenderOptions = RenderOptions(),
+                        background: Vec3 = (0.0, 0.0, 0.0), ghost: int = 1) -> RenderResult:
+    """Collective render of a decomposed synthetic field (the render_frame slot, engine.py:491-497):
+    each rank generates its own brick on its GPU, then renders."""
+    device = ep.device if ep.device.type == "cuda" else torch.device("cuda", torch.cuda.current_device())
+    brick = dev.DeviceBrick(decomposition.brick(ep.rank, ghost), device).generate(decomposition.field)
+    try:
+        return render_volume_with(ep, brick, decomposition, tf, cam, width, height, options, background)
+    finally:
+        torch.cuda.current_stream(device).synchronize()
+        brick.close()

@@ -1,0 +1,239 @@
+"""Rank endpoints: the reference's collective API shape over one-process-per-GPU ``torch.distributed``.
+
+The reference runs R ranks as threads of one process and moves bytes over queues or loopback TCP
+(pkg/src/dprt/transport.py:1-8, 164-204, 254-420) with four collectives: ``ring_exchange``,
+``gather_to_root``, ``broadcast_from_root``, ``barrier`` (transport.py:457-507).  Here each rank is a
+process bound to one GPU; the same four collectives form the host CONTROL plane (digest votes, tiny
+metadata) and carry the reference's per-(channel, kind) sequence check (transport.py:129-140) so that
+mismatched collective calls still raise ``ProtocolError``.  Image fragments use the DATA plane:
+``exchange`` posts grouped point-to-point sends/receives of device tensors (NCCL over NVLink on
+B200, gloo on CPU for tests), and ``device_barrier`` is a stream-ordered all-reduce used to order
+peer-memory (P2P) access without a host synchronisation.
+"""
+
+from __future__ import annotations
+
+import os
+import pickle
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .errors import ProtocolError, TransportError
+
+DEFAULT_TIMEOUT_SECS = 30.0
+
+
+def resolve_timeout(explicit: Optional[float] = None) -> float:
+    """Explicit value, else DPRT_TIMEOUT_SECS, else 30 s (transport.py:32-39)."""
+    if explicit is not None:
+        return float(explicit)
+    env = os.environ.get("DPRT_TIMEOUT_SECS")
+    return float(env) if env else DEFAULT_TIMEOUT_SECS
+
+
+@dataclass
+class TransportStats:
+    """Byte / message counters (transport.py:49-57); ``device_bytes_*`` count data-plane tensors."""
+
+    bytes_sent: int = 0
+    bytes_received: int = 0
+    messages_sent: int = 0
+    messages_received: int = 0
+    device_bytes_sent: int = 0
+    device_bytes_received: int = 0
+
+    def traffic(self) -> int:
+        return self.bytes_sent + self.bytes_received
+
+
+class RankEndpoint:
+    """One rank's handle; driven by a single thread.  Subclasses provide the byte transport."""
+
+    def __init__(self, rank: int, num_ranks: int, device: Optional[torch.device] = None):
+        if not (0 <= rank < num_ranks):
+            raise TransportError(f"rank {rank} outside [0, {num_ranks})")
+        self.rank = rank
+        self.R = num_ranks
+        self.device = device if device is not None else torch.device("cpu")
+        self.stats = TransportStats()
+        self._seq: Dict[str, int] = {}
+
+    # -- sequence tagging: every control message carries (kind, seq) like transport.py:101-143
+    def _tag(self, kind: str) -> Tuple[str, int]:
+        seq = self._seq.get(kind, 0)
+        self._seq[kind] = seq + 1
+        return kind, seq
+
+    def _check(self, tag: Tuple[str, int], got, src: int):
+        kind, seq = tag
+        if not (isinstance(got, tuple) and len(got) == 3):
+            raise ProtocolError(f"rank {self.rank}: malformed control message from rank {src}")
+        gkind, gseq, payload = got
+        if gkind != kind:
+            raise ProtocolError(f"rank {self.rank}: expected {kind} from rank {src}, got {gkind}; "
+                                "collective calls are mismatched")
+        if gseq != seq:
+            raise ProtocolError(f"rank {self.rank}: sequence {gseq} from rank {src} for {kind}, expected {seq}")
+        return payload
+
+    # -- control plane (bytes), same signatures as transport.py:457-507
+    def gather_to_root(self, tile: bytes) -> List[bytes]:
+        raise NotImplementedError
+
+    def broadcast_from_root(self, payload: Optional[bytes]) -> bytes:
+        raise NotImplementedError
+
+    def barrier(self) -> None:
+        raise NotImplementedError
+
+    def ring_exchange(self, outgoing: bytes) -> bytes:
+        raise NotImplementedError
+
+    # -- data plane (device tensors)
+    def exchange(self, sends: Sequence[Tuple[int, torch.Tensor]], recvs: Sequence[Tuple[int, torch.Tensor]]) -> None:
+        raise NotImplementedError
+
+    def device_barrier(self) -> None:
+        raise NotImplementedError
+
+    def all_gather_bytes(self, payload: bytes) -> List[bytes]:
+        """gather_to_root + broadcast_from_root, the reference's all-gather idiom (api.py:284-293)."""
+        tiles = self.gather_to_root(payload)
+        blob = pickle.dumps(tiles) if self.rank == 0 else None
+        return pickle.loads(self.broadcast_from_root(blob))
+
+    def close(self) -> None:
+        pass
+
+
+class SoloEndpoint(RankEndpoint):
+    """R == 1: every collective is the identity (transport.py:459-460, 467-468, 482-484, 499-500)."""
+
+    def __init__(self, device: Optional[torch.device] = None):
+        super().__init__(0, 1, device)
+
+    def gather_to_root(self, tile: bytes) -> List[bytes]:
+        return [tile]
+
+    def broadcast_from_root(self, payload: Optional[bytes]) -> bytes:
+        if payload is None:
+            raise TransportError("rank 0 must supply the broadcast payload")
+        return payload
+
+    def barrier(self) -> None:
+        return None
+
+    def ring_exchange(self, outgoing: bytes) -> bytes:
+        return outgoing
+
+    def exchange(self, sends, recvs) -> None:
+        if sends or recvs:
+            raise TransportError("a single rank has no peers to exchange with")
+
+    def device_barrier(self) -> None:
+        return None
+
+
+class DistEndpoint(RankEndpoint):
+    """torch.distributed process group (NCCL on GPUs, gloo on CPU).  One process per rank/GPU."""
+
+    def __init__(self, group=None, device: Optional[torch.device] = None):
+        if not dist.is_initialized():
+            raise TransportError("torch.distributed is not initialised; call init_dist() first")
+        super().__init__(dist.get_rank(group), dist.get_world_size(group), device)
+        self.group = group
+        self.backend = dist.get_backend(group)
+        self._token = None
+
+    def _obj_device(self):
+        return self.device if self.backend == "nccl" else None
+
+    def gather_to_root(self, tile: bytes) -> List[bytes]:
+        tag = self._tag("TILE")
+        msg = (tag[0], tag[1], tile)
+        out = [None] * self.R if self.rank == 0 else None
+        try:
+            dist.gather_object(msg, out, dst=0, group=self.group)
+        except Exception as exc:  # noqa: BLE001
+            raise TransportError(f"rank {self.rank}: gather_to_root failed: {exc}") from exc
+        self.stats.messages_sent += 1
+        self.stats.bytes_sent += len(tile)
+        if self.rank != 0:
+            return []
+        res = [self._check(tag, m, src) for src, m in enumerate(out)]
+        self.stats.messages_received += self.R - 1
+        self.stats.bytes_received += sum(len(t) for t in res[1:])
+        return res
+
+    def broadcast_from_root(self, payload: Optional[bytes]) -> bytes:
+        tag = self._tag("CONTROL")
+        if self.rank == 0 and payload is None:
+            raise TransportError("rank 0 must supply the broadcast payload")
+        box = [(tag[0], tag[1], payload) if self.rank == 0 else None]
+        try:
+            dist.broadcast_object_list(box, src=0, group=self.group, device=self._obj_device())
+        except Exception as exc:  # noqa: BLE001
+            raise TransportError(f"rank {self.rank}: broadcast_from_root failed: {exc}") from exc
+        data = self._check(tag, box[0], 0)
+        if self.rank != 0:
+            self.stats.messages_received += 1
+            self.stats.bytes_received += len(data)
+        return data
+
+    def barrier(self) -> None:
+        self.gather_to_root(b"")
+        self.broadcast_from_root(b"" if self.rank == 0 else None)
+
+    def ring_exchange(self, outgoing: bytes) -> bytes:
+        allb = self.all_gather_bytes(outgoing)
+        return allb[(self.rank - 1) % self.R]
+
+    def exchange(self, sends, recvs) -> None:
+        ops = []
+        for peer, t in sends:
+            ops.append(dist.P2POp(dist.isend, t, peer, group=self.group))
+            self.stats.device_bytes_sent += t.numel() * t.element_size()
+        for peer, t in recvs:
+            ops.append(dist.P2POp(dist.irecv, t, peer, group=self.group))
+            self.stats.device_bytes_received += t.numel() * t.element_size()
+        if not ops:
+            return
+        try:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        except Exception as exc:  # noqa: BLE001
+            raise TransportError(f"rank {self.rank}: fragment exchange failed: {exc}") from exc
+
+    def device_barrier(self) -> None:
+        if self._token is None:
+            dev = self.device if self.backend == "nccl" else torch.device("cpu")
+            self._token = torch.zeros(1, dtype=torch.int32, device=dev)
+        dist.all_reduce(self._token, group=self.group)
+
+
+def init_dist(backend: Optional[str] = None) -> DistEndpoint:
+    """Initialise the default process group from torchrun's env (RANK, WORLD_SIZE, MASTER_*) and bind
+    this process to cuda:LOCAL_RANK when using NCCL."""
+    if backend is None:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+    device = None
+    if backend == "nccl":
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        device = torch.device("cuda", local)
+    if not dist.is_initialized():
+        kwargs = {}
+        if device is not None:
+            kwargs["device_id"] = device
+        dist.init_process_group(backend, **kwargs)
+    return DistEndpoint(device=device)
+
+
+def endpoint_for(device: Optional[torch.device] = None) -> RankEndpoint:
+    """DistEndpoint under an initialised process group with >1 rank, else SoloEndpoint."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return DistEndpoint(device=device)
+    return SoloEndpoint(device)

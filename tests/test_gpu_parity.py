@@ -1,0 +1,167 @@
+"""GPU parity: the sm_100a data path through the C ABI against the CPU oracle on the same inputs.
+
+Integer / byte work is compared exactly (field voxels, per-pixel owned sample counts, brick ownership,
+visibility order); float RGBA within RGBA_ATOL (tests/scenes.py); RGB8 within 1 LSB.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2501_01628_b200 import device as dev
+from paper_2501_01628_b200.engine import RenderOptions, VolumeRenderer
+from paper_2501_01628_b200.geom import CameraSpec, auto_camera, orbit_camera
+from paper_2501_01628_b200.transport import SoloEndpoint
+from paper_2501_01628_b200.volume import BrickDesc, blob_field, decompose, default_tf
+from scenes import (RGB8_MAX_LSB, RGBA_ATOL, RGBA_MEAN_ATOL, c1, cam_array, dense_tf, oracle_brick,
+                    oracle_partials)
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_partials(dec, cam, tf, dt, ert, W, H, device, skip=True, ghost=1):
+    dtf = dev.DeviceTF(tf, device)
+    parts, samples = [], []
+    for r in range(dec.P):
+        b = dev.DeviceBrick(dec.brick(r, ghost), device).generate(dec.field)
+        p = torch.empty(H * W * 4, dtype=torch.float32, device=device)
+        s = torch.empty(H * W, dtype=torch.int32, device=device)
+        dev.march(b, cam, dtf, dt, ert, p, W, H, samples=s, skip=skip)
+        torch.cuda.synchronize()
+        parts.append(p)
+        samples.append(s)
+        b.close()
+    return parts, samples
+
+
+def _check_rgba(gpu: np.ndarray, ref: np.ndarray, what: str):
+    err = np.abs(gpu.astype(np.float64) - ref)
+    assert err.max() <= RGBA_ATOL, f"{what}: max |dRGBA| {err.max():.3e} > {RGBA_ATOL}"
+    assert err.mean() <= RGBA_MEAN_ATOL, f"{what}: mean |dRGBA| {err.mean():.3e}"
+
+
+def test_field_generation_bit_exact(cuda_device, oracle_lib):
+    f = blob_field((37, 29, 23), seed=5, n_blobs=16)
+    for lo, hi, g in [((0, 0, 0), (36, 28, 22), 0), ((5, 3, 7), (20, 28, 15), 1), ((0, 10, 0), (36, 20, 22), 2)]:
+        desc = BrickDesc(f.dims, lo, hi, g)
+        b = dev.DeviceBrick(desc, cuda_device).generate(f)
+        got = b.download()
+        ref = oracle.generate_field(f.dims, f.blobs, desc.stored_lo, desc.stored_dims)
+        assert np.array_equal(got, ref)
+        b.close()
+
+
+def test_upload_roundtrip(cuda_device):
+    desc = BrickDesc((9, 8, 7), (0, 0, 0), (8, 7, 6), 0)
+    vox = np.random.default_rng(0).random((7, 8, 9)).astype(np.float32)
+    b = dev.DeviceBrick(desc, cuda_device).upload(vox)
+    assert np.array_equal(b.download(), vox)
+    b.close()
+
+
+@pytest.mark.parametrize("skip", [False, True])
+def test_single_brick_matches_oracle(cuda_device, oracle_lib, skip):
+    f = blob_field((48, 40, 44), seed=7)
+    vox = oracle.generate_field(f.dims, f.blobs)
+    dec = decompose(f, 1)
+    W, H = 96, 80
+    for cam, tf, dt, ert in [(auto_camera(f.bounds(), W, H), default_tf(), 1.0, 0.99),
+                             (auto_camera(f.bounds(), W, H), dense_tf(), 0.6, 0.95),
+                             (CameraSpec((24.0, 20.0, 22.0), (0.2, 0.1, -1.0), (0, 1, 0), 80.0, W / H), dense_tf(),
+                              0.8, 0.99)]:
+        ref, rs = oracle_partials(vox, dec, cam, tf, dt, ert, W, H)
+        parts, samples = _gpu_partials(dec, cam, tf, dt, ert, W, H, cuda_device, skip=skip)
+        got = parts[0].view(H, W, 4).cpu().numpy()
+        assert np.array_equal(samples[0].view(H, W).cpu().numpy().astype(np.uint32), rs[0])
+        _check_rgba(got, ref[0], f"single brick skip={skip}")
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_bricks_and_composite_match_oracle(cuda_device, oracle_lib, P):
+    """C1 (64^3, 256^2) at P bricks: per-brick partials, integer-exact sample ownership, exact
+    visibility order, composite kernel vs oracle 'over' (float) and RGB8 within 1 LSB."""
+    s = c1(P=P)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, rs = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H)
+    parts, samples = _gpu_partials(s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H, cuda_device)
+    for r in range(P):
+        assert np.array_equal(samples[r].view(s.H, s.W).cpu().numpy().astype(np.uint32), rs[r])
+        _check_rgba(parts[r].view(s.H, s.W, 4).cpu().numpy(), ref[r], f"brick {r}")
+    order = s.dec.visibility_order(s.cam.position)
+    from scenes import oracle_order
+    assert order == oracle_order(s.dec, s.cam.position)
+    rgb8 = torch.empty(s.H * s.W * 3, dtype=torch.uint8, device=cuda_device)
+    rgba = torch.empty(s.H * s.W * 4, dtype=torch.float32, device=cuda_device)
+    dev.composite([parts[r] for r in order], s.background, rgb8=rgb8, rgba=rgba)
+    torch.cuda.synchronize()
+    img_ref = oracle.composite(ref, order, s.background)
+    blended = rgba.view(s.H, s.W, 4).double().cpu().numpy()
+    img = blended[..., :3] + (1.0 - blended[..., 3:4]) * np.asarray(s.background)
+    assert np.abs(img - img_ref).max() <= RGBA_ATOL
+    q = rgb8.view(s.H, s.W, 3).cpu().numpy().astype(np.int16)
+    assert np.abs(q - oracle.tone_map_rgb8(img_ref).astype(np.int16)).max() <= RGB8_MAX_LSB
+
+
+def test_composite_kernel_random_partials(cuda_device, oracle_lib):
+    """Compositing-only (config 5 style): seeded premultiplied RGBA with alpha <= 0.5, odd pixel count."""
+    rng = np.random.default_rng(11)
+    P, npix = 5, 1000 * 37 + 3
+    a = rng.uniform(0, 0.5, (P, npix, 1))
+    parts = np.concatenate([rng.uniform(0, 1, (P, npix, 3)) * a, a], axis=2).astype(np.float32)
+    order = [3, 0, 4, 1, 2]
+    bg = (0.2, 0.3, 0.4)
+    ts = [torch.from_numpy(parts[i].reshape(-1)).to(cuda_device) for i in range(P)]
+    rgb8 = torch.empty(npix * 3, dtype=torch.uint8, device=cuda_device)
+    rgba = torch.empty(npix * 4, dtype=torch.float32, device=cuda_device)
+    dev.composite([ts[r] for r in order], bg, rgb8=rgb8, rgba=rgba)
+    ref = oracle.composite([parts[i].astype(np.float64) for i in range(P)], order, bg)
+    out = rgba.view(npix, 4).double().cpu().numpy()
+    img = out[:, :3] + (1 - out[:, 3:4]) * np.asarray(bg)
+    assert np.abs(img - ref).max() < 1e-5
+    q = rgb8.view(npix, 3).cpu().numpy().astype(np.int16)
+    assert np.abs(q - oracle.tone_map_rgb8(ref).astype(np.int16)).max() <= 1
+
+
+def test_engine_single_rank_frame(cuda_device, oracle_lib):
+    """The public per-rank driver at R=1 (render_with slot): RGB8 frame + float image vs oracle."""
+    s = c1(P=1, W=160, H=120)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, _ = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H)
+    img_ref = oracle.composite(ref, [0], s.background)
+    brick = dev.DeviceBrick(s.dec.brick(0), cuda_device).generate(s.field)
+    r = VolumeRenderer(SoloEndpoint(cuda_device), brick, s.dec, s.tf, s.background)
+    res = r.render(s.cam, s.W, s.H, RenderOptions(keep_float=True))
+    torch.cuda.synchronize()
+    assert np.abs(res.image - img_ref).max() <= RGBA_ATOL
+    q = res.rgb8.cpu().numpy().astype(np.int16)
+    assert np.abs(q - oracle.tone_map_rgb8(img_ref).astype(np.int16)).max() <= RGB8_MAX_LSB
+    brick.close()
+
+
+def test_orbit_frames_order_and_ownership(cuda_device, oracle_lib):
+    """Config-4 style: uneven anisotropic bricks, orbiting camera; order exact every frame, samples exact."""
+    f = blob_field((72, 40, 24), seed=3, spacing=(1.0, 1.0, 2.0), lopsided=True)
+    vox = oracle.generate_field(f.dims, f.blobs)
+
+    def mass(axis, lo, hi):
+        sub = vox[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] >= np.float32(0.1)
+        return sub.sum(axis=tuple(a for a in range(3) if a != 2 - axis)).astype(np.int64)
+
+    dec = decompose(f, 8, "mass", mass)
+    leaves, nodes = oracle.kd_leaves(f.dims, f.spacing, 8, "mass", field=vox)
+    assert [tuple(map(tuple, l)) for l in leaves] == dec.boxes
+    W, H = 64, 48
+    b = f.bounds()
+    target = b.center()
+    for i in range(6):
+        cam = orbit_camera(target, 1.6 * b.diagonal(), np.radians(60.0 * i), np.radians(20.0), 45.0, W / H)
+        order = dec.visibility_order(cam.position)
+        assert order == oracle.kd_order(nodes, 8, cam.position, f.origin, f.spacing)
+        ref, rs = oracle_partials(vox, dec, cam, dense_tf(), 1.0, 0.99, W, H)
+        parts, samples = _gpu_partials(dec, cam, dense_tf(), 1.0, 0.99, W, H, cuda_device)
+        for r in range(8):
+            assert np.array_equal(samples[r].view(H, W).cpu().numpy().astype(np.uint32), rs[r])
+            _check_rgba(parts[r].view(H, W, 4).cpu().numpy(), ref[r], f"frame {i} brick {r}")
