@@ -218,7 +218,8 @@ def run_ours(args):
     desc = dec.brick(rank)
     brick = dev.DeviceBrick(desc, device).generate(f)
     renderer = VolumeRenderer(ep, brick, dec, tf, BACKGROUND)
-    opts = RenderOptions(dt=DT, ert=ERT, composite=args.composite)
+    skip = not args.no_skip
+    opts = RenderOptions(dt=DT, ert=ERT, composite=args.composite, skip_empty=skip)
     stream = torch.cuda.current_stream(device)
     torch.cuda.synchronize(device)
 
@@ -255,7 +256,7 @@ def run_ours(args):
     barrier()
     for a, b in ev:
         a.record(stream)
-        dev.march(brick, cam, renderer.dtf, DT, ERT, partial, W, H)
+        dev.march(brick, cam, renderer.dtf, DT, ERT, partial, W, H, skip=skip)
         b.record(stream)
     barrier()
     march_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
@@ -315,7 +316,7 @@ def run_ours(args):
             "config": {"workload": "c2: 512^3 f32 blob field (seed 1, 16 blobs), 1 brick per GPU, 1920x1080, "
                                    "dt=1 voxel, ERT 0.99, SURVEY 8(d) TF, auto camera",
                        "field": list(f.dims), "bricks": R, "image": [W, H], "composite": renderer.compositor.mode,
-                       "empty_space_skipping": True, "l2": "inputs larger than L2 (brick 512 MiB/GPU), no flush"},
+                       "empty_space_skipping": skip, "l2": "inputs larger than L2 (brick 512 MiB/GPU), no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "march_kernel", "kernel_ms": march_ms, "algorithmic_bytes": alg_bytes,
@@ -339,6 +340,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--composite", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-skip", action="store_true", help="disable exact empty-space skipping")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
