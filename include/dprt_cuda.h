@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 1
+#define DPRT_ABI_VERSION 2
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -70,7 +70,9 @@ typedef struct DprtFieldSpec {
     const double* blobs;
 } DprtFieldSpec;
 
-/* March parameters.  tf_rgba: DEVICE pointer to n_tf x {r, g, b, a} f32. */
+/* March parameters.  tf_rgba: DEVICE pointer to n_tf x {r, g, b, a} f32.
+ * tf_version: caller-maintained tag of the table contents; the brick caches its TF-dependent skip
+ * distances per tag and rebuilds them when it changes (0 = rebuild every call). */
 typedef struct DprtMarchParams {
     const float* tf_rgba;
     int32_t n_tf;
@@ -79,9 +81,10 @@ typedef struct DprtMarchParams {
     double vmax;
     double dt;
     double ert;
+    uint64_t tf_version;
 } DprtMarchParams;
 
-#define DPRT_MARCH_NO_SKIP 1      /* disable exact empty-space skipping (macrocell min/max grid) */
+#define DPRT_MARCH_NO_SKIP 1      /* disable exact empty-space skipping (macrocell skip distances) */
 #define DPRT_MARCH_FULL_FRAME 2   /* march every pixel instead of the brick's screen footprint */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */

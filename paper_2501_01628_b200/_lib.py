@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -60,7 +60,7 @@ class FieldSpec(ctypes.Structure):
 class MarchParams(ctypes.Structure):
     _fields_ = [("tf_rgba", ctypes.c_void_p), ("n_tf", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("vmin", ctypes.c_double), ("vmax", ctypes.c_double), ("dt", ctypes.c_double),
-                ("ert", ctypes.c_double)]
+                ("ert", ctypes.c_double), ("tf_version", ctypes.c_uint64)]
 
 
 _lib: Optional[ctypes.CDLL] = None

@@ -15,6 +15,7 @@
 
 namespace dprt {
 cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream);
+cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t* tmp, cudaStream_t stream);
 cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cudaStream_t stream);
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream);
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream);
@@ -115,10 +116,18 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     }
     b->vox = nullptr;
     b->macro = nullptr;
+    b->skipd = nullptr;
+    b->skip_tmp = nullptr;
+    b->skip_version = 0;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
+    if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc);
+    if (e == cudaSuccess) e = cudaMalloc(&b->skip_tmp, (size_t)nmc);
     if (e != cudaSuccess) {
-        if (b->vox) cudaFree(b->vox);
+        cudaFree(b->vox);
+        cudaFree(b->macro);
+        cudaFree(b->skipd);
+        cudaFree(b->skip_tmp);
         delete b;
         return cuda_fail(e, "brick allocation");
     }
@@ -142,6 +151,7 @@ int dprt_brick_build_macrocells(DprtBrick* b, void* stream) {
     int rc = bind(b->device);
     if (rc) return rc;
     CK(dprt::launch_macrocells(*b, (cudaStream_t)stream), "macrocell kernel launch");
+    b->skip_version = 0;  // TF-dependent skip distances must be rebuilt from the new min/max grid
     return DPRT_OK;
 }
 
@@ -183,6 +193,8 @@ int dprt_brick_destroy(DprtBrick* b) {
     if (rc) return rc;
     cudaFree(b->vox);
     cudaFree(b->macro);
+    cudaFree(b->skipd);
+    cudaFree(b->skip_tmp);
     delete b;
     return DPRT_OK;
 }
@@ -269,7 +281,7 @@ int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams*
     a.sy = (long long)b->sd[0];
     a.sz = (long long)b->sd[0] * b->sd[1];
     a.vox = b->vox;
-    a.macro = b->macro;
+    a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
     a.n_tf = p->n_tf;
@@ -288,6 +300,11 @@ int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams*
     } else {
         rc = dprt_brick_footprint(b, cam, W, H, a.rect);
         if (rc) return rc;
+    }
+    if (a.skip && (p->tf_version == 0 || b->skip_version != p->tf_version)) {
+        DprtBrick* mb = const_cast<DprtBrick*>(b);  // the skip-distance cache is mutable state
+        CK(dprt::launch_skip_build(*mb, a, mb->skip_tmp, (cudaStream_t)stream), "skip-distance build");
+        mb->skip_version = p->tf_version;
     }
     CK(dprt::launch_march(a, (cudaStream_t)stream), "march kernel launch");
     return DPRT_OK;

@@ -13,6 +13,7 @@ constexpr int kMacroShift = 3;
 constexpr int kTileX = 16;         // marcher CTA screen tile: 16 x 16 pixels, warps are 8 x 4 pixel tiles
 constexpr int kTileY = 16;
 constexpr int kMaxTf = 1024;       // transfer-function entries held in shared memory
+constexpr int kSkipCap = 15;       // Chebyshev skip distances are capped at this many macrocells
 
 struct DeviceBrick {
     int device;
@@ -22,6 +23,9 @@ struct DeviceBrick {
     float* vox;        // sd[0]*sd[1]*sd[2] f32, x fastest
     int64_t mcd[3];    // macrocell grid dims
     float2* macro;     // per macrocell (min, max) over its dilated voxel range
+    uint8_t* skipd;    // per macrocell Chebyshev distance to the nearest non-empty macrocell (TF-dependent)
+    uint8_t* skip_tmp; // scratch for the separable distance passes
+    uint64_t skip_version;  // tf_version the skip distances were built for (0 = never)
 };
 
 // Everything the marcher needs, by value (kernel parameter space).
@@ -40,7 +44,7 @@ struct MarchArgs {
     int sd[3];
     long long sy, sz;      // voxel strides
     const float* __restrict__ vox;
-    const float2* __restrict__ macro;
+    const uint8_t* __restrict__ skipd;
     int mcd[3];
     int skip;
     // transfer function

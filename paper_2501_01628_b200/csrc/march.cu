@@ -69,26 +69,9 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
 
 __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs a) {
     __shared__ float4 s_tf[kMaxTf];
-    __shared__ int s_next_nz[kMaxTf];  // smallest entry index >= i whose alpha > 0 (n_tf if none)
 
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_tf; i += blockDim.x) s_tf[i] = a.tf[i];
-    if (a.skip) {
-        // suffix scan of "alpha > 0" by one warp (n_tf <= 1024)
-        if (tid < 32) {
-            int carry = a.n_tf;
-            for (int base = ((a.n_tf - 1) / 32) * 32; base >= 0; base -= 32) {
-                int i = base + tid;
-                bool nz = i < a.n_tf && a.tf[i].w > 0.0f;
-                unsigned m = __ballot_sync(0xffffffffu, nz);
-                unsigned here = m & (0xffffffffu << tid);
-                int nxt = here ? base + __ffs(here) - 1 : carry;
-                if (i < a.n_tf) s_next_nz[i] = nxt;
-                int lowest = m ? base + __ffs(m) - 1 : carry;
-                carry = __shfl_sync(0xffffffffu, lowest, 0);
-            }
-        }
-    }
     __syncthreads();
 
     const int warp = tid >> 5, lane = tid & 31;
@@ -106,87 +89,152 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
     }
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
     if (n > 0) {
-        // start position in local (stored) continuous index space, and per-sample step
-        float p0[3], st[3];
+        // start position in local (stored) continuous index space, per-sample step and its reciprocal
+        float p0[3], st[3], ist[3];
         const double t0 = __dmul_rn((double)k0, a.dt);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             double p = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
             p0[i] = (float)(p - a.stored_lo_d[i]);
             st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
+            ist[i] = st[i] != 0.f ? 1.f / st[i] : 0.f;
         }
         const float top = (float)(a.n_tf - 1);
-        int cur_mc = -1;
-        int j = 0;
         const int nn = (int)n;
+        int j = 0;
         while (j < nn) {
+            // Which macrocell holds sample j, and how far the empty region around it extends.
             const float fj = (float)j;
-            const float ux = fmaf(fj, st[0], p0[0]);
-            const float uy = fmaf(fj, st[1], p0[1]);
-            const float uz = fmaf(fj, st[2], p0[2]);
-            const int ix = clampi(__float2int_rd(ux), a.clo[0], a.chi[0]);
-            const int iy = clampi(__float2int_rd(uy), a.clo[1], a.chi[1]);
-            const int iz = clampi(__float2int_rd(uz), a.clo[2], a.chi[2]);
-            if (a.skip) {
-                const int mx = ix >> kMacroShift, my = iy >> kMacroShift, mz = iz >> kMacroShift;
-                const int mc = (mz * a.mcd[1] + my) * a.mcd[0] + mx;
-                if (mc != cur_mc) {
-                    const float2 mm = __ldg(&a.macro[mc]);
-                    const float xl = fminf(fmaxf((mm.x - a.vmin) * a.tf_scale, 0.f), top);
-                    const float xh = fminf(fmaxf((mm.y - a.vmin) * a.tf_scale, 0.f), top);
-                    const int il = (int)xl;
-                    const int ih = min((int)xh + 2, a.n_tf - 1);
-                    if (s_next_nz[il] > ih) {
-                        // empty: jump to the first sample past this macrocell's far faces
-                        float jx = INFINITY, jy = INFINITY, jz = INFINITY;
-                        if (st[0] > 0.f) jx = ((float)((mx + 1) << kMacroShift) - p0[0]) / st[0];
-                        else if (st[0] < 0.f) jx = ((float)(mx << kMacroShift) - p0[0]) / st[0];
-                        if (st[1] > 0.f) jy = ((float)((my + 1) << kMacroShift) - p0[1]) / st[1];
-                        else if (st[1] < 0.f) jy = ((float)(my << kMacroShift) - p0[1]) / st[1];
-                        if (st[2] > 0.f) jz = ((float)((mz + 1) << kMacroShift) - p0[2]) / st[2];
-                        else if (st[2] < 0.f) jz = ((float)(mz << kMacroShift) - p0[2]) / st[2];
-                        const float je = fminf(jx, fminf(jy, jz));
-                        int jn = je < (float)nn ? (int)ceilf(je) : nn;
-                        j = jn > j ? jn : j + 1;
-                        cur_mc = -1;
-                        continue;
-                    }
-                    cur_mc = mc;
-                }
+            const int mx = clampi(__float2int_rd(fmaf(fj, st[0], p0[0])), a.clo[0], a.chi[0]) >> kMacroShift;
+            const int my = clampi(__float2int_rd(fmaf(fj, st[1], p0[1])), a.clo[1], a.chi[1]) >> kMacroShift;
+            const int mz = clampi(__float2int_rd(fmaf(fj, st[2], p0[2])), a.clo[2], a.chi[2]) >> kMacroShift;
+            int dist = 0;
+            if (a.skip) dist = __ldg(a.skipd + ((long long)mz * a.mcd[1] + my) * a.mcd[0] + mx);
+            // Exit of the cube of macrocells [m - r + 1, m + r] (r = max(dist, 1)): every sample before it
+            // lies in that cube; for dist > 0 the whole cube is empty for this TF (exact skip).
+            const int r = dist > 0 ? dist : 1;
+            float je = 3.0e38f;
+            {
+                const float fx = (float)((st[0] > 0.f ? mx + r : mx - r + 1) << kMacroShift);
+                const float fy = (float)((st[1] > 0.f ? my + r : my - r + 1) << kMacroShift);
+                const float fz = (float)((st[2] > 0.f ? mz + r : mz - r + 1) << kMacroShift);
+                if (st[0] != 0.f) je = fminf(je, (fx - p0[0]) * ist[0]);
+                if (st[1] != 0.f) je = fminf(je, (fy - p0[1]) * ist[1]);
+                if (st[2] != 0.f) je = fminf(je, (fz - p0[2]) * ist[2]);
             }
-            const float wx = __saturatef(ux - (float)ix);
-            const float wy = __saturatef(uy - (float)iy);
-            const float wz = __saturatef(uz - (float)iz);
-            const float* p = a.vox + (long long)iz * a.sz + (long long)iy * a.sy + ix;
-            const float v000 = __ldg(p), v100 = __ldg(p + 1);
-            const float v010 = __ldg(p + a.sy), v110 = __ldg(p + a.sy + 1);
-            const float v001 = __ldg(p + a.sz), v101 = __ldg(p + a.sz + 1);
-            const float v011 = __ldg(p + a.sz + a.sy), v111 = __ldg(p + a.sz + a.sy + 1);
-            const float c00 = fmaf(wx, v100 - v000, v000);
-            const float c10 = fmaf(wx, v110 - v010, v010);
-            const float c01 = fmaf(wx, v101 - v001, v001);
-            const float c11 = fmaf(wx, v111 - v011, v011);
-            const float c0 = fmaf(wy, c10 - c00, c00);
-            const float c1 = fmaf(wy, c11 - c01, c01);
-            const float v = fmaf(wz, c1 - c0, c0);
-            // transfer function
-            const float x = fminf(fmaxf((v - a.vmin) * a.tf_scale, 0.f), top);
-            const int ti = min((int)x, a.n_tf - 2);
-            const float tfr = x - (float)ti;
-            const float4 e0 = s_tf[ti], e1 = s_tf[ti + 1];
-            const float ea = fmaf(tfr, e1.w - e0.w, e0.w);
-            // front-to-back, premultiplied
-            const float w = (1.f - A) * ea;
-            C0 = fmaf(w, fmaf(tfr, e1.x - e0.x, e0.x), C0);
-            C1 = fmaf(w, fmaf(tfr, e1.y - e0.y, e0.y), C1);
-            C2 = fmaf(w, fmaf(tfr, e1.z - e0.z, e0.z), C2);
-            A += w;
-            if (A >= a.ert) break;
-            ++j;
+            int jend = je < (float)nn ? (int)ceilf(je) : nn;
+            if (jend <= j) jend = j + 1;
+            if (dist > 0) {
+                j = jend;
+                continue;
+            }
+            // Non-empty macrocell: sample j .. jend-1 with no per-sample skip bookkeeping.
+            for (; j < jend; ++j) {
+                const float fs = (float)j;
+                const float ux = fmaf(fs, st[0], p0[0]);
+                const float uy = fmaf(fs, st[1], p0[1]);
+                const float uz = fmaf(fs, st[2], p0[2]);
+                const int ix = clampi(__float2int_rd(ux), a.clo[0], a.chi[0]);
+                const int iy = clampi(__float2int_rd(uy), a.clo[1], a.chi[1]);
+                const int iz = clampi(__float2int_rd(uz), a.clo[2], a.chi[2]);
+                const float wx = __saturatef(ux - (float)ix);
+                const float wy = __saturatef(uy - (float)iy);
+                const float wz = __saturatef(uz - (float)iz);
+                const float* p = a.vox + (long long)iz * a.sz + (long long)iy * a.sy + ix;
+                const float v000 = __ldg(p), v100 = __ldg(p + 1);
+                const float v010 = __ldg(p + a.sy), v110 = __ldg(p + a.sy + 1);
+                const float v001 = __ldg(p + a.sz), v101 = __ldg(p + a.sz + 1);
+                const float v011 = __ldg(p + a.sz + a.sy), v111 = __ldg(p + a.sz + a.sy + 1);
+                const float c00 = fmaf(wx, v100 - v000, v000);
+                const float c10 = fmaf(wx, v110 - v010, v010);
+                const float c01 = fmaf(wx, v101 - v001, v001);
+                const float c11 = fmaf(wx, v111 - v011, v011);
+                const float c0 = fmaf(wy, c10 - c00, c00);
+                const float c1 = fmaf(wy, c11 - c01, c01);
+                const float v = fmaf(wz, c1 - c0, c0);
+                // transfer function
+                const float x = fminf(fmaxf((v - a.vmin) * a.tf_scale, 0.f), top);
+                const int ti = min((int)x, a.n_tf - 2);
+                const float tfr = x - (float)ti;
+                const float4 e0 = s_tf[ti], e1 = s_tf[ti + 1];
+                const float ea = fmaf(tfr, e1.w - e0.w, e0.w);
+                // front-to-back, premultiplied
+                const float w = (1.f - A) * ea;
+                C0 = fmaf(w, fmaf(tfr, e1.x - e0.x, e0.x), C0);
+                C1 = fmaf(w, fmaf(tfr, e1.y - e0.y, e0.y), C1);
+                C2 = fmaf(w, fmaf(tfr, e1.z - e0.z, e0.z), C2);
+                A += w;
+                if (A >= a.ert) goto done;  // early ray termination
+            }
         }
     }
+done:
     a.out[pix] = make_float4(C0, C1, C2, A);
     if (a.samples) a.samples[pix] = (uint32_t)n;
+}
+
+// Skip distances.  classify: 0 for a macrocell whose dilated value range [min, max]
+// can map to a non-zero alpha under the TF (conservatively one extra entry on each side), kSkipCap
+// otherwise.  Then three separable passes turn it into the Chebyshev distance (in macrocells, capped)
+// to the nearest non-empty macrocell: D(m) = min_c max(|m - c|_inf, E(c)).
+__global__ void skip_classify_kernel(const float2* __restrict__ macro, long long nmc, const float4* __restrict__ tf,
+                                     int n_tf, float vmin, float tf_scale, uint8_t* __restrict__ out) {
+    __shared__ int s_next_nz[kMaxTf];
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        int carry = n_tf;
+        for (int base = ((n_tf - 1) / 32) * 32; base >= 0; base -= 32) {
+            const int i = base + tid;
+            const bool nz = i < n_tf && tf[i].w > 0.0f;
+            const unsigned m = __ballot_sync(0xffffffffu, nz);
+            const unsigned here = m & (0xffffffffu << tid);
+            if (i < n_tf) s_next_nz[i] = here ? base + __ffs(here) - 1 : carry;
+            const int lowest = m ? base + __ffs(m) - 1 : carry;
+            carry = __shfl_sync(0xffffffffu, lowest, 0);
+        }
+    }
+    __syncthreads();
+    const float top = (float)(n_tf - 1);
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < nmc; i += (long long)gridDim.x * blockDim.x) {
+        const float2 mm = macro[i];
+        const float xl = fminf(fmaxf((mm.x - vmin) * tf_scale, 0.f), top);
+        const float xh = fminf(fmaxf((mm.y - vmin) * tf_scale, 0.f), top);
+        const int il = max((int)xl - 1, 0);
+        const int ih = min((int)xh + 2, n_tf - 1);
+        out[i] = s_next_nz[il] > ih ? (uint8_t)kSkipCap : (uint8_t)0;
+    }
+}
+
+__global__ void skip_pass_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int n0, int n1, int n2,
+                                 int axis) {
+    const long long total = (long long)n0 * n1 * n2;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % n0);
+        const int y = (int)((i / n0) % n1);
+        const int z = (int)(i / ((long long)n0 * n1));
+        const int c = axis == 0 ? x : (axis == 1 ? y : z);
+        const int n = axis == 0 ? n0 : (axis == 1 ? n1 : n2);
+        const long long stride = axis == 0 ? 1 : (axis == 1 ? n0 : (long long)n0 * n1);
+        int best = in[i];
+        for (int k = 1; k < best && k < kSkipCap; ++k) {
+            if (c - k >= 0) best = min(best, max(k, (int)in[i - k * stride]));
+            if (c + k < n) best = min(best, max(k, (int)in[i + k * stride]));
+        }
+        out[i] = (uint8_t)best;
+    }
+}
+
+cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t* tmp, cudaStream_t stream) {
+    const long long nmc = (long long)b.mcd[0] * b.mcd[1] * b.mcd[2];
+    const int block = 256;
+    const long long want = (nmc + block - 1) / block;
+    const int grid = (int)(want < 148LL * 16 ? (want > 0 ? want : 1) : 148LL * 16);
+    skip_classify_kernel<<<grid, block, 0, stream>>>(b.macro, nmc, a.tf, a.n_tf, a.vmin, a.tf_scale, b.skipd);
+    skip_pass_kernel<<<grid, block, 0, stream>>>(b.skipd, tmp, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 2);
+    skip_pass_kernel<<<grid, block, 0, stream>>>(tmp, b.skipd, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 1);
+    skip_pass_kernel<<<grid, block, 0, stream>>>(b.skipd, tmp, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 0);
+    return cudaMemcpyAsync(b.skipd, tmp, (size_t)nmc, cudaMemcpyDeviceToDevice, stream);
 }
 
 // Host launcher (called from abi.cu).

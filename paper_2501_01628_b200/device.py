@@ -8,6 +8,7 @@ reference's exception classes (errors.py); there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import itertools
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -129,16 +130,37 @@ class DeviceBrick:
             pass
 
 
+_TF_VERSIONS = itertools.count(1)
+
+
 class DeviceTF:
-    """A transfer function table resident on one device (4 KiB for 256 entries)."""
+    """A transfer function table resident on one device (4 KiB for 256 entries).
+
+    ``version`` tags the table contents for the bricks' cached skip distances; ``update`` re-uploads
+    and bumps it only when the contents change."""
 
     def __init__(self, tf: TransferFunction1D, device: torch.device):
         self.tf = tf
-        self.table = torch.from_numpy(tf.as_f32().reshape(-1)).to(device)
+        self._host = tf.as_f32().reshape(-1).copy()
+        self.table = torch.from_numpy(self._host.copy()).to(device)
+        self.version = next(_TF_VERSIONS)
+
+    def update(self, tf: TransferFunction1D, staging: Optional[torch.Tensor] = None) -> None:
+        """New table contents (optionally copied from a pinned host staging tensor)."""
+        host = tf.as_f32().reshape(-1)
+        if host.shape != self._host.shape or not np.array_equal(host, self._host) or (
+                tf.vmin, tf.vmax) != (self.tf.vmin, self.tf.vmax):
+            self.version = next(_TF_VERSIONS)
+            self._host = host.copy()
+            if host.shape[0] != self.table.numel():
+                self.table = torch.empty(host.shape[0], dtype=torch.float32, device=self.table.device)
+        self.tf = tf
+        src = staging if staging is not None else torch.from_numpy(self._host)
+        self.table.copy_(src, non_blocking=staging is not None)
 
     def params(self, dt: float, ert: float, flags: int = 0) -> _lib.MarchParams:
         return _lib.MarchParams(ctypes.c_void_p(self.table.data_ptr()), self.tf.n, flags, float(self.tf.vmin),
-                                float(self.tf.vmax), float(dt), float(ert))
+                                float(self.tf.vmax), float(dt), float(ert), self.version)
 
 
 def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, partial: torch.Tensor,

@@ -165,3 +165,29 @@ def test_orbit_frames_order_and_ownership(cuda_device, oracle_lib):
         for r in range(8):
             assert np.array_equal(samples[r].view(H, W).cpu().numpy().astype(np.uint32), rs[r])
             _check_rgba(parts[r].view(H, W, 4).cpu().numpy(), ref[r], f"frame {i} brick {r}")
+
+
+def test_skip_cache_follows_tf_updates(cuda_device, oracle_lib):
+    """The TF-dependent skip distances are cached per DeviceTF version; updating the TF (different
+    empty range) must rebuild them so the frame still matches the oracle for the new TF."""
+    from paper_2501_01628_b200.volume import TransferFunction1D
+
+    f = blob_field((40, 36, 32), seed=8)
+    vox = oracle.generate_field(f.dims, f.blobs)
+    dec = decompose(f, 1)
+    W, H = 64, 48
+    cam = auto_camera(f.bounds(), W, H)
+    b = dev.DeviceBrick(dec.brick(0), cuda_device).generate(f)
+    tf_a = default_tf(threshold=0.6)
+    t = dense_tf().as_f32().copy()
+    t[:, 3] = np.where(np.arange(256) < 20, 0.0, 0.05)
+    tf_b = TransferFunction1D(t, 0.0, 1.0)
+    dtf = dev.DeviceTF(tf_a, cuda_device)
+    p = torch.empty(H * W * 4, dtype=torch.float32, device=cuda_device)
+    for tf in (tf_a, tf_b, tf_a):
+        dtf.update(tf)
+        dev.march(b, cam, dtf, 1.0, 0.99, p, W, H)
+        torch.cuda.synchronize()
+        ref, _ = oracle_partials(vox, dec, cam, tf, 1.0, 0.99, W, H)
+        _check_rgba(p.view(H, W, 4).cpu().numpy(), ref[0], "after TF update")
+    b.close()
