@@ -97,6 +97,16 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
             return fail(DPRT_E_USAGE, "spacing/origin on axis %d must be finite, spacing > 0", a);
     }
     if (desc->ghost < 0) return fail(DPRT_E_USAGE, "ghost must be >= 0");
+    {
+        long long nv = 1;
+        for (int a = 0; a < 3; ++a) {
+            long long lo = desc->lo[a] - desc->ghost < 0 ? 0 : desc->lo[a] - desc->ghost;
+            long long hi = desc->hi[a] + desc->ghost > desc->dims[a] - 1 ? desc->dims[a] - 1 : desc->hi[a] + desc->ghost;
+            nv *= hi - lo + 1;
+        }
+        // the marcher addresses voxels with 32-bit offsets: split larger fields into more bricks
+        if (nv >= (1LL << 31)) return fail(DPRT_E_USAGE, "brick stores %lld voxels; the limit is 2^31 - 1 per brick", nv);
+    }
     int rc = bind(device);
     if (rc) return rc;
     DprtBrick* b = new DprtBrick();

@@ -68,10 +68,17 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
 }
 
 __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs a) {
-    __shared__ float4 s_tf[kMaxTf];
+    // TF as (entry, next - entry) pairs: the lerp e0 + (e1 - e0) * f becomes one FMA per channel with the
+    // identical rounding (the difference is formed once here instead of per sample).
+    extern __shared__ float4 s_tf[];  // 2 * n_tf entries (dynamic)
 
     const int tid = threadIdx.x;
-    for (int i = tid; i < a.n_tf; i += blockDim.x) s_tf[i] = a.tf[i];
+    for (int i = tid; i < a.n_tf; i += blockDim.x) {
+        const float4 e0 = a.tf[i];
+        const float4 e1 = i + 1 < a.n_tf ? a.tf[i + 1] : e0;
+        s_tf[2 * i] = e0;
+        s_tf[2 * i + 1] = make_float4(e1.x - e0.x, e1.y - e0.y, e1.z - e0.z, e1.w - e0.w);
+    }
     __syncthreads();
 
     const int warp = tid >> 5, lane = tid & 31;
@@ -99,76 +106,77 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
             st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
             ist[i] = st[i] != 0.f ? 1.f / st[i] : 0.f;
         }
-        const float top = (float)(a.n_tf - 1);
+        // loop invariants in registers
+        const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
+        const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
+        const float* __restrict__ vox = a.vox;
+        const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
+        const int tmax = a.n_tf - 2;
         const int nn = (int)n;
-        int j = 0;
+        int j = 0, jend = 0;  // samples [j, jend) lie in a macrocell known to be non-empty
         while (j < nn) {
-            // Which macrocell holds sample j, and how far the empty region around it extends.
-            const float fj = (float)j;
-            const int mx = clampi(__float2int_rd(fmaf(fj, st[0], p0[0])), a.clo[0], a.chi[0]) >> kMacroShift;
-            const int my = clampi(__float2int_rd(fmaf(fj, st[1], p0[1])), a.clo[1], a.chi[1]) >> kMacroShift;
-            const int mz = clampi(__float2int_rd(fmaf(fj, st[2], p0[2])), a.clo[2], a.chi[2]) >> kMacroShift;
-            int dist = 0;
-            if (a.skip) dist = __ldg(a.skipd + ((long long)mz * a.mcd[1] + my) * a.mcd[0] + mx);
-            // Exit of the cube of macrocells [m - r + 1, m + r] (r = max(dist, 1)): every sample before it
-            // lies in that cube; for dist > 0 the whole cube is empty for this TF (exact skip).
-            const int r = dist > 0 ? dist : 1;
-            float je = 3.0e38f;
-            {
-                const float fx = (float)((st[0] > 0.f ? mx + r : mx - r + 1) << kMacroShift);
-                const float fy = (float)((st[1] > 0.f ? my + r : my - r + 1) << kMacroShift);
-                const float fz = (float)((st[2] > 0.f ? mz + r : mz - r + 1) << kMacroShift);
-                if (st[0] != 0.f) je = fminf(je, (fx - p0[0]) * ist[0]);
-                if (st[1] != 0.f) je = fminf(je, (fy - p0[1]) * ist[1]);
-                if (st[2] != 0.f) je = fminf(je, (fz - p0[2]) * ist[2]);
+            if (j >= jend) {
+                // Which macrocell holds sample j, and how far the empty region around it extends.
+                const float fj = (float)j;
+                const int mx = clampi(__float2int_rd(fmaf(fj, st[0], p0[0])), 0, chx) >> kMacroShift;
+                const int my = clampi(__float2int_rd(fmaf(fj, st[1], p0[1])), 0, chy) >> kMacroShift;
+                const int mz = clampi(__float2int_rd(fmaf(fj, st[2], p0[2])), 0, chz) >> kMacroShift;
+                const int dist = a.skip ? (int)__ldg(a.skipd + (mz * a.mcd[1] + my) * a.mcd[0] + mx) : 0;
+                // Exit of the cube of macrocells [m - r + 1, m + r] (r = max(dist, 1)): samples before it
+                // lie in that cube; for dist > 0 the whole cube is empty for this TF (exact skip).
+                const int r = dist > 0 ? dist : 1;
+                float je = 3.0e38f;
+                if (st[0] != 0.f)
+                    je = fminf(je, ((float)((st[0] > 0.f ? mx + r : mx - r + 1) << kMacroShift) - p0[0]) * ist[0]);
+                if (st[1] != 0.f)
+                    je = fminf(je, ((float)((st[1] > 0.f ? my + r : my - r + 1) << kMacroShift) - p0[1]) * ist[1]);
+                if (st[2] != 0.f)
+                    je = fminf(je, ((float)((st[2] > 0.f ? mz + r : mz - r + 1) << kMacroShift) - p0[2]) * ist[2]);
+                int jn = je < (float)nn ? (int)ceilf(je) : nn;
+                if (jn <= j) jn = j + 1;
+                if (dist > 0) {
+                    j = jn;
+                    continue;
+                }
+                jend = jn;
             }
-            int jend = je < (float)nn ? (int)ceilf(je) : nn;
-            if (jend <= j) jend = j + 1;
-            if (dist > 0) {
-                j = jend;
-                continue;
-            }
-            // Non-empty macrocell: sample j .. jend-1 with no per-sample skip bookkeeping.
-            for (; j < jend; ++j) {
-                const float fs = (float)j;
-                const float ux = fmaf(fs, st[0], p0[0]);
-                const float uy = fmaf(fs, st[1], p0[1]);
-                const float uz = fmaf(fs, st[2], p0[2]);
-                const int ix = clampi(__float2int_rd(ux), a.clo[0], a.chi[0]);
-                const int iy = clampi(__float2int_rd(uy), a.clo[1], a.chi[1]);
-                const int iz = clampi(__float2int_rd(uz), a.clo[2], a.chi[2]);
-                const float wx = __saturatef(ux - (float)ix);
-                const float wy = __saturatef(uy - (float)iy);
-                const float wz = __saturatef(uz - (float)iz);
-                const float* p = a.vox + (long long)iz * a.sz + (long long)iy * a.sy + ix;
-                const float v000 = __ldg(p), v100 = __ldg(p + 1);
-                const float v010 = __ldg(p + a.sy), v110 = __ldg(p + a.sy + 1);
-                const float v001 = __ldg(p + a.sz), v101 = __ldg(p + a.sz + 1);
-                const float v011 = __ldg(p + a.sz + a.sy), v111 = __ldg(p + a.sz + a.sy + 1);
-                const float c00 = fmaf(wx, v100 - v000, v000);
-                const float c10 = fmaf(wx, v110 - v010, v010);
-                const float c01 = fmaf(wx, v101 - v001, v001);
-                const float c11 = fmaf(wx, v111 - v011, v011);
-                const float c0 = fmaf(wy, c10 - c00, c00);
-                const float c1 = fmaf(wy, c11 - c01, c01);
-                const float v = fmaf(wz, c1 - c0, c0);
-                // transfer function
-                const float x = fminf(fmaxf((v - a.vmin) * a.tf_scale, 0.f), top);
-                const int ti = min((int)x, a.n_tf - 2);
-                const float tfr = x - (float)ti;
-                const float4 e0 = s_tf[ti], e1 = s_tf[ti + 1];
-                const float ea = fmaf(tfr, e1.w - e0.w, e0.w);
-                // front-to-back, premultiplied
-                const float w = (1.f - A) * ea;
-                C0 = fmaf(w, fmaf(tfr, e1.x - e0.x, e0.x), C0);
-                C1 = fmaf(w, fmaf(tfr, e1.y - e0.y, e0.y), C1);
-                C2 = fmaf(w, fmaf(tfr, e1.z - e0.z, e0.z), C2);
-                A += w;
-                if (A >= a.ert) goto done;  // early ray termination
-            }
+            const float fs = (float)j;
+            const float ux = fmaf(fs, st[0], p0[0]);
+            const float uy = fmaf(fs, st[1], p0[1]);
+            const float uz = fmaf(fs, st[2], p0[2]);
+            const int ix = clampi(__float2int_rd(ux), 0, chx);
+            const int iy = clampi(__float2int_rd(uy), 0, chy);
+            const int iz = clampi(__float2int_rd(uz), 0, chz);
+            const float wx = __saturatef(ux - (float)ix);
+            const float wy = __saturatef(uy - (float)iy);
+            const float wz = __saturatef(uz - (float)iz);
+            const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+            const float v000 = __ldg(p), v100 = __ldg(p + 1);
+            const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
+            const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
+            const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
+            const float c00 = fmaf(wx, v100 - v000, v000);
+            const float c10 = fmaf(wx, v110 - v010, v010);
+            const float c01 = fmaf(wx, v101 - v001, v001);
+            const float c11 = fmaf(wx, v111 - v011, v011);
+            const float c0 = fmaf(wy, c10 - c00, c00);
+            const float c1 = fmaf(wy, c11 - c01, c01);
+            const float v = fmaf(wz, c1 - c0, c0);
+            // transfer function
+            const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
+            const int ti = min((int)x, tmax);
+            const float tfr = x - (float)ti;
+            const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+            // front-to-back, premultiplied
+            const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+            C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+            C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+            C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+            A += w;
+            if (A >= ert) break;  // early ray termination
+            ++j;
         }
     }
-done:
     a.out[pix] = make_float4(C0, C1, C2, A);
     if (a.samples) a.samples[pix] = (uint32_t)n;
 }
@@ -241,7 +249,7 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
 cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     dim3 block(kTileX * kTileY);
     dim3 grid((a.W + kTileX - 1) / kTileX, (a.H + kTileY - 1) / kTileY);
-    march_kernel<<<grid, block, 0, stream>>>(a);
+    march_kernel<<<grid, block, 2 * a.n_tf * sizeof(float4), stream>>>(a);
     return cudaGetLastError();
 }
 
