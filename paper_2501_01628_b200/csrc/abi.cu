@@ -129,7 +129,11 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     b->skipd = nullptr;
     b->skip_tmp = nullptr;
     b->skip_version = 0;
+    b->rays = nullptr;
+    b->ray_cap = 0;
+    b->counters = nullptr;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc);
     if (e == cudaSuccess) e = cudaMalloc(&b->skip_tmp, (size_t)nmc);
@@ -138,6 +142,7 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
         cudaFree(b->macro);
         cudaFree(b->skipd);
         cudaFree(b->skip_tmp);
+        cudaFree(b->counters);
         delete b;
         return cuda_fail(e, "brick allocation");
     }
@@ -205,6 +210,8 @@ int dprt_brick_destroy(DprtBrick* b) {
     cudaFree(b->macro);
     cudaFree(b->skipd);
     cudaFree(b->skip_tmp);
+    cudaFree(b->rays);
+    cudaFree(b->counters);
     delete b;
     return DPRT_OK;
 }
@@ -311,8 +318,18 @@ int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams*
         rc = dprt_brick_footprint(b, cam, W, H, a.rect);
         if (rc) return rc;
     }
+    DprtBrick* mb = const_cast<DprtBrick*>(b);  // ray queue + skip-distance cache are mutable scratch
+    if ((long long)W * H > mb->ray_cap) {
+        CK(cudaStreamSynchronize((cudaStream_t)stream), "ray queue resize sync");
+        cudaFree(mb->rays);
+        mb->rays = nullptr;
+        mb->ray_cap = 0;
+        CK(cudaMalloc(&mb->rays, (size_t)W * H * 2 * sizeof(float4)), "ray queue allocation");
+        mb->ray_cap = (long long)W * H;
+    }
+    a.rays = mb->rays;
+    a.counters = mb->counters;
     if (a.skip && (p->tf_version == 0 || b->skip_version != p->tf_version)) {
-        DprtBrick* mb = const_cast<DprtBrick*>(b);  // the skip-distance cache is mutable state
         CK(dprt::launch_skip_build(*mb, a, mb->skip_tmp, (cudaStream_t)stream), "skip-distance build");
         mb->skip_version = p->tf_version;
     }

@@ -26,6 +26,9 @@ struct DeviceBrick {
     uint8_t* skipd;    // per macrocell Chebyshev distance to the nearest non-empty macrocell (TF-dependent)
     uint8_t* skip_tmp; // scratch for the separable distance passes
     uint64_t skip_version;  // tf_version the skip distances were built for (0 = never)
+    float4* rays;      // ray queue scratch (2 float4 per pixel of the largest frame marched so far)
+    long long ray_cap; // pixels the queue can hold
+    int* counters;     // queue counters
 };
 
 // Everything the marcher needs, by value (kernel parameter space).
@@ -54,6 +57,8 @@ struct MarchArgs {
     // output
     float4* __restrict__ out;
     uint32_t* __restrict__ samples;
+    float4* rays;   // compacted ray queue: 2 float4 per ray {p0, pixel}, {step, n}
+    int* counters;  // [0] rays queued by ray_setup, [1] rays taken by march
     int W, H;
     int rect[4];
 };

@@ -11,8 +11,12 @@
 //   read-only path, transfer function from shared memory, front-to-back premultiplied blend, early ray
 //   termination.  Exact empty-space skipping jumps over macrocells whose (1-voxel dilated) value range
 //   maps to alpha == 0 everywhere in the TF: the skipped samples would add exact zeros.
-// * CTA = 16x16 pixel tile, each warp an 8x4 tile, so the 32 rays of a warp stay within a few voxels
-//   of each other and their 8-corner gathers share L1 lines.
+// * Two kernels.  ray_setup: one thread per pixel (warps = 8x4 pixel tiles) does the exact f64 setup,
+//   writes zeros / sample counts for pixels that miss the brick, and appends the rays that hit it to a
+//   compact queue, one contiguous chunk per warp tile (spatially coherent).  march: a persistent grid
+//   of warps drains the queue; each lane owns one ray, and when too many lanes of a warp have finished
+//   the warp refills them from the queue in one batch, so lanes stay busy and no SM waits on a tail of
+//   heavy tiles.
 
 #include <math.h>
 
@@ -67,11 +71,54 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
     return kb > ka ? kb - ka : 0;
 }
 
+constexpr int kRefillBelow = 20;  // refill a warp's idle lanes once fewer than this many are marching
+constexpr int kStepsPerCheck = 4;
+
+// Pass 1: exact ray setup, zero-fill of pixels that miss the brick, compaction of the ones that hit.
+__global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchArgs a) {
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int px = blockIdx.x * kTileX + (warp & 1) * 8 + (lane & 7);
+    const int py = blockIdx.y * kTileY + (warp >> 1) * 4 + (lane >> 3);
+    const bool inside = px < a.W && py < a.H;
+    const bool in_rect = inside && px >= a.rect[0] && py >= a.rect[1] && px < a.rect[2] && py < a.rect[3];
+    int64_t k0 = 0, n = 0;
+    double d[3];
+    if (in_rect) {
+        primary_dir(a, px, py, d);
+        n = lattice_range(a, d, &k0);
+    }
+    const int64_t pix = (int64_t)py * a.W + px;
+    if (inside) {
+        if (a.samples) a.samples[pix] = (uint32_t)n;
+        if (n == 0) a.out[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const bool hit = n > 0;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (!m) return;
+    int base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(a.counters, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (!hit) return;
+    const int slot = base + __popc(m & ((1u << lane) - 1));
+    // start position in local (stored) continuous index space and the per-sample step
+    const double t0 = __dmul_rn((double)k0, a.dt);
+    float p0[3], st[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double p = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
+        p0[i] = (float)(p - a.stored_lo_d[i]);
+        st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
+    }
+    a.rays[2 * slot] = make_float4(p0[0], p0[1], p0[2], __int_as_float((int)pix));
+    a.rays[2 * slot + 1] = make_float4(st[0], st[1], st[2], __int_as_float((int)n));
+}
+
+// Pass 2: persistent warps march the queued rays.
 __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs a) {
     // TF as (entry, next - entry) pairs: the lerp e0 + (e1 - e0) * f becomes one FMA per channel with the
     // identical rounding (the difference is formed once here instead of per sample).
     extern __shared__ float4 s_tf[];  // 2 * n_tf entries (dynamic)
-
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_tf; i += blockDim.x) {
         const float4 e0 = a.tf[i];
@@ -81,40 +128,52 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
     }
     __syncthreads();
 
-    const int warp = tid >> 5, lane = tid & 31;
-    const int px = blockIdx.x * kTileX + (warp & 1) * 8 + (lane & 7);
-    const int py = blockIdx.y * kTileY + (warp >> 1) * 4 + (lane >> 3);
-    if (px >= a.W || py >= a.H) return;
-    const int64_t pix = (int64_t)py * a.W + px;
+    const int lane = tid & 31;
+    const int total = a.counters[0];  // written by ray_setup_kernel, which completed before this launch
+    const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
+    const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
+    const float* __restrict__ vox = a.vox;
+    const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
+    const int tmax = a.n_tf - 2;
 
-    const bool in_rect = px >= a.rect[0] && py >= a.rect[1] && px < a.rect[2] && py < a.rect[3];
-    int64_t k0 = 0, n = 0;
-    double d[3];
-    if (in_rect) {
-        primary_dir(a, px, py, d);
-        n = lattice_range(a, d, &k0);
-    }
+    bool have = false, exhausted = false;
+    int pix = 0, nn = 0, j = 0, jend = 0;
+    float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f}, ist[3] = {0.f, 0.f, 0.f};
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
-    if (n > 0) {
-        // start position in local (stored) continuous index space, per-sample step and its reciprocal
-        float p0[3], st[3], ist[3];
-        const double t0 = __dmul_rn((double)k0, a.dt);
+    while (true) {
+        unsigned act = __ballot_sync(0xffffffffu, have);
+        if (!exhausted && __popc(act) < kRefillBelow) {
+            const unsigned need = ~act;
+            const int k = __popc(need);
+            int base = 0;
+            if (lane == 0) base = atomicAdd(a.counters + 1, k);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base + k >= total) exhausted = true;
+            if (!have) {
+                const int idx = base + __popc(need & ((1u << lane) - 1));
+                if (idx < total) {
+                    const float4 r0 = __ldg(a.rays + 2 * idx), r1 = __ldg(a.rays + 2 * idx + 1);
+                    p0[0] = r0.x; p0[1] = r0.y; p0[2] = r0.z;
+                    st[0] = r1.x; st[1] = r1.y; st[2] = r1.z;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            double p = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
-            p0[i] = (float)(p - a.stored_lo_d[i]);
-            st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
-            ist[i] = st[i] != 0.f ? 1.f / st[i] : 0.f;
+                    for (int i = 0; i < 3; ++i) ist[i] = st[i] != 0.f ? 1.f / st[i] : 0.f;
+                    pix = __float_as_int(r0.w);
+                    nn = __float_as_int(r1.w);
+                    j = 0;
+                    jend = 0;
+                    C0 = C1 = C2 = A = 0.f;
+                    have = true;
+                }
+            }
+            act = __ballot_sync(0xffffffffu, have);
         }
-        // loop invariants in registers
-        const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
-        const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
-        const float* __restrict__ vox = a.vox;
-        const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
-        const int tmax = a.n_tf - 2;
-        const int nn = (int)n;
-        int j = 0, jend = 0;  // samples [j, jend) lie in a macrocell known to be non-empty
-        while (j < nn) {
+        if (act == 0) break;
+        for (int s = 0; have && s < kStepsPerCheck; ++s) {
+            if (j >= nn) {
+                a.out[pix] = make_float4(C0, C1, C2, A);
+                have = false;
+                break;
+            }
             if (j >= jend) {
                 // Which macrocell holds sample j, and how far the empty region around it extends.
                 const float fj = (float)j;
@@ -144,9 +203,9 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
             const float ux = fmaf(fs, st[0], p0[0]);
             const float uy = fmaf(fs, st[1], p0[1]);
             const float uz = fmaf(fs, st[2], p0[2]);
-            const int ix = clampi(__float2int_rd(ux), 0, chx);
-            const int iy = clampi(__float2int_rd(uy), 0, chy);
-            const int iz = clampi(__float2int_rd(uz), 0, chz);
+            const int ix = min(__float2int_rd(fmaxf(ux, 0.f)), chx);
+            const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
+            const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
             const float wx = __saturatef(ux - (float)ix);
             const float wy = __saturatef(uy - (float)iy);
             const float wz = __saturatef(uz - (float)iz);
@@ -173,12 +232,10 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
             C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
             C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
             A += w;
-            if (A >= ert) break;  // early ray termination
             ++j;
+            if (A >= ert) j = nn;  // early ray termination: finish at the next step
         }
     }
-    a.out[pix] = make_float4(C0, C1, C2, A);
-    if (a.samples) a.samples[pix] = (uint32_t)n;
 }
 
 // Skip distances.  classify: 0 for a macrocell whose dilated value range [min, max]
@@ -245,11 +302,22 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
     return cudaMemcpyAsync(b.skipd, tmp, (size_t)nmc, cudaMemcpyDeviceToDevice, stream);
 }
 
-// Host launcher (called from abi.cu).
+// Host launchers (called from abi.cu).
 cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), stream);
+    if (e != cudaSuccess) return e;
     dim3 block(kTileX * kTileY);
     dim3 grid((a.W + kTileX - 1) / kTileX, (a.H + kTileY - 1) / kTileY);
-    march_kernel<<<grid, block, 2 * a.n_tf * sizeof(float4), stream>>>(a);
+    ray_setup_kernel<<<grid, block, 0, stream>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = 2 * a.n_tf * sizeof(float4);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, kTileX * kTileY, smem);
+    if (per_sm < 1) per_sm = 1;
+    march_kernel<<<sms * per_sm, block, smem, stream>>>(a);
     return cudaGetLastError();
 }
 
