@@ -45,6 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
            "-Xcompiler", "-fPIC,-ffp-contract=off", "-I", str(INCLUDE), "-o", str(LIB)]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    cmd += os.environ.get("DPRT_NVCC_EXTRA", "").split()
     cmd += [str(CSRC / s) for s in SOURCES]
     tmp = LIB.with_suffix(".so.tmp")
     cmd[cmd.index(str(LIB))] = str(tmp)

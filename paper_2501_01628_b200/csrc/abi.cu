@@ -132,7 +132,11 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     b->rays = nullptr;
     b->ray_cap = 0;
     b->counters = nullptr;
+    b->quad = nullptr;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
+#if DPRT_QUAD
+    if (e == cudaSuccess) e = cudaMalloc(&b->quad, (size_t)nvox * sizeof(float4));
+#endif
     if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc);
@@ -143,6 +147,7 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
         cudaFree(b->skipd);
         cudaFree(b->skip_tmp);
         cudaFree(b->counters);
+        cudaFree(b->quad);
         delete b;
         return cuda_fail(e, "brick allocation");
     }
@@ -212,6 +217,7 @@ int dprt_brick_destroy(DprtBrick* b) {
     cudaFree(b->skip_tmp);
     cudaFree(b->rays);
     cudaFree(b->counters);
+    cudaFree(b->quad);
     delete b;
     return DPRT_OK;
 }
@@ -298,6 +304,7 @@ int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams*
     a.sy = (long long)b->sd[0];
     a.sz = (long long)b->sd[0] * b->sd[1];
     a.vox = b->vox;
+    a.quad = b->quad;
     a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);

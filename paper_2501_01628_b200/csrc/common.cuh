@@ -6,6 +6,10 @@
 
 #include "dprt_cuda.h"
 
+#ifndef DPRT_QUAD
+#define DPRT_QUAD 1
+#endif
+
 namespace dprt {
 
 constexpr int kMacro = 8;          // macrocell edge in cells (empty-space skipping granularity)
@@ -21,6 +25,7 @@ struct DeviceBrick {
     int64_t s_lo[3];   // first stored voxel (global index)
     int64_t sd[3];     // stored voxel dims
     float* vox;        // sd[0]*sd[1]*sd[2] f32, x fastest
+    float4* quad;      // per voxel {v(i,j,k), v(i+1,j,k), v(i,j+1,k), v(i+1,j+1,k)} (edge-clamped), DPRT_QUAD
     int64_t mcd[3];    // macrocell grid dims
     float2* macro;     // per macrocell (min, max) over its dilated voxel range
     uint8_t* skipd;    // per macrocell Chebyshev distance to the nearest non-empty macrocell (TF-dependent)
@@ -47,6 +52,7 @@ struct MarchArgs {
     int sd[3];
     long long sy, sz;      // voxel strides
     const float* __restrict__ vox;
+    const float4* __restrict__ quad;
     const uint8_t* __restrict__ skipd;
     int mcd[3];
     int skip;

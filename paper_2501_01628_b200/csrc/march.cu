@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
     const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
     const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
     const float* __restrict__ vox = a.vox;
+    const float4* __restrict__ quad = a.quad;
     const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
     const int tmax = a.n_tf - 2;
 
@@ -209,11 +210,19 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
             const float wx = __saturatef(ux - (float)ix);
             const float wy = __saturatef(uy - (float)iy);
             const float wz = __saturatef(uz - (float)iz);
+#if DPRT_QUAD
+            // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
+            const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+            const float4 qa = __ldg(q), qb = __ldg(q + sz);
+            const float v000 = qa.x, v100 = qa.y, v010 = qa.z, v110 = qa.w;
+            const float v001 = qb.x, v101 = qb.y, v011 = qb.z, v111 = qb.w;
+#else
             const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
             const float v000 = __ldg(p), v100 = __ldg(p + 1);
             const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
             const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
             const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
+#endif
             const float c00 = fmaf(wx, v100 - v000, v000);
             const float c10 = fmaf(wx, v110 - v010, v010);
             const float c01 = fmaf(wx, v101 - v001, v001);
