@@ -125,7 +125,10 @@ int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams*
 int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, const float bg[3], int flags,
                    uint8_t* rgb8, float* rgba_out, void* stream);
 
-/* Peer memory over NVLink for the fused direct-send compositor (one process per GPU). */
+/* Peer memory over NVLink for the fused direct-send compositor (one process per GPU).  Buffers that peers
+ * map must come from dprt_device_alloc so the IPC handle covers exactly [ptr, ptr + bytes). */
+int dprt_device_alloc(int device, uint64_t bytes, void** out_ptr);
+int dprt_device_free(int device, void* ptr);
 int dprt_ipc_handle(int device, const void* dev_ptr, uint8_t handle[64]);
 int dprt_ipc_open(int device, const uint8_t handle[64], void** out_ptr);
 int dprt_ipc_close(int device, void* ptr);

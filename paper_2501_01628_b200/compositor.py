@@ -159,7 +159,7 @@ class Compositor:
             return self._direct_send(partial, order, background, keep_float)
         if self.mode == "binary_swap":
             return self._binary_swap(partial, order, background, keep_float)
-        return self._p2p(partial, order, background, keep_float)
+        return self._p2p_composite(partial, order, background, keep_float)
 
     def _single(self, partial, background, keep_float) -> CompositeOutput:
         if self.ep.rank != 0:
@@ -258,10 +258,19 @@ class Compositor:
                 return self._gather_tiles(keep_rows, tile, tile_f, all_rows, keep_float)
         raise AssertionError("binary swap with P > 1 always has a last round")
 
-    def _p2p(self, partial, order, background, keep_float) -> CompositeOutput:
-        from .p2p import P2PCompositor
-        if not hasattr(self, "_p2p_impl"):
+    def shared_partial(self) -> Optional[torch.Tensor]:
+        """The buffer the marcher should write into (peer-mapped in p2p mode), or None for any buffer."""
+        if self.mode != "p2p":
+            return None
+        return self._p2p().partial.tensor
+
+    def _p2p(self):
+        if getattr(self, "_p2p_impl", None) is None:
+            from .p2p import P2PCompositor
             self._p2p_impl = P2PCompositor(self.ep, self.W, self.H, self.device)
-        out = self._p2p_impl.composite(partial, order, background, keep_float)
+        return self._p2p_impl
+
+    def _p2p_composite(self, partial, order, background, keep_float) -> CompositeOutput:
+        out = self._p2p().composite(partial, order, background, keep_float)
         self.last_bytes = self._p2p_impl.last_bytes
         return out

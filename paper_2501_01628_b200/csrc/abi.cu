@@ -374,6 +374,23 @@ int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, 
     return DPRT_OK;
 }
 
+int dprt_device_alloc(int device, uint64_t bytes, void** out_ptr) {
+    if (!out_ptr || bytes == 0) return fail(DPRT_E_USAGE, "bad allocation request");
+    *out_ptr = nullptr;
+    int rc = bind(device);
+    if (rc) return rc;
+    CK(cudaMalloc(out_ptr, (size_t)bytes), "dprt_device_alloc");
+    return DPRT_OK;
+}
+
+int dprt_device_free(int device, void* ptr) {
+    if (!ptr) return DPRT_OK;
+    int rc = bind(device);
+    if (rc) return rc;
+    CK(cudaFree(ptr), "dprt_device_free");
+    return DPRT_OK;
+}
+
 int dprt_ipc_handle(int device, const void* dev_ptr, uint8_t handle[64]) {
     if (!dev_ptr || !handle) return fail(DPRT_E_USAGE, "null IPC argument");
     int rc = bind(device);

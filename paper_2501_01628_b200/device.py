@@ -252,3 +252,35 @@ def ipc_open(device_index: int, handle: bytes) -> int:
 
 def ipc_close(device_index: int, ptr: int) -> None:
     _lib.check(_lib.lib().dprt_ipc_close(device_index, ctypes.c_void_p(ptr)), "dprt_ipc_close")
+
+
+class DeviceBuffer:
+    """Device memory from dprt_device_alloc (allocation base == pointer, so a CUDA IPC handle maps
+    exactly this buffer), viewed as a torch tensor through __cuda_array_interface__."""
+
+    def __init__(self, device: torch.device, numel: int, dtype=torch.float32):
+        self.index = device.index if device.index is not None else torch.cuda.current_device()
+        self.device = torch.device("cuda", self.index)
+        self.numel = int(numel)
+        self.dtype = dtype
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        self.nbytes = self.numel * itemsize
+        p = ctypes.c_void_p()
+        _lib.check(_lib.lib().dprt_device_alloc(self.index, self.nbytes, ctypes.byref(p)), "dprt_device_alloc")
+        self.ptr = int(p.value)
+        typestr = {torch.float32: "<f4", torch.uint8: "|u1", torch.int32: "<i4"}[dtype]
+        self.__cuda_array_interface__ = {"shape": (self.numel,), "typestr": typestr, "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(self, device=self.device)
+
+    def close(self) -> None:
+        if self.ptr:
+            torch.cuda.synchronize(self.device)
+            _lib.check(_lib.lib().dprt_device_free(self.index, ctypes.c_void_p(self.ptr)), "dprt_device_free")
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -142,12 +142,14 @@ class VolumeRenderer:
 
     def _ensure(self, width: int, height: int, mode: str) -> None:
         if self._size != (width, height):
-            self.partial = torch.empty(height * width * 4, dtype=torch.float32, device=self.device)
             self.samples = torch.empty(height * width, dtype=torch.int32, device=self.device)
             self.compositor = None
             self._size = (width, height)
         if self.compositor is None or self.compositor.mode_requested != mode:
             self.compositor = Compositor(self.ep, width, height, mode, self.device)
+            shared = self.compositor.shared_partial()
+            self.partial = shared if shared is not None else torch.empty(height * width * 4, dtype=torch.float32,
+                                                                          device=self.device)
 
     def render(self, cam: CameraSpec, width: int, height: int, options: RenderOptions = RenderOptions(),
                verify: bool = True) -> RenderResult:

@@ -1,0 +1,76 @@
+"""Fused sort-last compositor over peer memory (NVLink P2P): exchange + blend + gather in one kernel.
+
+Each rank marches straight into a buffer that every peer has mapped (CUDA IPC handles exchanged once on
+the control plane).  After a stream-ordered device barrier (an NCCL all-reduce: it completes on a rank
+only once every rank's march has finished), rank j launches ONE composite kernel whose P input pointers
+are the peers' partial buffers offset to row block j (``assign_pixels``, engine.py:216-221), in
+visibility order, and whose RGB8 output pointer is rank 0's frame at row block j.  The fragment reads
+((1 - 1/P) * W * H * 16 B per rank) and the tile writes into rank 0 (3 B/px) cross NVLink inside that
+kernel; a second device barrier publishes the frame to rank 0 and keeps peers from overwriting a
+partial that is still being read.  This replaces both the reference's ring cycling of ray batches
+(engine.py:282-310) and its linear gather_to_root of f64 tiles (engine.py:485, transport.py:465-475).
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import device as dev
+from .compositor import CompositeOutput, assign_rows
+from .transport import RankEndpoint
+
+
+class P2PCompositor:
+    def __init__(self, ep: RankEndpoint, width: int, height: int, device: torch.device):
+        self.ep = ep
+        self.W = width
+        self.H = height
+        self.device = device
+        self.index = device.index if device.index is not None else torch.cuda.current_device()
+        n = width * height
+        self.partial = dev.DeviceBuffer(device, n * 4)
+        self.frame = dev.DeviceBuffer(device, n * 3, torch.uint8) if ep.rank == 0 else None
+        self.frame_rgba: Optional[dev.DeviceBuffer] = None
+        self.peer_partials = ep.share_pointers(self.index, self.partial.ptr)
+        self.root_frame = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)[0]
+        self.root_rgba = 0
+        self.last_bytes = 0
+
+    def _ensure_rgba(self) -> None:
+        if self.root_rgba:
+            return
+        if self.ep.rank == 0:
+            self.frame_rgba = dev.DeviceBuffer(self.device, self.W * self.H * 4)
+        self.root_rgba = self.ep.share_pointers(self.index, self.frame_rgba.ptr if self.frame_rgba else 0)[0]
+
+    def composite(self, partial: torch.Tensor, order: Sequence[int], background, keep_float: bool = False
+                  ) -> CompositeOutput:
+        ep = self.ep
+        if keep_float:
+            self._ensure_rgba()
+        if partial.data_ptr() != self.partial.ptr:
+            self.partial.tensor.copy_(partial)
+        ep.device_barrier()  # every rank's partial is complete
+        rows = assign_rows(self.H, ep.R)[ep.rank]
+        npix = (rows[1] - rows[0]) * self.W
+        if npix:
+            off = rows[0] * self.W
+            ptrs = [self.peer_partials[s] + 16 * off for s in order]
+            dev.composite_ptrs(self.index, ptrs, npix, background, rgb8_ptr=self.root_frame + 3 * off,
+                               rgba_ptr=(self.root_rgba + 16 * off) if keep_float else 0)
+        ep.device_barrier()  # every tile has landed in rank 0's frame
+        self.last_bytes = 16 * npix * (ep.R - 1) + (3 * npix if ep.rank else 0)
+        if ep.rank != 0:
+            return CompositeOutput(None, None)
+        frame = self.frame.tensor.view(self.H, self.W, 3)
+        return CompositeOutput(frame, self.frame_rgba.tensor if keep_float else None)
+
+    def close(self) -> None:
+        self.ep.unshare_pointers(self.index, self.peer_partials)
+        self.partial.close()
+        if self.frame is not None:
+            self.frame.close()
+        if self.frame_rgba is not None:
+            self.frame_rgba.close()

@@ -99,6 +99,13 @@ class RankEndpoint:
     def device_barrier(self) -> None:
         raise NotImplementedError
 
+    def share_pointers(self, device_index: int, ptr: int) -> List[int]:
+        """Every rank's buffer (allocated with dprt_device_alloc, or 0), usable from this rank's GPU."""
+        raise NotImplementedError
+
+    def unshare_pointers(self, device_index: int, ptrs: Sequence[int]) -> None:
+        """Release mappings returned by share_pointers."""
+
     def all_gather_bytes(self, payload: bytes) -> List[bytes]:
         """gather_to_root + broadcast_from_root, the reference's all-gather idiom (api.py:284-293)."""
         tiles = self.gather_to_root(payload)
@@ -135,6 +142,9 @@ class SoloEndpoint(RankEndpoint):
 
     def device_barrier(self) -> None:
         return None
+
+    def share_pointers(self, device_index: int, ptr: int) -> List[int]:
+        return [ptr]
 
 
 class DistEndpoint(RankEndpoint):
@@ -207,6 +217,29 @@ class DistEndpoint(RankEndpoint):
         except Exception as exc:  # noqa: BLE001
             raise TransportError(f"rank {self.rank}: fragment exchange failed: {exc}") from exc
 
+    def share_pointers(self, device_index: int, ptr: int) -> List[int]:
+        """CUDA IPC: export this rank's buffer, map every peer's (lazily enabling NVLink peer access)."""
+        from . import device as dev
+
+        handle = dev.ipc_handle(device_index, ptr) if ptr else b""
+        handles = self.all_gather_bytes(handle)
+        out = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                out.append(ptr)
+            elif h:
+                out.append(dev.ipc_open(device_index, h))
+            else:
+                out.append(0)
+        return out
+
+    def unshare_pointers(self, device_index: int, ptrs: Sequence[int]) -> None:
+        from . import device as dev
+
+        for r, p in enumerate(ptrs):
+            if r != self.rank and p:
+                dev.ipc_close(device_index, p)
+
     def device_barrier(self) -> None:
         if self._token is None:
             dev = self.device if self.backend == "nccl" else torch.device("cpu")
@@ -237,3 +270,149 @@ def endpoint_for(device: Optional[torch.device] = None) -> RankEndpoint:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         return DistEndpoint(device=device)
     return SoloEndpoint(device)
+
+
+# ---------------------------------------------------------------------------------------------------
+# in-process ranks (threads), the reference's inproc backend + run_collective harness
+# (transport.py:164-204, 519-566): R ranks share one process -- and, for tests on a single GPU, one
+# device.  Fragments move by device-to-device copy; peer pointers are plain pointers.
+
+
+class _InprocSession:
+    def __init__(self, num_ranks: int, timeout: float):
+        import queue
+        import threading
+
+        self.R = num_ranks
+        self.timeout = timeout
+        self.ctrl = {(s, d): queue.Queue() for s in range(num_ranks) for d in range(num_ranks)}
+        self.data = {(s, d): queue.Queue() for s in range(num_ranks) for d in range(num_ranks)}
+        self.acks = {(s, d): queue.Queue() for s in range(num_ranks) for d in range(num_ranks)}
+        self.barrier = threading.Barrier(num_ranks, timeout=timeout)
+        self.aborted = threading.Event()
+
+    def abort(self) -> None:
+        self.aborted.set()
+        self.barrier.abort()
+
+
+class InprocEndpoint(RankEndpoint):
+    """A rank thread of an in-process group."""
+
+    def __init__(self, rank: int, session: _InprocSession, device: Optional[torch.device] = None):
+        super().__init__(rank, session.R, device)
+        self.session = session
+
+    def _get(self, q, what: str):
+        import queue
+
+        try:
+            return q.get(timeout=self.session.timeout)
+        except queue.Empty:
+            raise TransportError(f"rank {self.rank}: timeout after {self.session.timeout:g}s waiting for {what}") from None
+
+    def _send_ctrl(self, dst: int, kind: str, payload) -> None:
+        tag = self._tag(f"{kind}->{dst}")
+        self.session.ctrl[(self.rank, dst)].put((tag[0], tag[1], payload))
+        if payload is not None:
+            self.stats.messages_sent += 1
+            self.stats.bytes_sent += len(payload)
+
+    def _recv_ctrl(self, src: int, kind: str):
+        tag = self._tag(f"{kind}<-{src}")
+        got = self._get(self.session.ctrl[(src, self.rank)], f"{kind} from rank {src}")
+        payload = self._check((f"{kind}->{self.rank}", tag[1]), got, src)
+        self.stats.messages_received += 1
+        self.stats.bytes_received += len(payload)
+        return payload
+
+    def gather_to_root(self, tile: bytes) -> List[bytes]:
+        if self.rank == 0:
+            return [tile] + [self._recv_ctrl(s, "TILE") for s in range(1, self.R)]
+        self._send_ctrl(0, "TILE", tile)
+        return []
+
+    def broadcast_from_root(self, payload: Optional[bytes]) -> bytes:
+        if self.rank == 0:
+            if payload is None:
+                raise TransportError("rank 0 must supply the broadcast payload")
+            for d in range(1, self.R):
+                self._send_ctrl(d, "CONTROL", payload)
+            return payload
+        return self._recv_ctrl(0, "CONTROL")
+
+    def barrier(self) -> None:
+        self.gather_to_root(b"")
+        self.broadcast_from_root(b"" if self.rank == 0 else None)
+
+    def ring_exchange(self, outgoing: bytes) -> bytes:
+        if self.R == 1:
+            return outgoing
+        self._send_ctrl((self.rank + 1) % self.R, "RING", outgoing)
+        return self._recv_ctrl((self.rank - 1) % self.R, "RING")
+
+    def exchange(self, sends, recvs) -> None:
+        """Point-to-point tensor exchange; a send buffer is reusable when exchange returns."""
+        if sends:
+            torch.cuda.current_stream(self.device).synchronize() if self.device.type == "cuda" else None
+        for peer, t in sends:
+            self.session.data[(self.rank, peer)].put(t)
+            self.stats.device_bytes_sent += t.numel() * t.element_size()
+        for peer, t in recvs:
+            src = self._get(self.session.data[(peer, self.rank)], f"fragment from rank {peer}")
+            if src.numel() != t.numel():
+                raise ProtocolError(f"rank {self.rank}: fragment from rank {peer} has {src.numel()} elements, "
+                                    f"expected {t.numel()}")
+            t.copy_(src.view_as(t))
+            if t.is_cuda:
+                torch.cuda.current_stream(t.device).synchronize()
+            self.session.acks[(peer, self.rank)].put(True)
+            self.stats.device_bytes_received += t.numel() * t.element_size()
+        for peer, _ in sends:
+            self._get(self.session.acks[(self.rank, peer)], f"receipt from rank {peer}")
+
+    def share_pointers(self, device_index: int, ptr: int) -> List[int]:
+        """Same process: peer pointers are plain pointers."""
+        return [int(b) for b in self.all_gather_bytes(str(ptr).encode())]
+
+    def device_barrier(self) -> None:
+        import threading
+
+        if self.device.type == "cuda":
+            torch.cuda.current_stream(self.device).synchronize()
+        try:
+            self.session.barrier.wait()
+        except threading.BrokenBarrierError:
+            raise TransportError(f"rank {self.rank}: collective aborted") from None
+
+
+def run_collective(num_ranks: int, body, device: Optional[torch.device] = None, timeout: Optional[float] = None):
+    """Drive ``body(ep)`` on R rank threads of one process (transport.py:519-566); returns per-rank
+    results, re-raising the first rank failure.  A failing rank aborts the others' pending calls."""
+    import threading
+
+    session = _InprocSession(num_ranks, resolve_timeout(timeout))
+    eps = [InprocEndpoint(r, session, device) for r in range(num_ranks)]
+    results: List[object] = [None] * num_ranks
+    errors: Dict[int, BaseException] = {}
+
+    def runner(ep):
+        try:
+            if device is not None and device.type == "cuda":
+                torch.cuda.set_device(device)
+            results[ep.rank] = body(ep)
+        except BaseException as exc:  # noqa: BLE001
+            errors[ep.rank] = exc
+            session.abort()
+
+    threads = [threading.Thread(target=runner, args=(ep,), daemon=True, name=f"dprt-rank-{ep.rank}") for ep in eps]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(session.timeout * (num_ranks + 2) + 60.0)
+    if any(t.is_alive() for t in threads):
+        raise TransportError("rank threads failed to finish; session leaked")
+    if errors:
+        first = [e for _, e in sorted(errors.items()) if not isinstance(e, TransportError)]
+        raise (first[0] if first else next(iter(sorted(errors.items())))[1])
+    return results

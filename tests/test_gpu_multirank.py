@@ -1,0 +1,150 @@
+"""Multi-rank sort-last frames on ONE GPU: R rank threads in one process (the reference's run_collective
++ inproc model, transport.py:519-566), each marching its own brick and compositing through the real
+exchange schedule (direct-send / binary-swap by device copies, p2p by plain peer pointers).  The frame on
+rank 0 is compared with the oracle; sample ownership per rank exactly."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2501_01628_b200 import device as dev
+from paper_2501_01628_b200.api import Device, map_frame
+from paper_2501_01628_b200.engine import RenderOptions, VolumeRenderer
+from paper_2501_01628_b200.transport import run_collective
+from scenes import RGB8_MAX_LSB, RGBA_ATOL, c1, oracle_partials
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("mode,R", [("direct_send", 2), ("direct_send", 3), ("binary_swap", 4), ("p2p", 2),
+                                    ("p2p", 4), ("binary_swap", 8)])
+def test_sort_last_frame_matches_oracle(cuda_device, oracle_lib, mode, R):
+    s = c1(P=R, W=160, H=122)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, rs = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H)
+    order = s.dec.visibility_order(s.cam.position)
+    img_ref = oracle.composite(ref, order, s.background)
+
+    def body(ep):
+        b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda_device).generate(s.field)
+        vr = VolumeRenderer(ep, b, s.dec, s.tf, s.background)
+        out = []
+        for frame in range(2):
+            res = vr.render(s.cam, s.W, s.H, RenderOptions(composite=mode, keep_float=True, collect_samples=True,
+                                                           frame_index=frame))
+            torch.cuda.synchronize()
+            samples = res.samples.cpu().numpy().astype(np.uint32)
+            out.append((res.image, None if res.rgb8 is None else res.rgb8.cpu().numpy(), samples, res.order))
+        return out
+
+    results = run_collective(R, body, device=cuda_device)
+    for r in range(R):
+        for image, rgb8, samples, got_order in results[r]:
+            assert np.array_equal(samples, rs[r])
+            assert got_order == order
+            if r == 0:
+                assert np.abs(image - img_ref).max() <= RGBA_ATOL
+                q = rgb8.astype(np.int16) - oracle.tone_map_rgb8(img_ref).astype(np.int16)
+                assert np.abs(q).max() <= RGB8_MAX_LSB
+            else:
+                assert image is None and rgb8 is None
+
+
+def test_disable_compositing_shows_only_root_brick(cuda_device, oracle_lib):
+    """Negative test (engine.py:172 analog): without compositing the frame is rank 0's brick alone."""
+    s = c1(P=2, W=96, H=96)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, _ = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H)
+    order = s.dec.visibility_order(s.cam.position)
+
+    def body(ep):
+        b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda_device).generate(s.field)
+        res = VolumeRenderer(ep, b, s.dec, s.tf, s.background).render(
+            s.cam, s.W, s.H, RenderOptions(disable_compositing=True, keep_float=True))
+        torch.cuda.synchronize()
+        return res.image
+
+    img = run_collective(2, body, device=cuda_device)[0]
+    solo = oracle.composite(ref, [0], s.background)
+    full = oracle.composite(ref, order, s.background)
+    assert np.abs(img - solo).max() <= RGBA_ATOL
+    assert np.abs(img - full).max() > 0.01
+
+
+def _api_frame(ep, cuda_device, W, H, composite="auto", fov=45.0):
+    d = Device(ep, cuda_device)
+    sf = d.create("spatialField")
+    sf.set_param("dims", (64, 64, 64))
+    sf.commit()
+    tf = d.create("transferFunction1D")
+    tf.commit()
+    vol = d.create("volume")
+    vol.set_param("field", sf)
+    vol.set_param("transferFunction", tf)
+    vol.commit()
+    world = d.create("world")
+    world.set_param("volumes", [vol])
+    world.commit()
+    from paper_2501_01628_b200.geom import auto_camera
+
+    c = auto_camera(world.decomposition.field.bounds(), W, H)
+    cam = d.create("camera")
+    cam.set_param("position", c.position)
+    cam.set_param("direction", c.view_dir)
+    cam.set_param("fovY", fov)
+    cam.set_param("aspect", W / H)
+    cam.commit()
+    rend = d.create("renderer")
+    rend.set_param("background", (0.05, 0.06, 0.08))
+    rend.set_param("composite", composite)
+    rend.commit()
+    frame = d.create("frame")
+    frame.set_param("world", world)
+    frame.set_param("camera", cam)
+    frame.set_param("renderer", rend)
+    frame.set_param("size", (W, H))
+    frame.commit()
+    return frame, cam, world
+
+
+@pytest.mark.parametrize("R,mode", [(1, "auto"), (2, "direct_send"), (4, "p2p")])
+def test_api_frame_matches_oracle_and_staging(cuda_device, oracle_lib, R, mode):
+    """Device/World/Frame -> render_frame_collective -> map_frame (api.py:329-371) on R rank threads."""
+    W, H = 96, 72
+
+    def body(ep):
+        frame, cam, world = _api_frame(ep, cuda_device, W, H, mode)
+        frame.render()
+        first = map_frame(frame)
+        pix1 = first.pixels if ep.rank == 0 else None
+        cam.set_param("fovY", 60.0)  # staged only
+        frame.render()
+        pix2 = map_frame(frame).pixels if ep.rank == 0 else None
+        stale = first.valid if ep.rank == 0 else None
+        cam.commit()
+        frame.render()
+        pix3 = map_frame(frame).pixels if ep.rank == 0 else None
+        return pix1, pix2, pix3, stale, world.decomposition.boxes
+
+    res = run_collective(R, body, device=cuda_device)
+    pix1, pix2, pix3, stale, boxes = res[0]
+    assert pix1 == pix2 and pix1 != pix3 and stale is False
+    # frame 1 against the oracle
+    from paper_2501_01628_b200.geom import auto_camera
+    from paper_2501_01628_b200.volume import blob_field, decompose, default_tf
+
+    f = blob_field((64, 64, 64))
+    dec = decompose(f, R)
+    assert dec.boxes == boxes
+    c = auto_camera(f.bounds(), W, H)
+    from paper_2501_01628_b200.geom import CameraSpec
+
+    cam = CameraSpec(c.position, c.view_dir, (0.0, 1.0, 0.0), 45.0, W / H)
+    vox = oracle.generate_field(f.dims, f.blobs)
+    ref, _ = oracle_partials(vox, dec, cam, default_tf(), 1.0, 0.99, W, H)
+    want = oracle.tone_map_rgb8(oracle.composite(ref, dec.visibility_order(cam.position), (0.05, 0.06, 0.08)))
+    got = np.frombuffer(pix1, np.uint8).reshape(H, W, 3)
+    assert np.abs(got.astype(np.int16) - want.astype(np.int16)).max() <= RGB8_MAX_LSB
