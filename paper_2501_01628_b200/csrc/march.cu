@@ -72,7 +72,8 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
 }
 
 constexpr int kRefillBelow = 20;  // refill a warp's idle lanes once fewer than this many are marching
-constexpr int kStepsPerCheck = 4;
+constexpr int kMaxSampleSteps = 16;   // phase-B steps between run refreshes
+constexpr int kMinSamplingLanes = 12;  // leave phase B once fewer lanes than this can sample
 
 // Pass 1: exact ray setup, zero-fill of pixels that miss the brick, compaction of the ones that hit.
 __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchArgs a) {
@@ -169,14 +170,15 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
             act = __ballot_sync(0xffffffffu, have);
         }
         if (act == 0) break;
-        for (int s = 0; have && s < kStepsPerCheck; ++s) {
-            if (j >= nn) {
-                a.out[pix] = make_float4(C0, C1, C2, A);
-                have = false;
-                break;
-            }
-            if (j >= jend) {
-                // Which macrocell holds sample j, and how far the empty region around it extends.
+        // Phase A (batched): lanes whose non-empty run is used up locate the next one -- consult the
+        // skip distance of the macrocell holding sample j, hop over empty cubes, or finish the ray.
+        if (have && j >= jend) {
+            while (true) {
+                if (j >= nn) {
+                    a.out[pix] = make_float4(C0, C1, C2, A);
+                    have = false;
+                    break;
+                }
                 const float fj = (float)j;
                 const int mx = clampi(__float2int_rd(fmaf(fj, st[0], p0[0])), 0, chx) >> kMacroShift;
                 const int my = clampi(__float2int_rd(fmaf(fj, st[1], p0[1])), 0, chy) >> kMacroShift;
@@ -194,55 +196,62 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
                     je = fminf(je, ((float)((st[2] > 0.f ? mz + r : mz - r + 1) << kMacroShift) - p0[2]) * ist[2]);
                 int jn = je < (float)nn ? (int)ceilf(je) : nn;
                 if (jn <= j) jn = j + 1;
-                if (dist > 0) {
-                    j = jn;
-                    continue;
+                if (dist == 0) {
+                    jend = jn;
+                    break;
                 }
-                jend = jn;
+                j = jn;
             }
-            const float fs = (float)j;
-            const float ux = fmaf(fs, st[0], p0[0]);
-            const float uy = fmaf(fs, st[1], p0[1]);
-            const float uz = fmaf(fs, st[2], p0[2]);
-            const int ix = min(__float2int_rd(fmaxf(ux, 0.f)), chx);
-            const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
-            const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
-            const float wx = __saturatef(ux - (float)ix);
-            const float wy = __saturatef(uy - (float)iy);
-            const float wz = __saturatef(uz - (float)iz);
-#if DPRT_QUAD
-            // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
-            const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-            const float4 qa = __ldg(q), qb = __ldg(q + sz);
-            const float v000 = qa.x, v100 = qa.y, v010 = qa.z, v110 = qa.w;
-            const float v001 = qb.x, v101 = qb.y, v011 = qb.z, v111 = qb.w;
-#else
-            const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-            const float v000 = __ldg(p), v100 = __ldg(p + 1);
-            const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
-            const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
-            const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
-#endif
-            const float c00 = fmaf(wx, v100 - v000, v000);
-            const float c10 = fmaf(wx, v110 - v010, v010);
-            const float c01 = fmaf(wx, v101 - v001, v001);
-            const float c11 = fmaf(wx, v111 - v011, v011);
-            const float c0 = fmaf(wy, c10 - c00, c00);
-            const float c1 = fmaf(wy, c11 - c01, c01);
-            const float v = fmaf(wz, c1 - c0, c0);
-            // transfer function
-            const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
-            const int ti = min((int)x, tmax);
-            const float tfr = x - (float)ti;
-            const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
-            // front-to-back, premultiplied
-            const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
-            C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
-            C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
-            C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-            A += w;
-            ++j;
-            if (A >= ert) j = nn;  // early ray termination: finish at the next step
+        }
+        // Phase B: sample while most lanes still have samples left in their current non-empty run.
+        for (int s = 0; s < kMaxSampleSteps; ++s) {
+            const bool can = have && j < jend;
+            if (__popc(__ballot_sync(0xffffffffu, can)) < kMinSamplingLanes) break;
+            if (can) {
+                const float fs = (float)j;
+                const float ux = fmaf(fs, st[0], p0[0]);
+                const float uy = fmaf(fs, st[1], p0[1]);
+                const float uz = fmaf(fs, st[2], p0[2]);
+                const int ix = min(__float2int_rd(fmaxf(ux, 0.f)), chx);
+                const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
+                const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
+                const float wx = __saturatef(ux - (float)ix);
+                const float wy = __saturatef(uy - (float)iy);
+                const float wz = __saturatef(uz - (float)iz);
+    #if DPRT_QUAD
+                // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
+                const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+                const float4 qa = __ldg(q), qb = __ldg(q + sz);
+                const float v000 = qa.x, v100 = qa.y, v010 = qa.z, v110 = qa.w;
+                const float v001 = qb.x, v101 = qb.y, v011 = qb.z, v111 = qb.w;
+    #else
+                const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+                const float v000 = __ldg(p), v100 = __ldg(p + 1);
+                const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
+                const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
+                const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
+    #endif
+                const float c00 = fmaf(wx, v100 - v000, v000);
+                const float c10 = fmaf(wx, v110 - v010, v010);
+                const float c01 = fmaf(wx, v101 - v001, v001);
+                const float c11 = fmaf(wx, v111 - v011, v011);
+                const float c0 = fmaf(wy, c10 - c00, c00);
+                const float c1 = fmaf(wy, c11 - c01, c01);
+                const float v = fmaf(wz, c1 - c0, c0);
+                // transfer function
+                const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
+                const int ti = min((int)x, tmax);
+                const float tfr = x - (float)ti;
+                const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+                // front-to-back, premultiplied
+                const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+                C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+                C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+                C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+                A += w;
+                ++j;
+                if (A >= ert) j = jend = nn;  // early ray termination: phase A finishes the ray
+            }
         }
     }
 }
