@@ -204,9 +204,12 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
             }
         }
         // Phase B: sample while most lanes still have samples left in their current non-empty run.
+        const int n_have = __popc(__ballot_sync(0xffffffffu, have));
         for (int s = 0; s < kMaxSampleSteps; ++s) {
             const bool can = have && j < jend;
-            if (__popc(__ballot_sync(0xffffffffu, can)) < kMinSamplingLanes) break;
+            const int n_can = __popc(__ballot_sync(0xffffffffu, can));
+            // always progress; stop early only when lanes are waiting for phase A
+            if (n_can == 0 || (s > 0 && n_can < kMinSamplingLanes && n_can < n_have)) break;
             if (can) {
                 const float fs = (float)j;
                 const float ux = fmaf(fs, st[0], p0[0]);
