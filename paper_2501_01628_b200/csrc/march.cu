@@ -72,8 +72,7 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
 }
 
 constexpr int kRefillBelow = 20;  // refill a warp's idle lanes once fewer than this many are marching
-constexpr int kMaxSampleSteps = 16;   // phase-B steps between run refreshes
-constexpr int kMinSamplingLanes = 12;  // leave phase B once fewer lanes than this can sample
+constexpr int kStepsPerCheck = 4;     // march steps between refill checks
 
 // Pass 1: exact ray setup, zero-fill of pixels that miss the brick, compaction of the ones that hit.
 __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchArgs a) {
@@ -116,7 +115,10 @@ __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchA
 }
 
 // Pass 2: persistent warps march the queued rays.
-__global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs a) {
+#ifndef DPRT_MARCH_MINBLOCKS
+#define DPRT_MARCH_MINBLOCKS 6
+#endif
+__global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_kernel(const MarchArgs a) {
     // TF as (entry, next - entry) pairs: the lerp e0 + (e1 - e0) * f becomes one FMA per channel with the
     // identical rounding (the difference is formed once here instead of per sample).
     extern __shared__ float4 s_tf[];  // 2 * n_tf entries (dynamic)
@@ -135,11 +137,13 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
     const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
     const float* __restrict__ vox = a.vox;
     const float4* __restrict__ quad = a.quad;
+    const uint8_t* __restrict__ skipd = a.skipd;
+    const int mcd0 = a.mcd[0], mcd1 = a.mcd[1], skip = a.skip;
     const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
     const int tmax = a.n_tf - 2;
 
     bool have = false, exhausted = false;
-    int pix = 0, nn = 0, j = 0, jend = 0;
+    int pix = 0, nn = 0, j = 0;
     float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f}, ist[3] = {0.f, 0.f, 0.f};
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
     while (true) {
@@ -162,7 +166,6 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
                     pix = __float_as_int(r0.w);
                     nn = __float_as_int(r1.w);
                     j = 0;
-                    jend = 0;
                     C0 = C1 = C2 = A = 0.f;
                     have = true;
                 }
@@ -170,91 +173,73 @@ __global__ void __launch_bounds__(kTileX * kTileY) march_kernel(const MarchArgs 
             act = __ballot_sync(0xffffffffu, have);
         }
         if (act == 0) break;
-        // Phase A (batched): lanes whose non-empty run is used up locate the next one -- consult the
-        // skip distance of the macrocell holding sample j, hop over empty cubes, or finish the ray.
-        if (have && j >= jend) {
-            while (true) {
-                if (j >= nn) {
-                    a.out[pix] = make_float4(C0, C1, C2, A);
-                    have = false;
-                    break;
-                }
-                const float fj = (float)j;
-                const int mx = clampi(__float2int_rd(fmaf(fj, st[0], p0[0])), 0, chx) >> kMacroShift;
-                const int my = clampi(__float2int_rd(fmaf(fj, st[1], p0[1])), 0, chy) >> kMacroShift;
-                const int mz = clampi(__float2int_rd(fmaf(fj, st[2], p0[2])), 0, chz) >> kMacroShift;
-                const int dist = a.skip ? (int)__ldg(a.skipd + (mz * a.mcd[1] + my) * a.mcd[0] + mx) : 0;
-                // Exit of the cube of macrocells [m - r + 1, m + r] (r = max(dist, 1)): samples before it
-                // lie in that cube; for dist > 0 the whole cube is empty for this TF (exact skip).
-                const int r = dist > 0 ? dist : 1;
+        for (int s = 0; have && s < kStepsPerCheck; ++s) {
+            if (j >= nn) {
+                a.out[pix] = make_float4(C0, C1, C2, A);
+                have = false;
+                break;
+            }
+            const float fs = (float)j;
+            const float ux = fmaf(fs, st[0], p0[0]);
+            const float uy = fmaf(fs, st[1], p0[1]);
+            const float uz = fmaf(fs, st[2], p0[2]);
+            const int ix = min(__float2int_rd(fmaxf(ux, 0.f)), chx);
+            const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
+            const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
+            const int mx = ix >> kMacroShift, my = iy >> kMacroShift, mz = iz >> kMacroShift;
+            // The skip distance of this sample's macrocell and the cell corners are loaded together; an
+            // empty macrocell's sample would add exact zeros, so it is dropped and the ray jumps.
+            const int dist = skip ? (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) : 0;
+#if DPRT_QUAD
+            const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+            const float4 qa = __ldg(q), qb = __ldg(q + sz);
+#endif
+            if (dist > 0) {
+                // jump to the exit of the empty cube of macrocells [m - dist + 1, m + dist]
                 float je = 3.0e38f;
                 if (st[0] != 0.f)
-                    je = fminf(je, ((float)((st[0] > 0.f ? mx + r : mx - r + 1) << kMacroShift) - p0[0]) * ist[0]);
+                    je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0]);
                 if (st[1] != 0.f)
-                    je = fminf(je, ((float)((st[1] > 0.f ? my + r : my - r + 1) << kMacroShift) - p0[1]) * ist[1]);
+                    je = fminf(je, ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << kMacroShift) - p0[1]) * ist[1]);
                 if (st[2] != 0.f)
-                    je = fminf(je, ((float)((st[2] > 0.f ? mz + r : mz - r + 1) << kMacroShift) - p0[2]) * ist[2]);
-                int jn = je < (float)nn ? (int)ceilf(je) : nn;
-                if (jn <= j) jn = j + 1;
-                if (dist == 0) {
-                    jend = jn;
-                    break;
-                }
-                j = jn;
+                    je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2]);
+                const int jn = je < (float)nn ? (int)ceilf(je) : nn;
+                j = jn > j ? jn : j + 1;
+                continue;
             }
-        }
-        // Phase B: sample while most lanes still have samples left in their current non-empty run.
-        const int n_have = __popc(__ballot_sync(0xffffffffu, have));
-        for (int s = 0; s < kMaxSampleSteps; ++s) {
-            const bool can = have && j < jend;
-            const int n_can = __popc(__ballot_sync(0xffffffffu, can));
-            // always progress; stop early only when lanes are waiting for phase A
-            if (n_can == 0 || (s > 0 && n_can < kMinSamplingLanes && n_can < n_have)) break;
-            if (can) {
-                const float fs = (float)j;
-                const float ux = fmaf(fs, st[0], p0[0]);
-                const float uy = fmaf(fs, st[1], p0[1]);
-                const float uz = fmaf(fs, st[2], p0[2]);
-                const int ix = min(__float2int_rd(fmaxf(ux, 0.f)), chx);
-                const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
-                const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
-                const float wx = __saturatef(ux - (float)ix);
-                const float wy = __saturatef(uy - (float)iy);
-                const float wz = __saturatef(uz - (float)iz);
-    #if DPRT_QUAD
-                // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
-                const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-                const float4 qa = __ldg(q), qb = __ldg(q + sz);
-                const float v000 = qa.x, v100 = qa.y, v010 = qa.z, v110 = qa.w;
-                const float v001 = qb.x, v101 = qb.y, v011 = qb.z, v111 = qb.w;
-    #else
-                const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-                const float v000 = __ldg(p), v100 = __ldg(p + 1);
-                const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
-                const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
-                const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
-    #endif
-                const float c00 = fmaf(wx, v100 - v000, v000);
-                const float c10 = fmaf(wx, v110 - v010, v010);
-                const float c01 = fmaf(wx, v101 - v001, v001);
-                const float c11 = fmaf(wx, v111 - v011, v011);
-                const float c0 = fmaf(wy, c10 - c00, c00);
-                const float c1 = fmaf(wy, c11 - c01, c01);
-                const float v = fmaf(wz, c1 - c0, c0);
-                // transfer function
-                const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
-                const int ti = min((int)x, tmax);
-                const float tfr = x - (float)ti;
-                const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
-                // front-to-back, premultiplied
-                const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
-                C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
-                C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
-                C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-                A += w;
-                ++j;
-                if (A >= ert) j = jend = nn;  // early ray termination: phase A finishes the ray
-            }
+            const float wx = __saturatef(ux - (float)ix);
+            const float wy = __saturatef(uy - (float)iy);
+            const float wz = __saturatef(uz - (float)iz);
+#if DPRT_QUAD
+            const float v000 = qa.x, v100 = qa.y, v010 = qa.z, v110 = qa.w;
+            const float v001 = qb.x, v101 = qb.y, v011 = qb.z, v111 = qb.w;
+#else
+            const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+            const float v000 = __ldg(p), v100 = __ldg(p + 1);
+            const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
+            const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
+            const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
+#endif
+            const float c00 = fmaf(wx, v100 - v000, v000);
+            const float c10 = fmaf(wx, v110 - v010, v010);
+            const float c01 = fmaf(wx, v101 - v001, v001);
+            const float c11 = fmaf(wx, v111 - v011, v011);
+            const float c0 = fmaf(wy, c10 - c00, c00);
+            const float c1 = fmaf(wy, c11 - c01, c01);
+            const float v = fmaf(wz, c1 - c0, c0);
+            // transfer function
+            const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
+            const int ti = min((int)x, tmax);
+            const float tfr = x - (float)ti;
+            const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+            // front-to-back, premultiplied
+            const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+            C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+            C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+            C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+            A += w;
+            ++j;
+            if (A >= ert) j = nn;  // early ray termination: the next step finishes the ray
         }
     }
 }
