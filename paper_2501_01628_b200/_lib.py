@@ -102,7 +102,7 @@ def lib() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = Path(os.environ.get("DPRT_CUDA_LIB", str(LIB_PATH)))
+    path = Path(os.environ.get("DPRT_CUDA_LIB") or str(LIB_PATH)).resolve()
     if not path.exists():
         raise NativeLibraryMissing(
             f"{path} not built: run `python -m paper_2501_01628_b200.build` (there is no CPU fallback)")

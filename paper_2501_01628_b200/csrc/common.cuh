@@ -9,6 +9,12 @@
 #ifndef DPRT_QUAD
 #define DPRT_QUAD 1
 #endif
+#ifndef DPRT_SPEC_LOADS
+#define DPRT_SPEC_LOADS 0
+#endif
+#ifndef DPRT_MC_CACHE
+#define DPRT_MC_CACHE 1
+#endif
 
 namespace dprt {
 

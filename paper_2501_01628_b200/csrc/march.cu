@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
     const int tmax = a.n_tf - 2;
 
     bool have = false, exhausted = false;
-    int pix = 0, nn = 0, j = 0;
+    int pix = 0, nn = 0, j = 0, cur_mc = -1;
     float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f}, ist[3] = {0.f, 0.f, 0.f};
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
     while (true) {
@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                     pix = __float_as_int(r0.w);
                     nn = __float_as_int(r1.w);
                     j = 0;
+                    cur_mc = -1;
                     C0 = C1 = C2 = A = 0.f;
                     have = true;
                 }
@@ -187,10 +188,19 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
             const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
             const int mx = ix >> kMacroShift, my = iy >> kMacroShift, mz = iz >> kMacroShift;
-            // The skip distance of this sample's macrocell and the cell corners are loaded together; an
-            // empty macrocell's sample would add exact zeros, so it is dropped and the ray jumps.
-            const int dist = skip ? (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) : 0;
-#if DPRT_QUAD
+            // Skip distance of this sample's macrocell (re-read only when the sample leaves the last
+            // non-empty macrocell).  An empty macrocell's sample would add exact zeros: drop it and jump.
+            const int mc = (mz * mcd1 + my) * mcd0 + mx;
+            int dist = 0;
+#if DPRT_MC_CACHE
+            if (skip && mc != cur_mc) {
+                dist = (int)__ldg(skipd + mc);
+                if (dist == 0) cur_mc = mc;
+            }
+#else
+            if (skip) dist = (int)__ldg(skipd + mc);
+#endif
+#if DPRT_QUAD && DPRT_SPEC_LOADS
             const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
             const float4 qa = __ldg(q), qb = __ldg(q + sz);
 #endif
@@ -211,6 +221,10 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             const float wy = __saturatef(uy - (float)iy);
             const float wz = __saturatef(uz - (float)iz);
 #if DPRT_QUAD
+#if !DPRT_SPEC_LOADS
+            const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+            const float4 qa = __ldg(q), qb = __ldg(q + sz);
+#endif
             const float v000 = qa.x, v100 = qa.y, v010 = qa.z, v110 = qa.w;
             const float v001 = qb.x, v101 = qb.y, v011 = qb.z, v111 = qb.w;
 #else
