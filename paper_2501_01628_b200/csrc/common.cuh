@@ -13,7 +13,7 @@
 #define DPRT_SPEC_LOADS 0
 #endif
 #ifndef DPRT_MC_CACHE
-#define DPRT_MC_CACHE 1
+#define DPRT_MC_CACHE 0
 #endif
 
 namespace dprt {

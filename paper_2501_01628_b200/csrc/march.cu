@@ -71,8 +71,14 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
     return kb > ka ? kb - ka : 0;
 }
 
-constexpr int kRefillBelow = 20;  // refill a warp's idle lanes once fewer than this many are marching
-constexpr int kStepsPerCheck = 4;     // march steps between refill checks
+#ifndef DPRT_REFILL_BELOW
+#define DPRT_REFILL_BELOW 8
+#endif
+#ifndef DPRT_STEPS_PER_CHECK
+#define DPRT_STEPS_PER_CHECK 16
+#endif
+constexpr int kRefillBelow = DPRT_REFILL_BELOW;  // refill a warp's idle lanes once fewer than this many march
+constexpr int kStepsPerCheck = DPRT_STEPS_PER_CHECK;  // march steps between refill checks
 
 // Pass 1: exact ray setup, zero-fill of pixels that miss the brick, compaction of the ones that hit.
 __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchArgs a) {
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchA
 
 // Pass 2: persistent warps march the queued rays.
 #ifndef DPRT_MARCH_MINBLOCKS
-#define DPRT_MARCH_MINBLOCKS 6
+#define DPRT_MARCH_MINBLOCKS 4
 #endif
 __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_kernel(const MarchArgs a) {
     // TF as (entry, next - entry) pairs: the lerp e0 + (e1 - e0) * f becomes one FMA per channel with the
