@@ -308,7 +308,7 @@ def run_ours(args):
         cpu = cpu_baseline(vox, dec, cam, tf)
 
     if rank == 0:
-        launches = args.steps * (2 if R == 1 else 2)
+        launches = args.steps * 3  # ray_setup + march + composite per frame (plus one 8-byte memset)
         line = {
             "metric": METRIC, "value": fps * 1.0, "unit": UNIT, "n_gpus": R, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
