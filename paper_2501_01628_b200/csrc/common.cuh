@@ -9,11 +9,8 @@
 #ifndef DPRT_QUAD
 #define DPRT_QUAD 1
 #endif
-#ifndef DPRT_SPEC_LOADS
-#define DPRT_SPEC_LOADS 0
-#endif
-#ifndef DPRT_MC_CACHE
-#define DPRT_MC_CACHE 0
+#ifndef DPRT_PAIR
+#define DPRT_PAIR 1
 #endif
 
 namespace dprt {

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
     const int tmax = a.n_tf - 2;
 
     bool have = false, exhausted = false;
-    int pix = 0, nn = 0, j = 0, cur_mc = -1;
+    int pix = 0, nn = 0, j = 0;
     float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f}, ist[3] = {0.f, 0.f, 0.f};
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
     while (true) {
@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                     pix = __float_as_int(r0.w);
                     nn = __float_as_int(r1.w);
                     j = 0;
-                    cur_mc = -1;
                     C0 = C1 = C2 = A = 0.f;
                     have = true;
                 }
@@ -194,22 +193,10 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
             const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
             const int mx = ix >> kMacroShift, my = iy >> kMacroShift, mz = iz >> kMacroShift;
-            // Skip distance of this sample's macrocell (re-read only when the sample leaves the last
-            // non-empty macrocell).  An empty macrocell's sample would add exact zeros: drop it and jump.
+            // Skip distance of this sample's macrocell.  An empty macrocell's sample would add exact
+            // zeros: drop it and jump over the empty cube around it.
             const int mc = (mz * mcd1 + my) * mcd0 + mx;
-            int dist = 0;
-#if DPRT_MC_CACHE
-            if (skip && mc != cur_mc) {
-                dist = (int)__ldg(skipd + mc);
-                if (dist == 0) cur_mc = mc;
-            }
-#else
-            if (skip) dist = (int)__ldg(skipd + mc);
-#endif
-#if DPRT_QUAD && DPRT_SPEC_LOADS
-            const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-            const float4 qa = __ldg(q), qb = __ldg(q + sz);
-#endif
+            const int dist = skip ? (int)__ldg(skipd + mc) : 0;
             if (dist > 0) {
                 // jump to the exit of the empty cube of macrocells [m - dist + 1, m + dist]
                 float je = 3.0e38f;
@@ -223,43 +210,70 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                 j = jn > j ? jn : j + 1;
                 continue;
             }
-            const float wx = __saturatef(ux - (float)ix);
-            const float wy = __saturatef(uy - (float)iy);
-            const float wz = __saturatef(uz - (float)iz);
+            // trilinear + TF (§2.6) + front-to-back blend (§2.7) of one sample
+            auto shade = [&](float4 qa, float4 qb, float wx, float wy, float wz) {
+                const float c00 = fmaf(wx, qa.y - qa.x, qa.x);
+                const float c10 = fmaf(wx, qa.w - qa.z, qa.z);
+                const float c01 = fmaf(wx, qb.y - qb.x, qb.x);
+                const float c11 = fmaf(wx, qb.w - qb.z, qb.z);
+                const float c0 = fmaf(wy, c10 - c00, c00);
+                const float c1 = fmaf(wy, c11 - c01, c01);
+                const float v = fmaf(wz, c1 - c0, c0);
+                const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
+                const int ti = min((int)x, tmax);
+                const float tfr = x - (float)ti;
+                const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+                const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+                C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+                C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+                C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+                A += w;
+            };
 #if DPRT_QUAD
-#if !DPRT_SPEC_LOADS
+            // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
             const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
             const float4 qa = __ldg(q), qb = __ldg(q + sz);
-#endif
-            const float v000 = qa.x, v100 = qa.y, v010 = qa.z, v110 = qa.w;
-            const float v001 = qb.x, v101 = qb.y, v011 = qb.z, v111 = qb.w;
 #else
             const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-            const float v000 = __ldg(p), v100 = __ldg(p + 1);
-            const float v010 = __ldg(p + sy), v110 = __ldg(p + sy + 1);
-            const float v001 = __ldg(p + sz), v101 = __ldg(p + sz + 1);
-            const float v011 = __ldg(p + sz + sy), v111 = __ldg(p + sz + sy + 1);
+            const float4 qa = make_float4(__ldg(p), __ldg(p + 1), __ldg(p + sy), __ldg(p + sy + 1));
+            const float4 qb = make_float4(__ldg(p + sz), __ldg(p + sz + 1), __ldg(p + sz + sy), __ldg(p + sz + sy + 1));
 #endif
-            const float c00 = fmaf(wx, v100 - v000, v000);
-            const float c10 = fmaf(wx, v110 - v010, v010);
-            const float c01 = fmaf(wx, v101 - v001, v001);
-            const float c11 = fmaf(wx, v111 - v011, v011);
-            const float c0 = fmaf(wy, c10 - c00, c00);
-            const float c1 = fmaf(wy, c11 - c01, c01);
-            const float v = fmaf(wz, c1 - c0, c0);
-            // transfer function
-            const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
-            const int ti = min((int)x, tmax);
-            const float tfr = x - (float)ti;
-            const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
-            // front-to-back, premultiplied
-            const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
-            C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
-            C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
-            C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-            A += w;
+#if DPRT_PAIR && DPRT_QUAD
+            // Second sample of the step (j + 1) when it is still in a non-empty macrocell: its corner
+            // loads are issued before the first sample is shaded, doubling memory-level parallelism.
+            const float fs1 = fs + 1.f;
+            const float vx1 = fmaf(fs1, st[0], p0[0]);
+            const float vy1 = fmaf(fs1, st[1], p0[1]);
+            const float vz1 = fmaf(fs1, st[2], p0[2]);
+            const int jx1 = min(__float2int_rd(fmaxf(vx1, 0.f)), chx);
+            const int jy1 = min(__float2int_rd(fmaxf(vy1, 0.f)), chy);
+            const int jz1 = min(__float2int_rd(fmaxf(vz1, 0.f)), chz);
+            const int mc1 = ((jz1 >> kMacroShift) * mcd1 + (jy1 >> kMacroShift)) * mcd0 + (jx1 >> kMacroShift);
+            bool two = j + 1 < nn;
+            if (two && skip && mc1 != mc) two = __ldg(skipd + mc1) == 0;
+            float4 qa1 = qa, qb1 = qb;
+            if (two) {
+                const float4* q1 = quad + ((unsigned)jz1 * sz + (unsigned)jy1 * sy + (unsigned)jx1);
+                qa1 = __ldg(q1);
+                qb1 = __ldg(q1 + sz);
+            }
+            shade(qa, qb, __saturatef(ux - (float)ix), __saturatef(uy - (float)iy), __saturatef(uz - (float)iz));
+            ++j;
+            if (A >= ert) {  // early ray termination: the next step finishes the ray
+                j = nn;
+                continue;
+            }
+            if (two) {
+                shade(qa1, qb1, __saturatef(vx1 - (float)jx1), __saturatef(vy1 - (float)jy1),
+                      __saturatef(vz1 - (float)jz1));
+                ++j;
+                if (A >= ert) j = nn;
+            }
+#else
+            shade(qa, qb, __saturatef(ux - (float)ix), __saturatef(uy - (float)iy), __saturatef(uz - (float)iz));
             ++j;
             if (A >= ert) j = nn;  // early ray termination: the next step finishes the ray
+#endif
         }
     }
 }
