@@ -10,7 +10,7 @@
 #define DPRT_QUAD 1
 #endif
 #ifndef DPRT_PAIR
-#define DPRT_PAIR 1
+#define DPRT_PAIR 0
 #endif
 
 namespace dprt {

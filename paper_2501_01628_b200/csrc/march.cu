@@ -355,6 +355,9 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = 2 * a.n_tf * sizeof(float4);
+#ifdef DPRT_CARVEOUT
+    cudaFuncSetAttribute(march_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, DPRT_CARVEOUT);
+#endif
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, kTileX * kTileY, smem);
     if (per_sm < 1) per_sm = 1;
     march_kernel<<<sms * per_sm, block, smem, stream>>>(a);
