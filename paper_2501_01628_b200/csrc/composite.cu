@@ -17,51 +17,71 @@ __device__ __forceinline__ unsigned tone8(float x) {
     return (unsigned)floorf(fminf(fmaxf(x, 0.f), 1.f) * 255.f + 0.5f);
 }
 
-__device__ __forceinline__ float4 blend_pixel(const CompositeArgs& a, long long i) {
-    float4 acc = __ldg(a.in[0] + i);
-    for (int p = 1; p < a.P; ++p) {
-        const float4 f = __ldg(a.in[p] + i);
-        const float one = 1.f - acc.w;
-        acc.x = fmaf(one, f.x, acc.x);
-        acc.y = fmaf(one, f.y, acc.y);
-        acc.z = fmaf(one, f.z, acc.z);
-        acc.w = fmaf(one, f.w, acc.w);
-    }
-    return acc;
+__device__ __forceinline__ void over(float4& acc, const float4 f) {
+    const float one = 1.f - acc.w;
+    acc.x = fmaf(one, f.x, acc.x);
+    acc.y = fmaf(one, f.y, acc.y);
+    acc.z = fmaf(one, f.z, acc.z);
+    acc.w = fmaf(one, f.w, acc.w);
 }
 
-// Each thread composites 4 consecutive pixels so the RGB8 output is three aligned 32-bit stores.
+__device__ __forceinline__ uint32_t pack_rgb8(const float4 c, const float bg[3], int ch) {
+    const float one = 1.f - c.w;
+    const float v = ch == 0 ? fmaf(one, bg[0], c.x) : (ch == 1 ? fmaf(one, bg[1], c.y) : fmaf(one, bg[2], c.z));
+    return tone8(v);
+}
+
+// Each thread composites 4 consecutive pixels: per fragment it issues the four 16-byte loads together
+// (and the next fragment's before blending, via unrolling), so P fragments keep 4-8 loads in flight;
+// the 12 RGB8 bytes leave as three aligned 32-bit stores.
 __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long i0 = q * 4;
     if (i0 >= a.npix) return;
-    const int cnt = (int)min(4LL, a.npix - i0);
-    unsigned char px[12];
-    for (int k = 0; k < cnt; ++k) {
-        const float4 c = blend_pixel(a, i0 + k);
-        if (a.flags & DPRT_COMPOSITE_RGBA) a.rgba[i0 + k] = c;
-        if (a.flags & DPRT_COMPOSITE_TONEMAP) {
-            const float one = 1.f - c.w;
-            px[3 * k + 0] = (unsigned char)tone8(fmaf(one, a.bg[0], c.x));
-            px[3 * k + 1] = (unsigned char)tone8(fmaf(one, a.bg[1], c.y));
-            px[3 * k + 2] = (unsigned char)tone8(fmaf(one, a.bg[2], c.z));
-        }
-    }
-    if (a.flags & DPRT_COMPOSITE_TONEMAP) {
-        uint8_t* dst = a.rgb8 + 3 * i0;
-        if (cnt == 4 && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
-            uint32_t w[3];
+    if (i0 + 4 <= a.npix) {
+        float4 acc[4];
+        const float4* f0 = a.in[0] + i0;
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
-                w[k] = (uint32_t)px[4 * k] | ((uint32_t)px[4 * k + 1] << 8) | ((uint32_t)px[4 * k + 2] << 16) |
-                       ((uint32_t)px[4 * k + 3] << 24);
-            uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-            d32[0] = w[0];
-            d32[1] = w[1];
-            d32[2] = w[2];
-        } else {
-            for (int k = 0; k < 3 * cnt; ++k) dst[k] = px[k];
+        for (int k = 0; k < 4; ++k) acc[k] = __ldg(f0 + k);
+#pragma unroll 2
+        for (int p = 1; p < a.P; ++p) {
+            const float4* fp = a.in[p] + i0;
+            float4 f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) f[k] = __ldg(fp + k);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) over(acc[k], f[k]);
         }
+        if (a.flags & DPRT_COMPOSITE_RGBA) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) a.rgba[i0 + k] = acc[k];
+        }
+        if (a.flags & DPRT_COMPOSITE_TONEMAP) {
+            uint32_t b[12];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) b[3 * k + ch] = pack_rgb8(acc[k], a.bg, ch);
+            uint8_t* dst = a.rgb8 + 3 * i0;
+            if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+#pragma unroll
+                for (int w = 0; w < 3; ++w)
+                    d32[w] = b[4 * w] | (b[4 * w + 1] << 8) | (b[4 * w + 2] << 16) | (b[4 * w + 3] << 24);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 12; ++k) dst[k] = (uint8_t)b[k];
+            }
+        }
+        return;
+    }
+    // tail: fewer than 4 pixels left
+    for (long long i = i0; i < a.npix; ++i) {
+        float4 acc = __ldg(a.in[0] + i);
+        for (int p = 1; p < a.P; ++p) over(acc, __ldg(a.in[p] + i));
+        if (a.flags & DPRT_COMPOSITE_RGBA) a.rgba[i] = acc;
+        if (a.flags & DPRT_COMPOSITE_TONEMAP)
+            for (int ch = 0; ch < 3; ++ch) a.rgb8[3 * i + ch] = (uint8_t)pack_rgb8(acc, a.bg, ch);
     }
 }
 
