@@ -134,7 +134,11 @@ int dprt_ipc_open(int device, const uint8_t handle[64], void** out_ptr);
 int dprt_ipc_close(int device, void* ptr);
 int dprt_enable_peer(int device, int peer);
 
-/* Stream-ordered helpers for the host driver (no torch types): device sync and an event timer. */
+/* Instrumented builds (-DDPRT_COUNTERS=1) count {shaded samples, contributing samples, skip steps, rays}
+ * in march_kernel; other builds report zeros. */
+int dprt_march_counters(int device, uint64_t out[4], int reset);
+
+/* Stream-ordered helpers for the host driver (no torch types): device sync. */
 int dprt_device_synchronize(int device);
 
 #ifdef __cplusplus

@@ -36,7 +36,7 @@ EXPORTS = (
     "dprt_brick_create", "dprt_brick_stored", "dprt_brick_upload", "dprt_brick_download",
     "dprt_brick_generate", "dprt_brick_build_macrocells", "dprt_brick_destroy", "dprt_brick_footprint",
     "dprt_march", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
-    "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free",
+    "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters",
 )
 
 c_double3 = ctypes.c_double * 3
@@ -90,6 +90,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_enable_peer": ([I, I], I),
         "dprt_device_alloc": ([I, ctypes.c_uint64, P], I),
         "dprt_device_free": ([I, P], I),
+        "dprt_march_counters": ([I, P, I], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -19,6 +19,7 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
 cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cudaStream_t stream);
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream);
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream);
+cudaError_t read_counters(unsigned long long out[4], int reset);
 }  // namespace dprt
 
 struct DprtBrick : dprt::DeviceBrick {};
@@ -371,6 +372,16 @@ int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, 
     a.rgb8 = rgb8;
     a.rgba = reinterpret_cast<float4*>(rgba_out);
     CK(dprt::launch_composite(a, (cudaStream_t)stream), "composite kernel launch");
+    return DPRT_OK;
+}
+
+int dprt_march_counters(int device, uint64_t out[4], int reset) {
+    if (!out) return fail(DPRT_E_USAGE, "null output");
+    int rc = bind(device);
+    if (rc) return rc;
+    unsigned long long tmp[4];
+    CK(dprt::read_counters(tmp, reset), "march counters");
+    for (int i = 0; i < 4; ++i) out[i] = tmp[i];
     return DPRT_OK;
 }
 

@@ -9,14 +9,20 @@
 #ifndef DPRT_QUAD
 #define DPRT_QUAD 1
 #endif
+#ifndef DPRT_COUNTERS
+#define DPRT_COUNTERS 0
+#endif
 #ifndef DPRT_PAIR
 #define DPRT_PAIR 0
 #endif
 
 namespace dprt {
 
-constexpr int kMacro = 8;          // macrocell edge in cells (empty-space skipping granularity)
-constexpr int kMacroShift = 3;
+#ifndef DPRT_MACRO_SHIFT
+#define DPRT_MACRO_SHIFT 3
+#endif
+constexpr int kMacroShift = DPRT_MACRO_SHIFT;
+constexpr int kMacro = 1 << kMacroShift;  // macrocell edge in cells (empty-space skipping granularity)
 constexpr int kTileX = 16;         // marcher CTA screen tile: 16 x 16 pixels, warps are 8 x 4 pixel tiles
 constexpr int kTileY = 16;
 constexpr int kMaxTf = 1024;       // transfer-function entries held in shared memory

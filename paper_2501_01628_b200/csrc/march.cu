@@ -24,6 +24,13 @@
 
 namespace dprt {
 
+#if DPRT_COUNTERS
+__device__ unsigned long long g_counters[4];  // shaded samples, contributing samples, skip steps, rays
+#define DPRT_COUNT(i, v) atomicAdd(&g_counters[i], (unsigned long long)(v))
+#else
+#define DPRT_COUNT(i, v) ((void)0)
+#endif
+
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // geom.py:240-259 with every f64 op explicitly rounded (no FMA contraction), matching dvr_oracle.c.
@@ -150,6 +157,9 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 
     bool have = false, exhausted = false;
     int pix = 0, nn = 0, j = 0;
+#if DPRT_COUNTERS
+    unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
+#endif
     float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f}, ist[3] = {0.f, 0.f, 0.f};
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
     while (true) {
@@ -174,11 +184,22 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                     j = 0;
                     C0 = C1 = C2 = A = 0.f;
                     have = true;
+#if DPRT_COUNTERS
+                    ++c_rays;
+#endif
                 }
             }
             act = __ballot_sync(0xffffffffu, have);
         }
-        if (act == 0) break;
+        if (act == 0) {
+#if DPRT_COUNTERS
+            DPRT_COUNT(0, c_shade);
+            DPRT_COUNT(1, c_contrib);
+            DPRT_COUNT(2, c_skip);
+            DPRT_COUNT(3, c_rays);
+#endif
+            break;
+        }
         for (int s = 0; have && s < kStepsPerCheck; ++s) {
             if (j >= nn) {
                 a.out[pix] = make_float4(C0, C1, C2, A);
@@ -208,6 +229,9 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                     je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2]);
                 const int jn = je < (float)nn ? (int)ceilf(je) : nn;
                 j = jn > j ? jn : j + 1;
+#if DPRT_COUNTERS
+                ++c_skip;
+#endif
                 continue;
             }
             // trilinear + TF (§2.6) + front-to-back blend (§2.7) of one sample
@@ -224,6 +248,10 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                 const float tfr = x - (float)ti;
                 const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
                 const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+#if DPRT_COUNTERS
+                ++c_shade;
+                c_contrib += w > 0.f;
+#endif
                 C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
                 C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
                 C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
@@ -340,6 +368,21 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
     skip_pass_kernel<<<grid, block, 0, stream>>>(tmp, b.skipd, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 1);
     skip_pass_kernel<<<grid, block, 0, stream>>>(b.skipd, tmp, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 0);
     return cudaMemcpyAsync(b.skipd, tmp, (size_t)nmc, cudaMemcpyDeviceToDevice, stream);
+}
+
+cudaError_t read_counters(unsigned long long out[4], int reset) {
+#if DPRT_COUNTERS
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_counters, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        e = cudaMemcpyToSymbol(g_counters, z, sizeof(z));
+    }
+    return e;
+#else
+    for (int i = 0; i < 4; ++i) out[i] = 0;
+    (void)reset;
+    return cudaSuccess;
+#endif
 }
 
 // Host launchers (called from abi.cu).

@@ -45,3 +45,11 @@ a = p.view(-1, 4)[:, 3]
 print(f"edge {args.edge} {args.W}x{args.H} skip={not args.no_skip}: march {ms:.4f} ms; rays hitting brick {hit}, "
       f"owned samples {owned} ({owned / max(hit, 1):.0f}/ray); pixels A>=0.99: {int((a >= 0.99).sum())}, "
       f"A>0: {int((a > 0).sum())}; {owned / ms / 1e6:.1f} G owned samples/s")
+import ctypes
+from paper_2501_01628_b200 import _lib
+cnt = (ctypes.c_uint64 * 4)()
+_lib.check(_lib.lib().dprt_march_counters(0, cnt, 1), "counters")
+if any(cnt):
+    launches = args.iters + 4
+    print("per frame: shaded samples %.1fM, contributing %.1fM, skip steps %.1fM, rays %.0fK" %
+          tuple(v / launches / s for v, s in zip(cnt, (1e6, 1e6, 1e6, 1e3))))
