@@ -86,6 +86,11 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
 #endif
 constexpr int kRefillBelow = DPRT_REFILL_BELOW;  // refill a warp's idle lanes once fewer than this many march
 constexpr int kStepsPerCheck = DPRT_STEPS_PER_CHECK;  // march steps between refill checks
+#ifndef DPRT_ASYNC_DEPTH
+#define DPRT_ASYNC_DEPTH 4
+#endif
+constexpr int kDepth = DPRT_ASYNC_DEPTH;  // cp.async samples in flight per lane (DPRT_ASYNC)
+constexpr int kThreads = kTileX * kTileY;
 
 // Pass 1: exact ray setup, zero-fill of pixels that miss the brick, compaction of the ones that hit.
 __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchArgs a) {
@@ -157,6 +162,10 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 
     bool have = false, exhausted = false;
     int pix = 0, nn = 0, j = 0;
+#if DPRT_ASYNC
+    int jend = 0, jpf = 0;  // [j, jend): verified non-empty run; [j, jpf): samples whose copies are issued
+    const unsigned ring = (unsigned)__cvta_generic_to_shared(s_tf + 2 * a.n_tf) + (unsigned)tid * 16u;
+#endif
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
@@ -182,6 +191,9 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                     pix = __float_as_int(r0.w);
                     nn = __float_as_int(r1.w);
                     j = 0;
+#if DPRT_ASYNC
+                    jend = jpf = 0;
+#endif
                     C0 = C1 = C2 = A = 0.f;
                     have = true;
 #if DPRT_COUNTERS
@@ -200,6 +212,109 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 #endif
             break;
         }
+#if DPRT_ASYNC
+        for (int s = 0; have && s < kStepsPerCheck; ++s) {
+            if (j >= nn) {
+                asm volatile("cp.async.wait_all;\n" ::: "memory");  // no copy may land in a reused slot
+                a.out[pix] = make_float4(C0, C1, C2, A);
+                have = false;
+                break;
+            }
+            if (j >= jend) {
+                // Start of a run: locate the macrocell of sample j; hop over empty cubes.
+                const float fj = (float)j;
+                const int mx = min(__float2int_rd(fmaxf(fmaf(fj, st[0], p0[0]), 0.f)), chx) >> kMacroShift;
+                const int my = min(__float2int_rd(fmaxf(fmaf(fj, st[1], p0[1]), 0.f)), chy) >> kMacroShift;
+                const int mz = min(__float2int_rd(fmaxf(fmaf(fj, st[2], p0[2]), 0.f)), chz) >> kMacroShift;
+                const int dist = skip ? (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) : 0;
+                const int r = dist > 0 ? dist : 1;
+                float je = 3.0e38f;
+                if (st[0] != 0.f)
+                    je = fminf(je, ((float)((st[0] > 0.f ? mx + r : mx - r + 1) << kMacroShift) - p0[0]) * ist[0]);
+                if (st[1] != 0.f)
+                    je = fminf(je, ((float)((st[1] > 0.f ? my + r : my - r + 1) << kMacroShift) - p0[1]) * ist[1]);
+                if (st[2] != 0.f)
+                    je = fminf(je, ((float)((st[2] > 0.f ? mz + r : mz - r + 1) << kMacroShift) - p0[2]) * ist[2]);
+                int jn = je < (float)nn ? (int)ceilf(je) : nn;
+                if (jn <= j) jn = j + 1;
+#if DPRT_COUNTERS
+                if (dist > 0) ++c_skip;
+#endif
+                if (dist > 0) {
+                    j = jpf = jn;  // empty cube: its samples would add exact zeros
+                    continue;
+                }
+                jend = jn;
+                jpf = j;
+            }
+            // Keep up to kDepth samples of the run in flight: cp.async copies the two corner quads of each
+            // into this lane's ring slot in shared memory -- no registers held while the loads are out.
+            while (jpf < jend && jpf < j + kDepth) {
+                const float fp = (float)jpf;
+                const int px_ = min(__float2int_rd(fmaxf(fmaf(fp, st[0], p0[0]), 0.f)), chx);
+                const int py_ = min(__float2int_rd(fmaxf(fmaf(fp, st[1], p0[1]), 0.f)), chy);
+                const int pz_ = min(__float2int_rd(fmaxf(fmaf(fp, st[2], p0[2]), 0.f)), chz);
+                const float4* q = quad + ((unsigned)pz_ * sz + (unsigned)py_ * sy + (unsigned)px_);
+                const unsigned slot = (unsigned)(jpf % kDepth);
+                const unsigned dst = ring + (slot * 2u * kThreads) * 16u;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(q) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst + kThreads * 16u), "l"(q + sz)
+                             : "memory");
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+                ++jpf;
+            }
+            // wait for sample j's group: (jpf - j - 1) younger groups may still be in flight
+            switch (jpf - j - 1) {
+                case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+                case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+                case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+                case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+                case 4: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
+                case 5: asm volatile("cp.async.wait_group 5;\n" ::: "memory"); break;
+                case 6: asm volatile("cp.async.wait_group 6;\n" ::: "memory"); break;
+                default: asm volatile("cp.async.wait_group 7;\n" ::: "memory"); break;
+            }
+            const unsigned slot = (unsigned)(j % kDepth);
+            float4 qa, qb;
+            {
+                const unsigned src = ring + (slot * 2u * kThreads) * 16u;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                             : "=f"(qa.x), "=f"(qa.y), "=f"(qa.z), "=f"(qa.w) : "r"(src) : "memory");
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                             : "=f"(qb.x), "=f"(qb.y), "=f"(qb.z), "=f"(qb.w) : "r"(src + kThreads * 16u) : "memory");
+            }
+            const float fs = (float)j;
+            const float ux = fmaf(fs, st[0], p0[0]);
+            const float uy = fmaf(fs, st[1], p0[1]);
+            const float uz = fmaf(fs, st[2], p0[2]);
+            const float wx = __saturatef(ux - (float)min(__float2int_rd(fmaxf(ux, 0.f)), chx));
+            const float wy = __saturatef(uy - (float)min(__float2int_rd(fmaxf(uy, 0.f)), chy));
+            const float wz = __saturatef(uz - (float)min(__float2int_rd(fmaxf(uz, 0.f)), chz));
+            // trilinear + TF (§2.6) + front-to-back blend (§2.7)
+            const float c00 = fmaf(wx, qa.y - qa.x, qa.x);
+            const float c10 = fmaf(wx, qa.w - qa.z, qa.z);
+            const float c01 = fmaf(wx, qb.y - qb.x, qb.x);
+            const float c11 = fmaf(wx, qb.w - qb.z, qb.z);
+            const float c0 = fmaf(wy, c10 - c00, c00);
+            const float c1 = fmaf(wy, c11 - c01, c01);
+            const float v = fmaf(wz, c1 - c0, c0);
+            const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
+            const int ti = min((int)x, tmax);
+            const float tfr = x - (float)ti;
+            const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+            const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+#if DPRT_COUNTERS
+            ++c_shade;
+            c_contrib += w > 0.f;
+#endif
+            C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+            C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+            C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+            A += w;
+            ++j;
+            if (A >= ert) j = jend = nn;  // early ray termination: the next step finishes the ray
+        }
+#else
         for (int s = 0; have && s < kStepsPerCheck; ++s) {
             if (j >= nn) {
                 a.out[pix] = make_float4(C0, C1, C2, A);
@@ -303,6 +418,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             if (A >= ert) j = nn;  // early ray termination: the next step finishes the ray
 #endif
         }
+#endif
     }
 }
 
@@ -397,7 +513,11 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = 2 * a.n_tf * sizeof(float4);
+    size_t smem = 2 * a.n_tf * sizeof(float4);
+#if DPRT_ASYNC
+    smem += (size_t)kDepth * 2 * kThreads * sizeof(float4);  // per-lane ring of corner quads
+    cudaFuncSetAttribute(march_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#endif
 #ifdef DPRT_CARVEOUT
     cudaFuncSetAttribute(march_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, DPRT_CARVEOUT);
 #endif
