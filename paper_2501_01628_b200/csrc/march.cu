@@ -78,6 +78,16 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
     return kb > ka ? kb - ka : 0;
 }
 
+#ifndef DPRT_FAKE_MEM
+#define DPRT_FAKE_MEM 0
+#endif
+#ifndef DPRT_CHUNKED
+#define DPRT_CHUNKED 0
+#endif
+#ifndef DPRT_CHUNK
+#define DPRT_CHUNK 32
+#endif
+constexpr int kChunk = DPRT_CHUNK;
 #ifndef DPRT_REFILL_BELOW
 #define DPRT_REFILL_BELOW 8
 #endif
@@ -171,8 +181,61 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 #endif
     float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f}, ist[3] = {0.f, 0.f, 0.f};
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+#if DPRT_CHUNKED
+    // Warp-private window of the ray queue: [cbase, cbase + cleft) are reserved for this warp; the next
+    // window is requested from the global counter as soon as the current one runs dry, so the atomic's
+    // latency overlaps marching instead of stalling the refill.
+    int cbase = 0, cleft = 0;
+    if (lane == 0) cbase = atomicAdd(a.counters + 1, kChunk);
+    cbase = __shfl_sync(0xffffffffu, cbase, 0);
+    cleft = cbase < total ? min(kChunk, total - cbase) : 0;
+    int nbase = -1;  // pending next window (warp-uniform), -1 = none requested
+#endif
     while (true) {
         unsigned act = __ballot_sync(0xffffffffu, have);
+#if DPRT_CHUNKED
+        if (!exhausted && __popc(act) < kRefillBelow) {
+            const unsigned need = ~act;
+            int k = __popc(need);
+            if (cleft == 0) {
+                if (nbase < 0) {
+                    if (lane == 0) nbase = atomicAdd(a.counters + 1, kChunk);
+                    nbase = __shfl_sync(0xffffffffu, nbase, 0);
+                }
+                cbase = nbase;
+                cleft = cbase < total ? min(kChunk, total - cbase) : 0;
+                nbase = -1;
+                if (cleft == 0) exhausted = true;
+            }
+            const int take = min(k, cleft);
+            if (!have) {
+                const int rank = __popc(need & ((1u << lane) - 1));
+                if (rank < take) {
+                    const int idx = cbase + rank;
+                    const float4 r0 = __ldg(a.rays + 2 * idx), r1 = __ldg(a.rays + 2 * idx + 1);
+                    p0[0] = r0.x; p0[1] = r0.y; p0[2] = r0.z;
+                    st[0] = r1.x; st[1] = r1.y; st[2] = r1.z;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) ist[i] = st[i] != 0.f ? __frcp_rn(st[i]) : 0.f;
+                    pix = __float_as_int(r0.w);
+                    nn = __float_as_int(r1.w);
+                    j = 0;
+                    C0 = C1 = C2 = A = 0.f;
+                    have = true;
+#if DPRT_COUNTERS
+                    ++c_rays;
+#endif
+                }
+            }
+            cbase += take;
+            cleft -= take;
+            if (cleft == 0 && !exhausted && nbase < 0) {  // request the next window early
+                if (lane == 0) nbase = atomicAdd(a.counters + 1, kChunk);
+                nbase = __shfl_sync(0xffffffffu, nbase, 0);
+            }
+            act = __ballot_sync(0xffffffffu, have);
+        }
+#else
         if (!exhausted && __popc(act) < kRefillBelow) {
             const unsigned need = ~act;
             const int k = __popc(need);
@@ -203,6 +266,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             }
             act = __ballot_sync(0xffffffffu, have);
         }
+#endif
         if (act == 0) {
 #if DPRT_COUNTERS
             DPRT_COUNT(0, c_shade);
@@ -374,7 +438,11 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             };
 #if DPRT_QUAD
             // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
+#if DPRT_FAKE_MEM
+            const float4* q = quad + (((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix) & 4095u);  // timing experiment only
+#else
             const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+#endif
             const float4 qa = __ldg(q), qb = __ldg(q + sz);
 #else
             const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
