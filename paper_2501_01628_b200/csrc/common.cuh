@@ -9,14 +9,8 @@
 #ifndef DPRT_QUAD
 #define DPRT_QUAD 1
 #endif
-#ifndef DPRT_ASYNC
-#define DPRT_ASYNC 0
-#endif
 #ifndef DPRT_COUNTERS
 #define DPRT_COUNTERS 0
-#endif
-#ifndef DPRT_PAIR
-#define DPRT_PAIR 0
 #endif
 
 namespace dprt {

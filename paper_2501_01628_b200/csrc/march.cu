@@ -78,16 +78,6 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
     return kb > ka ? kb - ka : 0;
 }
 
-#ifndef DPRT_FAKE_MEM
-#define DPRT_FAKE_MEM 0
-#endif
-#ifndef DPRT_CHUNKED
-#define DPRT_CHUNKED 0
-#endif
-#ifndef DPRT_CHUNK
-#define DPRT_CHUNK 32
-#endif
-constexpr int kChunk = DPRT_CHUNK;
 #ifndef DPRT_REFILL_BELOW
 #define DPRT_REFILL_BELOW 8
 #endif
@@ -96,11 +86,6 @@ constexpr int kChunk = DPRT_CHUNK;
 #endif
 constexpr int kRefillBelow = DPRT_REFILL_BELOW;  // refill a warp's idle lanes once fewer than this many march
 constexpr int kStepsPerCheck = DPRT_STEPS_PER_CHECK;  // march steps between refill checks
-#ifndef DPRT_ASYNC_DEPTH
-#define DPRT_ASYNC_DEPTH 4
-#endif
-constexpr int kDepth = DPRT_ASYNC_DEPTH;  // cp.async samples in flight per lane (DPRT_ASYNC)
-constexpr int kThreads = kTileX * kTileY;
 
 // Pass 1: exact ray setup, zero-fill of pixels that miss the brick, compaction of the ones that hit.
 __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchArgs a) {
@@ -172,70 +157,13 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 
     bool have = false, exhausted = false;
     int pix = 0, nn = 0, j = 0;
-#if DPRT_ASYNC
-    int jend = 0, jpf = 0;  // [j, jend): verified non-empty run; [j, jpf): samples whose copies are issued
-    const unsigned ring = (unsigned)__cvta_generic_to_shared(s_tf + 2 * a.n_tf) + (unsigned)tid * 16u;
-#endif
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
     float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f}, ist[3] = {0.f, 0.f, 0.f};
     float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
-#if DPRT_CHUNKED
-    // Warp-private window of the ray queue: [cbase, cbase + cleft) are reserved for this warp; the next
-    // window is requested from the global counter as soon as the current one runs dry, so the atomic's
-    // latency overlaps marching instead of stalling the refill.
-    int cbase = 0, cleft = 0;
-    if (lane == 0) cbase = atomicAdd(a.counters + 1, kChunk);
-    cbase = __shfl_sync(0xffffffffu, cbase, 0);
-    cleft = cbase < total ? min(kChunk, total - cbase) : 0;
-    int nbase = -1;  // pending next window (warp-uniform), -1 = none requested
-#endif
     while (true) {
         unsigned act = __ballot_sync(0xffffffffu, have);
-#if DPRT_CHUNKED
-        if (!exhausted && __popc(act) < kRefillBelow) {
-            const unsigned need = ~act;
-            int k = __popc(need);
-            if (cleft == 0) {
-                if (nbase < 0) {
-                    if (lane == 0) nbase = atomicAdd(a.counters + 1, kChunk);
-                    nbase = __shfl_sync(0xffffffffu, nbase, 0);
-                }
-                cbase = nbase;
-                cleft = cbase < total ? min(kChunk, total - cbase) : 0;
-                nbase = -1;
-                if (cleft == 0) exhausted = true;
-            }
-            const int take = min(k, cleft);
-            if (!have) {
-                const int rank = __popc(need & ((1u << lane) - 1));
-                if (rank < take) {
-                    const int idx = cbase + rank;
-                    const float4 r0 = __ldg(a.rays + 2 * idx), r1 = __ldg(a.rays + 2 * idx + 1);
-                    p0[0] = r0.x; p0[1] = r0.y; p0[2] = r0.z;
-                    st[0] = r1.x; st[1] = r1.y; st[2] = r1.z;
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) ist[i] = st[i] != 0.f ? __frcp_rn(st[i]) : 0.f;
-                    pix = __float_as_int(r0.w);
-                    nn = __float_as_int(r1.w);
-                    j = 0;
-                    C0 = C1 = C2 = A = 0.f;
-                    have = true;
-#if DPRT_COUNTERS
-                    ++c_rays;
-#endif
-                }
-            }
-            cbase += take;
-            cleft -= take;
-            if (cleft == 0 && !exhausted && nbase < 0) {  // request the next window early
-                if (lane == 0) nbase = atomicAdd(a.counters + 1, kChunk);
-                nbase = __shfl_sync(0xffffffffu, nbase, 0);
-            }
-            act = __ballot_sync(0xffffffffu, have);
-        }
-#else
         if (!exhausted && __popc(act) < kRefillBelow) {
             const unsigned need = ~act;
             const int k = __popc(need);
@@ -254,9 +182,6 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                     pix = __float_as_int(r0.w);
                     nn = __float_as_int(r1.w);
                     j = 0;
-#if DPRT_ASYNC
-                    jend = jpf = 0;
-#endif
                     C0 = C1 = C2 = A = 0.f;
                     have = true;
 #if DPRT_COUNTERS
@@ -266,7 +191,6 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             }
             act = __ballot_sync(0xffffffffu, have);
         }
-#endif
         if (act == 0) {
 #if DPRT_COUNTERS
             DPRT_COUNT(0, c_shade);
@@ -276,109 +200,6 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 #endif
             break;
         }
-#if DPRT_ASYNC
-        for (int s = 0; have && s < kStepsPerCheck; ++s) {
-            if (j >= nn) {
-                asm volatile("cp.async.wait_all;\n" ::: "memory");  // no copy may land in a reused slot
-                a.out[pix] = make_float4(C0, C1, C2, A);
-                have = false;
-                break;
-            }
-            if (j >= jend) {
-                // Start of a run: locate the macrocell of sample j; hop over empty cubes.
-                const float fj = (float)j;
-                const int mx = min(__float2int_rd(fmaxf(fmaf(fj, st[0], p0[0]), 0.f)), chx) >> kMacroShift;
-                const int my = min(__float2int_rd(fmaxf(fmaf(fj, st[1], p0[1]), 0.f)), chy) >> kMacroShift;
-                const int mz = min(__float2int_rd(fmaxf(fmaf(fj, st[2], p0[2]), 0.f)), chz) >> kMacroShift;
-                const int dist = skip ? (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) : 0;
-                const int r = dist > 0 ? dist : 1;
-                float je = 3.0e38f;
-                if (st[0] != 0.f)
-                    je = fminf(je, ((float)((st[0] > 0.f ? mx + r : mx - r + 1) << kMacroShift) - p0[0]) * ist[0]);
-                if (st[1] != 0.f)
-                    je = fminf(je, ((float)((st[1] > 0.f ? my + r : my - r + 1) << kMacroShift) - p0[1]) * ist[1]);
-                if (st[2] != 0.f)
-                    je = fminf(je, ((float)((st[2] > 0.f ? mz + r : mz - r + 1) << kMacroShift) - p0[2]) * ist[2]);
-                int jn = je < (float)nn ? (int)ceilf(je) : nn;
-                if (jn <= j) jn = j + 1;
-#if DPRT_COUNTERS
-                if (dist > 0) ++c_skip;
-#endif
-                if (dist > 0) {
-                    j = jpf = jn;  // empty cube: its samples would add exact zeros
-                    continue;
-                }
-                jend = jn;
-                jpf = j;
-            }
-            // Keep up to kDepth samples of the run in flight: cp.async copies the two corner quads of each
-            // into this lane's ring slot in shared memory -- no registers held while the loads are out.
-            while (jpf < jend && jpf < j + kDepth) {
-                const float fp = (float)jpf;
-                const int px_ = min(__float2int_rd(fmaxf(fmaf(fp, st[0], p0[0]), 0.f)), chx);
-                const int py_ = min(__float2int_rd(fmaxf(fmaf(fp, st[1], p0[1]), 0.f)), chy);
-                const int pz_ = min(__float2int_rd(fmaxf(fmaf(fp, st[2], p0[2]), 0.f)), chz);
-                const float4* q = quad + ((unsigned)pz_ * sz + (unsigned)py_ * sy + (unsigned)px_);
-                const unsigned slot = (unsigned)(jpf % kDepth);
-                const unsigned dst = ring + (slot * 2u * kThreads) * 16u;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(q) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst + kThreads * 16u), "l"(q + sz)
-                             : "memory");
-                asm volatile("cp.async.commit_group;\n" ::: "memory");
-                ++jpf;
-            }
-            // wait for sample j's group: (jpf - j - 1) younger groups may still be in flight
-            switch (jpf - j - 1) {
-                case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
-                case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
-                case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
-                case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
-                case 4: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
-                case 5: asm volatile("cp.async.wait_group 5;\n" ::: "memory"); break;
-                case 6: asm volatile("cp.async.wait_group 6;\n" ::: "memory"); break;
-                default: asm volatile("cp.async.wait_group 7;\n" ::: "memory"); break;
-            }
-            const unsigned slot = (unsigned)(j % kDepth);
-            float4 qa, qb;
-            {
-                const unsigned src = ring + (slot * 2u * kThreads) * 16u;
-                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                             : "=f"(qa.x), "=f"(qa.y), "=f"(qa.z), "=f"(qa.w) : "r"(src) : "memory");
-                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                             : "=f"(qb.x), "=f"(qb.y), "=f"(qb.z), "=f"(qb.w) : "r"(src + kThreads * 16u) : "memory");
-            }
-            const float fs = (float)j;
-            const float ux = fmaf(fs, st[0], p0[0]);
-            const float uy = fmaf(fs, st[1], p0[1]);
-            const float uz = fmaf(fs, st[2], p0[2]);
-            const float wx = __saturatef(ux - (float)min(__float2int_rd(fmaxf(ux, 0.f)), chx));
-            const float wy = __saturatef(uy - (float)min(__float2int_rd(fmaxf(uy, 0.f)), chy));
-            const float wz = __saturatef(uz - (float)min(__float2int_rd(fmaxf(uz, 0.f)), chz));
-            // trilinear + TF (§2.6) + front-to-back blend (§2.7)
-            const float c00 = fmaf(wx, qa.y - qa.x, qa.x);
-            const float c10 = fmaf(wx, qa.w - qa.z, qa.z);
-            const float c01 = fmaf(wx, qb.y - qb.x, qb.x);
-            const float c11 = fmaf(wx, qb.w - qb.z, qb.z);
-            const float c0 = fmaf(wy, c10 - c00, c00);
-            const float c1 = fmaf(wy, c11 - c01, c01);
-            const float v = fmaf(wz, c1 - c0, c0);
-            const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
-            const int ti = min((int)x, tmax);
-            const float tfr = x - (float)ti;
-            const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
-            const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
-#if DPRT_COUNTERS
-            ++c_shade;
-            c_contrib += w > 0.f;
-#endif
-            C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
-            C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
-            C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-            A += w;
-            ++j;
-            if (A >= ert) j = jend = nn;  // early ray termination: the next step finishes the ray
-        }
-#else
         for (int s = 0; have && s < kStepsPerCheck; ++s) {
             if (j >= nn) {
                 a.out[pix] = make_float4(C0, C1, C2, A);
@@ -438,55 +259,17 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             };
 #if DPRT_QUAD
             // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
-#if DPRT_FAKE_MEM
-            const float4* q = quad + (((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix) & 4095u);  // timing experiment only
-#else
             const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-#endif
             const float4 qa = __ldg(q), qb = __ldg(q + sz);
 #else
             const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
             const float4 qa = make_float4(__ldg(p), __ldg(p + 1), __ldg(p + sy), __ldg(p + sy + 1));
             const float4 qb = make_float4(__ldg(p + sz), __ldg(p + sz + 1), __ldg(p + sz + sy), __ldg(p + sz + sy + 1));
 #endif
-#if DPRT_PAIR && DPRT_QUAD
-            // Second sample of the step (j + 1) when it is still in a non-empty macrocell: its corner
-            // loads are issued before the first sample is shaded, doubling memory-level parallelism.
-            const float fs1 = fs + 1.f;
-            const float vx1 = fmaf(fs1, st[0], p0[0]);
-            const float vy1 = fmaf(fs1, st[1], p0[1]);
-            const float vz1 = fmaf(fs1, st[2], p0[2]);
-            const int jx1 = min(__float2int_rd(fmaxf(vx1, 0.f)), chx);
-            const int jy1 = min(__float2int_rd(fmaxf(vy1, 0.f)), chy);
-            const int jz1 = min(__float2int_rd(fmaxf(vz1, 0.f)), chz);
-            const int mc1 = ((jz1 >> kMacroShift) * mcd1 + (jy1 >> kMacroShift)) * mcd0 + (jx1 >> kMacroShift);
-            bool two = j + 1 < nn;
-            if (two && skip && mc1 != mc) two = __ldg(skipd + mc1) == 0;
-            float4 qa1 = qa, qb1 = qb;
-            if (two) {
-                const float4* q1 = quad + ((unsigned)jz1 * sz + (unsigned)jy1 * sy + (unsigned)jx1);
-                qa1 = __ldg(q1);
-                qb1 = __ldg(q1 + sz);
-            }
-            shade(qa, qb, __saturatef(ux - (float)ix), __saturatef(uy - (float)iy), __saturatef(uz - (float)iz));
-            ++j;
-            if (A >= ert) {  // early ray termination: the next step finishes the ray
-                j = nn;
-                continue;
-            }
-            if (two) {
-                shade(qa1, qb1, __saturatef(vx1 - (float)jx1), __saturatef(vy1 - (float)jy1),
-                      __saturatef(vz1 - (float)jz1));
-                ++j;
-                if (A >= ert) j = nn;
-            }
-#else
             shade(qa, qb, __saturatef(ux - (float)ix), __saturatef(uy - (float)iy), __saturatef(uz - (float)iz));
             ++j;
             if (A >= ert) j = nn;  // early ray termination: the next step finishes the ray
-#endif
         }
-#endif
     }
 }
 
@@ -581,14 +364,7 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    size_t smem = 2 * a.n_tf * sizeof(float4);
-#if DPRT_ASYNC
-    smem += (size_t)kDepth * 2 * kThreads * sizeof(float4);  // per-lane ring of corner quads
-    cudaFuncSetAttribute(march_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-#endif
-#ifdef DPRT_CARVEOUT
-    cudaFuncSetAttribute(march_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, DPRT_CARVEOUT);
-#endif
+    const size_t smem = 2 * a.n_tf * sizeof(float4);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, kTileX * kTileY, smem);
     if (per_sm < 1) per_sm = 1;
     march_kernel<<<sms * per_sm, block, smem, stream>>>(a);
