@@ -25,6 +25,7 @@ from .dvr import (  # noqa: F401
     max_threads,
     primary_dirs,
     render_brick,
+    sample_counts,
     slab,
     tone_map_rgb8,
 )

@@ -19,7 +19,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_build" / "libdvr_oracle.so"
-_ABI = 3
+_ABI = 4
 
 _lib = None
 
@@ -63,6 +63,7 @@ def load_oracle():
         ctypes.c_int]
     lib.dvr_oracle_render_brick.restype = ctypes.c_int
     lib.dvr_oracle_max_threads.restype = ctypes.c_int
+    lib.dvr_oracle_sample_counts.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
     _lib = lib
     return lib
 
@@ -173,6 +174,18 @@ class OracleBrick:
         s = self.stored_lo
         d = self.stored_dims
         return np.ascontiguousarray(field[s[2]:s[2] + d[2], s[1]:s[1] + d[1], s[0]:s[0] + d[0]])
+
+
+def sample_counts(brick: "OracleBrick", cam: np.ndarray, dt: float, width: int, height: int,
+                  nthreads: int = 0) -> np.ndarray:
+    """(H, W) owned lattice sample counts of the brick's owned box, no marching."""
+    lo, hi = brick.box_world()
+    lo_ = np.asarray(lo, np.float64)
+    hi_ = np.asarray(hi, np.float64)
+    out = np.zeros((height, width), np.uint32)
+    load_oracle().dvr_oracle_sample_counts(_ptr(lo_), _ptr(hi_), _ptr(np.ascontiguousarray(cam, np.float64)),
+                                           float(dt), width, height, _ptr(out), nthreads)
+    return out
 
 
 def render_brick(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.ndarray, vmin: float,

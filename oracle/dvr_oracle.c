@@ -26,7 +26,7 @@
 #include <omp.h>
 #endif
 
-#define ORACLE_ABI_VERSION 3
+#define ORACLE_ABI_VERSION 4
 
 int dvr_oracle_version(void) { return ORACLE_ABI_VERSION; }
 
@@ -279,6 +279,23 @@ int dvr_oracle_render_brick(const float* vox, const int64_t* geo, const double* 
         }
     }
     return 0;
+}
+
+/* Owned lattice sample counts only (no marching): per pixel of the full W x H frame for the owned box
+ * [lo_w, hi_w] -- the integer-exact ownership check used at full BASELINE sizes. */
+void dvr_oracle_sample_counts(const double* lo_w, const double* hi_w, const double* cam, double dt, int W, int H,
+                              uint32_t* out, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(static)
+    for (int py = 0; py < H; ++py)
+        for (int px = 0; px < W; ++px) {
+            double d[3];
+            primary_dir(cam, px, py, W, H, d);
+            int64_t k0 = 0;
+            out[(int64_t)py * W + px] = (uint32_t)lattice_range(cam, d, lo_w, hi_w, dt, &k0);
+        }
 }
 
 int dvr_oracle_max_threads(void) {
