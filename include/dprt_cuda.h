@@ -86,6 +86,8 @@ typedef struct DprtMarchParams {
 
 #define DPRT_MARCH_NO_SKIP 1      /* disable exact empty-space skipping (macrocell skip distances) */
 #define DPRT_MARCH_FULL_FRAME 2   /* march every pixel instead of the brick's screen footprint */
+#define DPRT_MARCH_BEAM 4         /* force the warp-beam marcher (8x4 pixel beams, slab-wise skipping) */
+#define DPRT_MARCH_QUEUE 8        /* force the ray-queue marcher (persistent warps, per-lane refill) */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
 #define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */

@@ -28,6 +28,8 @@ MAX_PARTS = 64
 
 MARCH_NO_SKIP = 1
 MARCH_FULL_FRAME = 2
+MARCH_BEAM = 4
+MARCH_QUEUE = 8
 COMPOSITE_TONEMAP = 1
 COMPOSITE_RGBA = 2
 

@@ -9,6 +9,9 @@
 #ifndef DPRT_QUAD
 #define DPRT_QUAD 1
 #endif
+#ifndef DPRT_BEAM_DEFAULT
+#define DPRT_BEAM_DEFAULT 0
+#endif
 #ifndef DPRT_COUNTERS
 #define DPRT_COUNTERS 0
 #endif
@@ -62,6 +65,7 @@ struct MarchArgs {
     const uint8_t* __restrict__ skipd;
     int mcd[3];
     int skip;
+    int beam;  // 1: march_beam_kernel (warp beams, per-pixel ray records); 0: ray queue + march_kernel
     // transfer function
     const float4* __restrict__ tf;
     int n_tf;

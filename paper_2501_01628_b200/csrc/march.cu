@@ -106,6 +106,24 @@ __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchA
         if (a.samples) a.samples[pix] = (uint32_t)n;
         if (n == 0) a.out[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if (a.beam) {
+        // beam marcher: one record per pixel of the footprint rectangle, indexed by pixel
+        if (in_rect) {
+            float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
+            if (n > 0) {
+                const double t0 = __dmul_rn((double)k0, a.dt);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const double p = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
+                    p0[i] = (float)(p - a.stored_lo_d[i]);
+                    st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
+                }
+            }
+            a.rays[2 * pix] = make_float4(p0[0], p0[1], p0[2], __int_as_float((int)pix));
+            a.rays[2 * pix + 1] = make_float4(st[0], st[1], st[2], __int_as_float((int)n));
+        }
+        return;
+    }
     const bool hit = n > 0;
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (!m) return;
@@ -273,6 +291,185 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
     }
 }
 
+// Pass 2 (beam variant): a warp marches one 8x4 pixel tile as a coherent beam, slab by slab along the
+// beam's dominant axis (slab = one macrocell layer).  Per slab the warp bounds the beam's cells on the
+// two other axes with warp reductions, reads those macrocells' skip distances cooperatively and either
+// jumps every lane over the empty slabs at once or lets each lane shade its samples in the slab.  No
+// per-sample skip test, lanes stay in step, and the 32 rays read the same L1 lines.
+__device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
+
+__global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
+    extern __shared__ float4 s_tf[];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < a.n_tf; i += blockDim.x) {
+        const float4 e0 = a.tf[i];
+        const float4 e1 = i + 1 < a.n_tf ? a.tf[i + 1] : e0;
+        s_tf[2 * i] = e0;
+        s_tf[2 * i + 1] = make_float4(e1.x - e0.x, e1.y - e0.y, e1.z - e0.z, e1.w - e0.w);
+    }
+    __syncthreads();
+    const unsigned FULL = 0xffffffffu;
+    const int lane = tid & 31;
+    const int rw = a.rect[2] - a.rect[0], rh = a.rect[3] - a.rect[1];
+    const int tiles_x = (rw + 7) >> 3, tiles_y = (rh + 3) >> 2;
+    const int ntiles = tiles_x * tiles_y;
+    const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
+    const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
+    const float4* __restrict__ quad = a.quad;
+    const uint8_t* __restrict__ skipd = a.skipd;
+    const int mcd0 = a.mcd[0], mcd1 = a.mcd[1];
+    const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
+    const int tmax = a.n_tf - 2;
+#if DPRT_COUNTERS
+    unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
+#endif
+    while (true) {
+        int tile = 0;
+        if (lane == 0) tile = atomicAdd(a.counters + 1, 1);
+        tile = __shfl_sync(FULL, tile, 0);
+        if (tile >= ntiles) break;
+        const int px = a.rect[0] + (tile % tiles_x) * 8 + (lane & 7);
+        const int py = a.rect[1] + (tile / tiles_x) * 4 + (lane >> 3);
+        int nn = 0, pix = 0;
+        float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
+        if (px < a.rect[2] && py < a.rect[3]) {
+            pix = py * a.W + px;
+            const float4 r0 = __ldg(a.rays + 2 * pix), r1 = __ldg(a.rays + 2 * pix + 1);
+            p0[0] = r0.x; p0[1] = r0.y; p0[2] = r0.z;
+            st[0] = r1.x; st[1] = r1.y; st[2] = r1.z;
+            nn = __float_as_int(r1.w);
+        }
+        const unsigned hitm = __ballot_sync(FULL, nn > 0);
+        if (!hitm) continue;
+#if DPRT_COUNTERS
+        c_rays += nn > 0;
+#endif
+        // dominant axis of the beam (from its first ray) and whether every ray agrees with it
+        const int ref = __ffs(hitm) - 1;
+        const float rx = __shfl_sync(FULL, st[0], ref), ry = __shfl_sync(FULL, st[1], ref), rz = __shfl_sync(FULL, st[2], ref);
+        const float ax = fabsf(rx), ay = fabsf(ry), az = fabsf(rz);
+        const int ka = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
+        const int kb = ka == 0 ? 1 : 0, kc = ka == 2 ? 1 : 2;
+        // this ray's components permuted to (a, b, c) once, so the loops below index no arrays
+        auto sel = [&](const float* v, int k3) { return k3 == 0 ? v[0] : (k3 == 1 ? v[1] : v[2]); };
+        const float sa = sel(st, ka), sb = sel(st, kb), sc = sel(st, kc);
+        const float pa = sel(p0, ka), pb = sel(p0, kb), pc = sel(p0, kc);
+        const int cha = ka == 0 ? chx : (ka == 1 ? chy : chz);
+        const int chb = kb == 0 ? chx : (kb == 1 ? chy : chz);
+        const int chc = kc == 0 ? chx : (kc == 1 ? chy : chz);
+        const bool pos = (ka == 0 ? rx : (ka == 1 ? ry : rz)) > 0.f;
+        const bool ok = nn == 0 || ((sa > 0.f) == pos && sa != 0.f && fabsf(sb) <= fabsf(sa) && fabsf(sc) <= fabsf(sa));
+        const bool dominant = __all_sync(FULL, ok);  // multi-slab jumps need |st_b|, |st_c| <= |st_a| on all rays
+        const float isa = sa != 0.f ? 1.f / sa : 0.f;
+        int j = 0;
+        float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+        bool live = nn > 0;
+        while (true) {
+            const unsigned livem = __ballot_sync(FULL, live);
+            if (!livem) break;
+            // current slab: the nearest (in the march direction) slab holding a live lane's next sample
+            int ksl = 0;
+            if (live) ksl = fl2cell(fmaf((float)j, sa, pa), cha) >> kMacroShift;
+            const int key = live ? (pos ? ksl : -ksl) : 0x7fffffff;
+            const int kmin = __reduce_min_sync(FULL, key);
+            const int K = pos ? kmin : -kmin;
+            // this lane's samples in slab K: j .. jend-1 (first sample past the slab's far face)
+            int jend = j;
+            if (live) {
+                const float face = (float)((pos ? K + 1 : K) << kMacroShift);
+                const float je = (face - pa) * isa;
+                jend = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;  // >= 1 sample: progress
+                if (ksl != K) jend = j;  // this ray is not in slab K yet
+            }
+            // bound the beam's cells on the other two axes over all samples in the slab
+            int b0 = 0x7fffffff, b1 = -1, c0 = 0x7fffffff, c1 = -1;
+            if (jend > j) {
+                const float f0 = (float)j, f1 = (float)(jend - 1);
+                const int ub0 = fl2cell(fmaf(f0, sb, pb), chb), ub1 = fl2cell(fmaf(f1, sb, pb), chb);
+                const int uc0 = fl2cell(fmaf(f0, sc, pc), chc), uc1 = fl2cell(fmaf(f1, sc, pc), chc);
+                b0 = min(ub0, ub1) >> kMacroShift;
+                b1 = max(ub0, ub1) >> kMacroShift;
+                c0 = min(uc0, uc1) >> kMacroShift;
+                c1 = max(uc0, uc1) >> kMacroShift;
+            }
+            const int B0 = __reduce_min_sync(FULL, b0), B1 = __reduce_max_sync(FULL, b1);
+            const int Cc0 = __reduce_min_sync(FULL, c0), Cc1 = __reduce_max_sync(FULL, c1);
+            int dmin = 0;
+            if (a.skip && B1 >= B0) {
+                const int nb = B1 - B0 + 1, nc = Cc1 - Cc0 + 1;
+                if (nb * nc <= 32) {
+                    int dl = 255;
+                    if (lane < nb * nc) {
+                        const int mb = B0 + lane % nb, mc = Cc0 + lane / nb;
+                        const int mx = ka == 0 ? K : (kb == 0 ? mb : mc);
+                        const int my = ka == 1 ? K : (kb == 1 ? mb : mc);
+                        const int mz = ka == 2 ? K : (kb == 2 ? mb : mc);
+                        dl = (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx);
+                    }
+                    dmin = __reduce_min_sync(FULL, dl);
+                }
+            }
+            if (dmin > 0) {
+                // every macrocell the beam touches in slab K is empty; with all rays dominated by axis a
+                // the next dmin - 1 slabs are inside their empty Chebyshev cubes too
+                const int jump = dominant ? dmin : 1;
+#if DPRT_COUNTERS
+                c_skip += live;
+#endif
+                if (live && ksl == K) {
+                    const float face = (float)((pos ? K + jump : K - jump + 1) << kMacroShift);
+                    const float je = (face - pa) * isa;
+                    j = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;
+                    if (j >= nn) live = false;
+                }
+                continue;
+            }
+            for (; j < jend; ++j) {
+                const float fs = (float)j;
+                const float ux = fmaf(fs, st[0], p0[0]);
+                const float uy = fmaf(fs, st[1], p0[1]);
+                const float uz = fmaf(fs, st[2], p0[2]);
+                const int ix = fl2cell(ux, chx), iy = fl2cell(uy, chy), iz = fl2cell(uz, chz);
+                const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+                const float4 qa = __ldg(q), qb = __ldg(q + sz);
+                const float wx = __saturatef(ux - (float)ix), wy = __saturatef(uy - (float)iy), wz = __saturatef(uz - (float)iz);
+                const float e00 = fmaf(wx, qa.y - qa.x, qa.x);
+                const float e10 = fmaf(wx, qa.w - qa.z, qa.z);
+                const float e01 = fmaf(wx, qb.y - qb.x, qb.x);
+                const float e11 = fmaf(wx, qb.w - qb.z, qb.z);
+                const float g0 = fmaf(wy, e10 - e00, e00);
+                const float g1 = fmaf(wy, e11 - e01, e01);
+                const float v = fmaf(wz, g1 - g0, g0);
+                const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
+                const int ti = min((int)x, tmax);
+                const float tfr = x - (float)ti;
+                const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+                const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+#if DPRT_COUNTERS
+                ++c_shade;
+                c_contrib += w > 0.f;
+#endif
+                C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+                C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+                C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+                A += w;
+                if (A >= ert) {  // early ray termination
+                    live = false;
+                    break;
+                }
+            }
+            if (j >= nn) live = false;
+        }
+        if (nn > 0) a.out[pix] = make_float4(C0, C1, C2, A);
+    }
+#if DPRT_COUNTERS
+    DPRT_COUNT(0, c_shade);
+    DPRT_COUNT(1, c_contrib);
+    DPRT_COUNT(2, c_skip);
+    DPRT_COUNT(3, c_rays);
+#endif
+}
+
 // Skip distances.  classify: 0 for a macrocell whose dilated value range [min, max]
 // can map to a non-zero alpha under the TF (conservatively one extra entry on each side), kSkipCap
 // otherwise.  Then three separable passes turn it into the Chebyshev distance (in macrocells, capped)
@@ -365,6 +562,12 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = 2 * a.n_tf * sizeof(float4);
+    if (a.beam) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kTileX * kTileY, smem);
+        if (per_sm < 1) per_sm = 1;
+        march_beam_kernel<<<sms * per_sm, block, smem, stream>>>(a);
+        return cudaGetLastError();
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, kTileX * kTileY, smem);
     if (per_sm < 1) per_sm = 1;
     march_kernel<<<sms * per_sm, block, smem, stream>>>(a);

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import itertools
+import os
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -177,6 +178,11 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
             raise UsageError("samples buffer must hold one count per pixel")
         sp = ctypes.c_void_p(samples.data_ptr())
     flags = (0 if skip else _lib.MARCH_NO_SKIP) | (0 if footprint else _lib.MARCH_FULL_FRAME)
+    variant = os.environ.get("DPRT_MARCHER", "")
+    if variant == "beam":
+        flags |= _lib.MARCH_BEAM
+    elif variant == "queue":
+        flags |= _lib.MARCH_QUEUE
     p = tf.params(dt, ert, flags)
     c = camera_struct(cam)
     rc = _lib.lib().dprt_march(brick.handle, ctypes.byref(c), ctypes.byref(p), ctypes.c_void_p(partial.data_ptr()),
