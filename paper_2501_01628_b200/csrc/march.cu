@@ -296,6 +296,11 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 // two other axes with warp reductions, reads those macrocells' skip distances cooperatively and either
 // jumps every lane over the empty slabs at once or lets each lane shade its samples in the slab.  No
 // per-sample skip test, lanes stay in step, and the 32 rays read the same L1 lines.
+#ifndef DPRT_BEAM_UNROLL
+#define DPRT_BEAM_UNROLL 4
+#endif
+constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
+
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
 __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
@@ -424,36 +429,57 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_b
                 }
                 continue;
             }
-            for (; j < jend; ++j) {
-                const float fs = (float)j;
-                const float ux = fmaf(fs, st[0], p0[0]);
-                const float uy = fmaf(fs, st[1], p0[1]);
-                const float uz = fmaf(fs, st[2], p0[2]);
-                const int ix = fl2cell(ux, chx), iy = fl2cell(uy, chy), iz = fl2cell(uz, chz);
-                const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-                const float4 qa = __ldg(q), qb = __ldg(q + sz);
-                const float wx = __saturatef(ux - (float)ix), wy = __saturatef(uy - (float)iy), wz = __saturatef(uz - (float)iz);
-                const float e00 = fmaf(wx, qa.y - qa.x, qa.x);
-                const float e10 = fmaf(wx, qa.w - qa.z, qa.z);
-                const float e01 = fmaf(wx, qb.y - qb.x, qb.x);
-                const float e11 = fmaf(wx, qb.w - qb.z, qb.z);
-                const float g0 = fmaf(wy, e10 - e00, e00);
-                const float g1 = fmaf(wy, e11 - e01, e01);
-                const float v = fmaf(wz, g1 - g0, g0);
-                const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
-                const int ti = min((int)x, tmax);
-                const float tfr = x - (float)ti;
-                const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
-                const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+            // Shade this lane's samples in the slab, kBeamUnroll at a time: all their corner loads are
+            // issued before the first is shaded, so each lane keeps several loads in flight.
+            while (j < jend) {
+                const int cnt = min(kBeamUnroll, jend - j);
+                float4 qa[kBeamUnroll], qb[kBeamUnroll];
+                float wx[kBeamUnroll], wy[kBeamUnroll], wz[kBeamUnroll];
+#pragma unroll
+                for (int u = 0; u < kBeamUnroll; ++u) {
+                    if (u < cnt) {
+                        const float fs = (float)(j + u);
+                        const float ux = fmaf(fs, st[0], p0[0]);
+                        const float uy = fmaf(fs, st[1], p0[1]);
+                        const float uz = fmaf(fs, st[2], p0[2]);
+                        const int ix = fl2cell(ux, chx), iy = fl2cell(uy, chy), iz = fl2cell(uz, chz);
+                        const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+                        qa[u] = __ldg(q);
+                        qb[u] = __ldg(q + sz);
+                        wx[u] = __saturatef(ux - (float)ix);
+                        wy[u] = __saturatef(uy - (float)iy);
+                        wz[u] = __saturatef(uz - (float)iz);
+                    }
+                }
+                bool stop = false;
+#pragma unroll
+                for (int u = 0; u < kBeamUnroll; ++u) {
+                    if (u < cnt && !stop) {
+                        const float e00 = fmaf(wx[u], qa[u].y - qa[u].x, qa[u].x);
+                        const float e10 = fmaf(wx[u], qa[u].w - qa[u].z, qa[u].z);
+                        const float e01 = fmaf(wx[u], qb[u].y - qb[u].x, qb[u].x);
+                        const float e11 = fmaf(wx[u], qb[u].w - qb[u].z, qb[u].z);
+                        const float g0 = fmaf(wy[u], e10 - e00, e00);
+                        const float g1 = fmaf(wy[u], e11 - e01, e01);
+                        const float v = fmaf(wz[u], g1 - g0, g0);
+                        const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
+                        const int ti = min((int)x, tmax);
+                        const float tfr = x - (float)ti;
+                        const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+                        const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
 #if DPRT_COUNTERS
-                ++c_shade;
-                c_contrib += w > 0.f;
+                        ++c_shade;
+                        c_contrib += w > 0.f;
 #endif
-                C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
-                C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
-                C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-                A += w;
-                if (A >= ert) {  // early ray termination
+                        C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+                        C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+                        C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+                        A += w;
+                        if (A >= ert) stop = true;  // early ray termination
+                    }
+                }
+                j += cnt;
+                if (stop) {
                     live = false;
                     break;
                 }
