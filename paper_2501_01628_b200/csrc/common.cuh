@@ -10,7 +10,7 @@
 #define DPRT_QUAD 1
 #endif
 #ifndef DPRT_BEAM_DEFAULT
-#define DPRT_BEAM_DEFAULT 0
+#define DPRT_BEAM_DEFAULT 1
 #endif
 #ifndef DPRT_COUNTERS
 #define DPRT_COUNTERS 0

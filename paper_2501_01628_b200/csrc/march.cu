@@ -303,7 +303,10 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
-__global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
+#ifndef DPRT_BEAM_MINBLOCKS
+#define DPRT_BEAM_MINBLOCKS 3
+#endif
+__global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_tf; i += blockDim.x) {
@@ -443,9 +446,15 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_b
                         const float uy = fmaf(fs, st[1], p0[1]);
                         const float uz = fmaf(fs, st[2], p0[2]);
                         const int ix = fl2cell(ux, chx), iy = fl2cell(uy, chy), iz = fl2cell(uz, chz);
+#if DPRT_QUAD
                         const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
                         qa[u] = __ldg(q);
                         qb[u] = __ldg(q + sz);
+#else
+                        const float* pv = a.vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+                        qa[u] = make_float4(__ldg(pv), __ldg(pv + 1), __ldg(pv + sy), __ldg(pv + sy + 1));
+                        qb[u] = make_float4(__ldg(pv + sz), __ldg(pv + sz + 1), __ldg(pv + sz + sy), __ldg(pv + sz + sy + 1));
+#endif
                         wx[u] = __saturatef(ux - (float)ix);
                         wy[u] = __saturatef(uy - (float)iy);
                         wz[u] = __saturatef(uz - (float)iz);
