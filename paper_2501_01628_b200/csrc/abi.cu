@@ -328,7 +328,7 @@ int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams*
         if (rc) return rc;
     }
     DprtBrick* mb = const_cast<DprtBrick*>(b);  // ray queue + skip-distance cache are mutable scratch
-    if ((long long)W * H > mb->ray_cap) {
+    if (!a.beam && (long long)W * H > mb->ray_cap) {  // the queue marcher needs 32 B per pixel
         CK(cudaStreamSynchronize((cudaStream_t)stream), "ray queue resize sync");
         cudaFree(mb->rays);
         mb->rays = nullptr;

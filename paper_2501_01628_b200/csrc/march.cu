@@ -106,24 +106,6 @@ __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchA
         if (a.samples) a.samples[pix] = (uint32_t)n;
         if (n == 0) a.out[pix] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (a.beam) {
-        // beam marcher: one record per pixel of the footprint rectangle, indexed by pixel
-        if (in_rect) {
-            float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
-            if (n > 0) {
-                const double t0 = __dmul_rn((double)k0, a.dt);
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const double p = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
-                    p0[i] = (float)(p - a.stored_lo_d[i]);
-                    st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
-                }
-            }
-            a.rays[2 * pix] = make_float4(p0[0], p0[1], p0[2], __int_as_float((int)pix));
-            a.rays[2 * pix + 1] = make_float4(st[0], st[1], st[2], __int_as_float((int)n));
-        }
-        return;
-    }
     const bool hit = n > 0;
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (!m) return;
@@ -341,11 +323,23 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
         int nn = 0, pix = 0;
         float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
         if (px < a.rect[2] && py < a.rect[3]) {
+            // exact f64 ray setup for this lane's pixel, fused
             pix = py * a.W + px;
-            const float4 r0 = __ldg(a.rays + 2 * pix), r1 = __ldg(a.rays + 2 * pix + 1);
-            p0[0] = r0.x; p0[1] = r0.y; p0[2] = r0.z;
-            st[0] = r1.x; st[1] = r1.y; st[2] = r1.z;
-            nn = __float_as_int(r1.w);
+            double d[3];
+            int64_t k0 = 0;
+            primary_dir(a, px, py, d);
+            const int64_t n = lattice_range(a, d, &k0);
+            if (a.samples) a.samples[pix] = (uint32_t)n;
+            if (n > 0) {
+                const double t0 = __dmul_rn((double)k0, a.dt);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const double pw = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
+                    p0[i] = (float)(pw - a.stored_lo_d[i]);
+                    st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
+                }
+                nn = (int)n;
+            }
         }
         const unsigned hitm = __ballot_sync(FULL, nn > 0);
         if (!hitm) continue;
@@ -590,14 +584,20 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     dim3 block(kTileX * kTileY);
     dim3 grid((a.W + kTileX - 1) / kTileX, (a.H + kTileY - 1) / kTileY);
-    ray_setup_kernel<<<grid, block, 0, stream>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (!a.beam) {
+        ray_setup_kernel<<<grid, block, 0, stream>>>(a);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = 2 * a.n_tf * sizeof(float4);
     if (a.beam) {
+        // pixels the beams do not write (misses, outside the footprint) must read as zero
+        e = cudaMemsetAsync(a.out, 0, (size_t)a.W * a.H * sizeof(float4), stream);
+        if (e == cudaSuccess && a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.W * a.H * sizeof(uint32_t), stream);
+        if (e != cudaSuccess) return e;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kTileX * kTileY, smem);
         if (per_sm < 1) per_sm = 1;
         march_beam_kernel<<<sms * per_sm, block, smem, stream>>>(a);
