@@ -135,6 +135,8 @@ class VolumeRenderer:
         self.partial = None
         self.samples = None
         self.compositor: Optional[Compositor] = None
+        self._copy_stream = None
+        self._pending_copy = None
 
     def set_tf(self, tf: TransferFunction1D) -> None:
         self.tf = tf
@@ -166,6 +168,10 @@ class VolumeRenderer:
                   samples=self.samples if options.collect_samples else None, skip=options.skip_empty)
         if options.disable_compositing:
             order = [self.ep.rank] if self.ep.R == 1 else order
+        if self._pending_copy is not None:
+            # the previous frame's read-back may still be draining the device frame buffer
+            torch.cuda.current_stream(self.device).wait_event(self._pending_copy)
+            self._pending_copy = None
         out = self.compositor.composite(self.partial, order, self.background,
                                         keep_float=options.keep_float, solo=options.disable_compositing)
         nbytes = self.compositor.last_bytes
@@ -180,6 +186,43 @@ class VolumeRenderer:
         if options.collect_samples:
             res.samples = self.samples.view(height, width)
         return res
+
+    def render_to_host(self, cam: CameraSpec, width: int, height: int, host: Optional[torch.Tensor],
+                       options: RenderOptions = RenderOptions(), verify: bool = True) -> "HostFrame":
+        """Collective render whose RGB8 frame is copied into ``host`` (pinned, (H, W, 3) uint8, rank 0) on a
+        side stream: the read-back of frame k overlaps the march of frame k+1.  ``HostFrame.wait()``
+        blocks until the bytes are in host memory."""
+        res = self.render(cam, width, height, options, verify)
+        if res.rgb8 is None:
+            return HostFrame(None, None, res)
+        if host is None or tuple(host.shape) != (height, width, 3) or host.dtype != torch.uint8:
+            raise UsageError("host frame must be a (H, W, 3) uint8 tensor")
+        main = torch.cuda.current_stream(self.device)
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        self._copy_stream.wait_event(ready)
+        with torch.cuda.stream(self._copy_stream):
+            host.copy_(res.rgb8, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self._copy_stream)
+        self._pending_copy = done
+        return HostFrame(host, done, res)
+
+
+@dataclass
+class HostFrame:
+    """A frame on its way to host memory (VolumeRenderer.render_to_host)."""
+
+    pixels: Optional[torch.Tensor]
+    event: Optional[torch.cuda.Event]
+    result: RenderResult
+
+    def wait(self) -> Optional[torch.Tensor]:
+        if self.event is not None:
+            self.event.synchronize()
+        return self.pixels
 
 
 def render_volume_with(ep: RankEndpoint, brick: dev.DeviceBrick, decomposition: Decomposition,
