@@ -136,7 +136,8 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     b->quad = nullptr;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
 #if DPRT_QUAD
-    if (e == cudaSuccess) e = cudaMalloc(&b->quad, (size_t)nvox * sizeof(float4));
+    // quad layout: 16 B per voxel; octet layout (DPRT_QUAD == 2): 32 B per voxel
+    if (e == cudaSuccess) e = cudaMalloc(&b->quad, (size_t)nvox * sizeof(float4) * (DPRT_QUAD == 2 ? 2 : 1));
 #endif
     if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));

@@ -91,12 +91,34 @@ __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long l
     quad[(z * sd1 + y) * sd0 + x] = make_float4(r0[x], r0[x1], r1[x], r1[x1]);
 }
 
+// Octet layout (DPRT_QUAD == 2): the 8 corners of the cell a voxel anchors, 32 bytes, one 256-bit load.
+__global__ void octet_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
+                             float4* __restrict__ oct) {
+    const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long y = blockIdx.y, z = blockIdx.z;
+    if (x >= sd0) return;
+    const long long x1 = x + 1 < sd0 ? x + 1 : x;
+    const long long y1 = y + 1 < sd1 ? y + 1 : y;
+    const long long z1 = z + 1 < sd2 ? z + 1 : z;
+    const float* r00 = vox + (z * sd1 + y) * sd0;
+    const float* r10 = vox + (z * sd1 + y1) * sd0;
+    const float* r01 = vox + (z1 * sd1 + y) * sd0;
+    const float* r11 = vox + (z1 * sd1 + y1) * sd0;
+    const long long i = (z * sd1 + y) * sd0 + x;
+    oct[2 * i] = make_float4(r00[x], r00[x1], r10[x], r10[x1]);
+    oct[2 * i + 1] = make_float4(r01[x], r01[x1], r11[x], r11[x1]);
+}
+
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream) {
 #if DPRT_QUAD
     {
         dim3 qb(256);
         dim3 qg((unsigned)((b.sd[0] + 255) / 256), (unsigned)b.sd[1], (unsigned)b.sd[2]);
+#if DPRT_QUAD == 2
+        octet_kernel<<<qg, qb, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], b.quad);
+#else
         quad_kernel<<<qg, qb, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], b.quad);
+#endif
     }
 #endif
     dim3 block(64);

@@ -257,7 +257,10 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                 C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
                 A += w;
             };
-#if DPRT_QUAD
+#if DPRT_QUAD == 2
+            const float4* q = quad + 2u * ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+            const float4 qa = __ldg(q), qb = __ldg(q + 1);
+#elif DPRT_QUAD
             // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
             const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
             const float4 qa = __ldg(q), qb = __ldg(q + sz);
@@ -440,7 +443,13 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                         const float uy = fmaf(fs, st[1], p0[1]);
                         const float uz = fmaf(fs, st[2], p0[2]);
                         const int ix = fl2cell(ux, chx), iy = fl2cell(uy, chy), iz = fl2cell(uz, chz);
-#if DPRT_QUAD
+#if DPRT_QUAD == 2
+                        const float4* q = quad + 2u * ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
+                        asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                                     : "=f"(qa[u].x), "=f"(qa[u].y), "=f"(qa[u].z), "=f"(qa[u].w), "=f"(qb[u].x),
+                                       "=f"(qb[u].y), "=f"(qb[u].z), "=f"(qb[u].w)
+                                     : "l"(q));
+#elif DPRT_QUAD
                         const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
                         qa[u] = __ldg(q);
                         qb[u] = __ldg(q + sz);
