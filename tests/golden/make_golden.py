@@ -15,6 +15,7 @@ CUDA marcher restate:
   PPM              ppm.encode_ppm (ppm.py:12-16)
   longest axis     geom.Aabb.longest_axis (geom.py:107-116)
   auto camera      cli.default_camera (cli.py:23-34)
+  wire format      protocol.encode_message (protocol.py:196-209) for frame / camera / control messages
 """
 
 from __future__ import annotations
@@ -29,7 +30,7 @@ REF = Path(sys.argv[1] if len(sys.argv) > 1 else "/root/reference")
 sys.path.insert(0, str(REF / "pkg" / "src"))
 os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
 
-from dprt import cli, engine, geom, ppm, transport  # noqa: E402
+from dprt import cli, engine, geom, ppm, protocol, transport  # noqa: E402
 from dprt.scene import SceneDesc  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -118,6 +119,14 @@ def main() -> None:
         autocams.append([*cam.position, *cam.view_dir, *cam.up, cam.fov_y, cam.aspect])
     data["autocam_bounds"] = bounds
     data["autocam"] = np.array(autocams, np.float64)
+
+    # --- service wire format (protocol.py): frame, camera update, control messages
+    px = (np.arange(5 * 4 * 3) % 251).astype(np.uint8).tobytes()
+    msgs = [protocol.FrameMessage(width=5, height=4, sequence=7, render_millis=12, pixels=px),
+            protocol.CameraUpdateMessage((1.0, 2.0, 3.0), (0.0, 0.0, -1.0), (0.0, 1.0, 0.0), 45.0, 640, 360),
+            protocol.ControlMessage({"status": "busy"})]
+    for i, m in enumerate(msgs):
+        data[f"wire_{i}"] = np.frombuffer(protocol.encode_message(m), np.uint8)
 
     np.savez_compressed(OUT / "reference_vectors.npz", **data)
 
