@@ -61,13 +61,14 @@ def test_serve_streams_frames_latest_wins_and_refuses_second_client(cuda_device)
         client_out["busy"] = _recv_messages(s2, 1)
         s2.close()
         got = msgs
-        deadline = time.time() + 60
-        while time.time() < deadline:
-            more = _recv_messages(s, 1, timeout=2.0) if True else []
-            got.extend(more)
-            if got and isinstance(got[-1], FrameMessage) and got[-1].sequence >= 2 and len(got) >= 2:
-                # newest update rendered?
+        while True:  # drain until the server goes quiet
+            try:
+                more = _recv_messages(s, 1, timeout=3.0)
+            except socket.timeout:
                 break
+            if not more:
+                break
+            got.extend(more)
         client_out["frames"] = got
         s.close()
 
