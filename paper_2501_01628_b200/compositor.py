@@ -26,7 +26,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import torch
 
-from .errors import UsageError
+from .errors import TransportError, UsageError
 from .transport import RankEndpoint
 
 
@@ -122,7 +122,7 @@ class Compositor:
         if P == 1:
             return "single"
         if mode == "auto":
-            return "direct_send"
+            return "auto"  # p2p if every rank can map its peers (decided collectively), else direct_send
         if mode == "binary_swap" and P & (P - 1):
             raise UsageError(f"binary_swap needs a power-of-two rank count, got {P}")
         if mode not in ("direct_send", "binary_swap", "p2p"):
@@ -153,6 +153,8 @@ class Compositor:
         if sorted(order) != list(range(self.ep.R)):
             raise UsageError(f"visibility order {order} is not a permutation of {self.ep.R} ranks")
         self.last_bytes = 0
+        if self.mode == "auto":
+            self.shared_partial()  # resolves auto collectively
         if self.mode == "single" or solo:
             return self._single(partial, background, keep_float)
         if self.mode == "direct_send":
@@ -259,7 +261,16 @@ class Compositor:
         raise AssertionError("binary swap with P > 1 always has a last round")
 
     def shared_partial(self) -> Optional[torch.Tensor]:
-        """The buffer the marcher should write into (peer-mapped in p2p mode), or None for any buffer."""
+        """The buffer the marcher should write into (peer-mapped in p2p mode), or None for any buffer.
+        In ``auto`` mode this is where the fused path is chosen: every rank tries to map its peers'
+        buffers and the group switches to p2p only if all succeed (collective), else to direct_send."""
+        if self.mode == "auto":
+            impl = None
+            if self.device.type == "cuda":
+                from .p2p import P2PCompositor
+                impl = P2PCompositor.try_create(self.ep, self.W, self.H, self.device)
+            self._p2p_impl = impl
+            self.mode = "p2p" if impl is not None else "direct_send"
         if self.mode != "p2p":
             return None
         return self._p2p().partial.tensor
@@ -267,7 +278,11 @@ class Compositor:
     def _p2p(self):
         if getattr(self, "_p2p_impl", None) is None:
             from .p2p import P2PCompositor
-            self._p2p_impl = P2PCompositor(self.ep, self.W, self.H, self.device)
+            impl = P2PCompositor.try_create(self.ep, self.W, self.H, self.device)
+            if impl is None:
+                raise TransportError("p2p compositing needs every rank to map its peers' buffers "
+                                     "(CUDA IPC over NVLink); use composite='direct_send'")
+            self._p2p_impl = impl
         return self._p2p_impl
 
     def _p2p_composite(self, partial, order, background, keep_float) -> CompositeOutput:

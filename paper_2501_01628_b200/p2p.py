@@ -24,19 +24,37 @@ from .transport import RankEndpoint
 
 class P2PCompositor:
     def __init__(self, ep: RankEndpoint, width: int, height: int, device: torch.device):
+        """Collective.  Local failures never skip a collective call: they leave ``self.ok`` False."""
         self.ep = ep
         self.W = width
         self.H = height
         self.device = device
         self.index = device.index if device.index is not None else torch.cuda.current_device()
         n = width * height
-        self.partial = dev.DeviceBuffer(device, n * 4)
-        self.frame = dev.DeviceBuffer(device, n * 3, torch.uint8) if ep.rank == 0 else None
-        self.frame_rgba: Optional[dev.DeviceBuffer] = None
-        self.peer_partials = ep.share_pointers(self.index, self.partial.ptr)
+        self.ok = True
+        self.partial = self.frame = self.frame_rgba = None
+        try:
+            self.partial = dev.DeviceBuffer(device, n * 4)
+            if ep.rank == 0:
+                self.frame = dev.DeviceBuffer(device, n * 3, torch.uint8)
+        except Exception:  # noqa: BLE001 - reported through self.ok
+            self.ok = False
+        self.peer_partials = ep.share_pointers(self.index, self.partial.ptr if self.partial else 0)
         self.root_frame = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)[0]
+        self.ok = self.ok and all(self.peer_partials) and self.root_frame != 0
         self.root_rgba = 0
         self.last_bytes = 0
+
+    @classmethod
+    def try_create(cls, ep: RankEndpoint, width: int, height: int, device: torch.device) -> Optional["P2PCompositor"]:
+        """Collectively set up peer mappings; every rank gets None if any rank cannot (no NVLink P2P,
+        IPC refused, ...), so the caller can pick the NCCL exchange instead -- on every rank alike."""
+        impl = cls(ep, width, height, device)
+        flags = ep.all_gather_bytes(b"1" if impl.ok else b"0")
+        if all(f == b"1" for f in flags):
+            return impl
+        impl.close()
+        return None
 
     def _ensure_rgba(self) -> None:
         if self.root_rgba:
@@ -69,8 +87,6 @@ class P2PCompositor:
 
     def close(self) -> None:
         self.ep.unshare_pointers(self.index, self.peer_partials)
-        self.partial.close()
-        if self.frame is not None:
-            self.frame.close()
-        if self.frame_rgba is not None:
-            self.frame_rgba.close()
+        for buf in (self.partial, self.frame, self.frame_rgba):
+            if buf is not None:
+                buf.close()

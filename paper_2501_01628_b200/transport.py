@@ -221,14 +221,22 @@ class DistEndpoint(RankEndpoint):
         """CUDA IPC: export this rank's buffer, map every peer's (lazily enabling NVLink peer access)."""
         from . import device as dev
 
-        handle = dev.ipc_handle(device_index, ptr) if ptr else b""
-        handles = self.all_gather_bytes(handle)
+        handle = b""
+        if ptr:
+            try:
+                handle = dev.ipc_handle(device_index, ptr)
+            except Exception:  # noqa: BLE001 - a 0 entry tells every rank this mapping failed
+                handle = b""
+        handles = self.all_gather_bytes(handle)  # always collective, even after a local failure
         out = []
         for r, h in enumerate(handles):
             if r == self.rank:
                 out.append(ptr)
             elif h:
-                out.append(dev.ipc_open(device_index, h))
+                try:
+                    out.append(dev.ipc_open(device_index, h))
+                except Exception:  # noqa: BLE001
+                    out.append(0)
             else:
                 out.append(0)
         return out
@@ -238,7 +246,10 @@ class DistEndpoint(RankEndpoint):
 
         for r, p in enumerate(ptrs):
             if r != self.rank and p:
-                dev.ipc_close(device_index, p)
+                try:
+                    dev.ipc_close(device_index, p)
+                except Exception:  # noqa: BLE001 - best effort on teardown
+                    pass
 
     def device_barrier(self) -> None:
         if self._token is None:

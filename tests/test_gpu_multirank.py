@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("mode,R", [("direct_send", 2), ("direct_send", 3), ("binary_swap", 4), ("p2p", 2),
-                                    ("p2p", 4), ("binary_swap", 8)])
+                                    ("p2p", 4), ("binary_swap", 8), ("auto", 3)])
 def test_sort_last_frame_matches_oracle(cuda_device, oracle_lib, mode, R):
     s = c1(P=R, W=160, H=122)
     vox = oracle.generate_field(s.field.dims, s.field.blobs)
@@ -38,6 +38,8 @@ def test_sort_last_frame_matches_oracle(cuda_device, oracle_lib, mode, R):
             torch.cuda.synchronize()
             samples = res.samples.cpu().numpy().astype(np.uint32)
             out.append((res.image, None if res.rgb8 is None else res.rgb8.cpu().numpy(), samples, res.order))
+        if mode == "auto":  # same process, one GPU: the peer mapping succeeds, so auto picks the fused path
+            assert vr.compositor.mode == "p2p"
         return out
 
     results = run_collective(R, body, device=cuda_device)
