@@ -356,10 +356,9 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
         const int ka = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
         const int kb = ka == 0 ? 1 : 0, kc = ka == 2 ? 1 : 2;
         // this ray's components permuted to (a, b, c) once, so the loops below index no arrays
-#define DPRT_SEL3(v, k3) ((k3) == 0 ? (v)[0] : ((k3) == 1 ? (v)[1] : (v)[2]))
-        const float sa = DPRT_SEL3(st, ka), sb = DPRT_SEL3(st, kb), sc = DPRT_SEL3(st, kc);
-        const float pa = DPRT_SEL3(p0, ka), pb = DPRT_SEL3(p0, kb), pc = DPRT_SEL3(p0, kc);
-#undef DPRT_SEL3
+        auto sel = [&](const float* v, int k3) { return k3 == 0 ? v[0] : (k3 == 1 ? v[1] : v[2]); };
+        const float sa = sel(st, ka), sb = sel(st, kb), sc = sel(st, kc);
+        const float pa = sel(p0, ka), pb = sel(p0, kb), pc = sel(p0, kc);
         const int cha = ka == 0 ? chx : (ka == 1 ? chy : chz);
         const int chb = kb == 0 ? chx : (kb == 1 ? chy : chz);
         const int chc = kc == 0 ? chx : (kc == 1 ? chy : chz);
