@@ -250,6 +250,30 @@ def run_ours(args):
     ms_step = float(ms_t.item()) / args.steps
     fps = 1000.0 / ms_step
 
+    # ---- compositing exchange alone (N > 1): fragments over NVLink + blend + gather, max over ranks
+    nvlink = None
+    if R > 1:
+        order = renderer.decomposition.visibility_order(cam.position)
+        comp = renderer.compositor
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for a_, b_ in cev:
+            a_.record(stream)
+            comp.composite(renderer.partial, order, BACKGROUND)
+            b_.record(stream)
+        barrier()
+        cms = torch.tensor([sum(a_.elapsed_time(b_) for a_, b_ in cev) / len(cev)], dtype=torch.float64,
+                           device=device)
+        dist.all_reduce(cms, op=dist.ReduceOp.MAX)
+        comp_ms = float(cms.item())
+        frag_bytes = int((1 - 1 / R) * W * H * 16)          # RGBA f32 fragments each rank sends
+        gather_bytes = int((R - 1) / R * W * H * 3)          # RGB8 tiles into rank 0
+        achieved_nv = frag_bytes / (comp_ms * 1e-3) / 1e9
+        nvlink = {"bound": "nvlink", "achieved": achieved_nv, "peak": 770.0, "unit": "GB/s",
+                  "frac": achieved_nv / 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                  "composite_ms": comp_ms, "fragment_bytes_per_rank": frag_bytes, "rgb8_into_root": gather_bytes,
+                  "mode": comp.mode}
+
     # ---- marcher alone, CUDA events on its launch stream (roofline)
     partial = renderer.partial
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -334,6 +358,7 @@ def run_ours(args):
                          "footprint_px": fp_px},
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
+            "compositor_roofline": nvlink,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
