@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
             }
             const int B0 = __reduce_min_sync(FULL, b0), B1 = __reduce_max_sync(FULL, b1);
             const int Cc0 = __reduce_min_sync(FULL, c0), Cc1 = __reduce_max_sync(FULL, c1);
-            int dmin = 0, mine = 0;
+            int dmin = 0;
             if (a.skip && B1 >= B0) {
                 const int nb = B1 - B0 + 1, nc = Cc1 - Cc0 + 1;
                 if (nb * nc <= 32) {
@@ -412,12 +412,6 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                         dl = (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx);
                     }
                     dmin = __reduce_min_sync(FULL, dl);
-                    // a lane whose slab samples all lie in ONE macrocell learns its distance from the lane
-                    // that loaded it; if that macrocell is empty the lane drops its slab samples (exact)
-                    const bool single = jend > j && b0 == b1 && c0 == c1;
-                    const int src = single ? (b0 - B0) + (c0 - Cc0) * nb : 0;
-                    const int got = __shfl_sync(FULL, dl, src);
-                    mine = single ? got : 0;
                 }
             }
             if (dmin > 0) {
@@ -434,12 +428,6 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                     if (j >= nn) live = false;
                 }
                 continue;
-            }
-            if (mine > 0) {
-#if DPRT_COUNTERS
-                ++c_skip;
-#endif
-                j = jend;  // this lane's samples in slab K sit in an empty macrocell: nothing to shade
             }
             // Shade this lane's samples in the slab, kBeamUnroll at a time: all their corner loads are
             // issued before the first is shaded, so each lane keeps several loads in flight.
