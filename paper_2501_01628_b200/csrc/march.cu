@@ -22,6 +22,10 @@
 
 #include "common.cuh"
 
+#ifndef DPRT_BOUNDS_CHECK
+#define DPRT_BOUNDS_CHECK 0
+#endif
+
 namespace dprt {
 
 #if DPRT_COUNTERS
@@ -262,6 +266,9 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             const float4 qa = __ldg(q), qb = __ldg(q + 1);
 #elif DPRT_QUAD
             // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
+#if DPRT_BOUNDS_CHECK
+            if ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix + sz >= (unsigned)(a.sd[0] * a.sd[1] * a.sd[2])) __trap();
+#endif
             const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
             const float4 qa = __ldg(q), qb = __ldg(q + sz);
 #else
@@ -450,6 +457,9 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                                        "=f"(qb[u].y), "=f"(qb[u].z), "=f"(qb[u].w)
                                      : "l"(q));
 #elif DPRT_QUAD
+#if DPRT_BOUNDS_CHECK
+                        if ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix + sz >= (unsigned)(a.sd[0] * a.sd[1] * a.sd[2])) __trap();
+#endif
                         const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
                         qa[u] = __ldg(q);
                         qb[u] = __ldg(q + sz);
