@@ -315,12 +315,21 @@ class InprocEndpoint(RankEndpoint):
         self.session = session
 
     def _get(self, q, what: str):
+        """Blocking receive that gives up at the deadline or as soon as another rank has failed
+        (the abort-on-failure behaviour of run_collective, transport.py:533-543)."""
         import queue
+        import time as _time
 
-        try:
-            return q.get(timeout=self.session.timeout)
-        except queue.Empty:
-            raise TransportError(f"rank {self.rank}: timeout after {self.session.timeout:g}s waiting for {what}") from None
+        deadline = _time.monotonic() + self.session.timeout
+        while True:
+            try:
+                return q.get(timeout=0.02)
+            except queue.Empty:
+                if self.session.aborted.is_set():
+                    raise TransportError(f"rank {self.rank}: collective aborted while waiting for {what}") from None
+                if _time.monotonic() > deadline:
+                    raise TransportError(f"rank {self.rank}: timeout after {self.session.timeout:g}s waiting "
+                                         f"for {what}") from None
 
     def _send_ctrl(self, dst: int, kind: str, payload) -> None:
         tag = self._tag(f"{kind}->{dst}")

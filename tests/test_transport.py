@@ -81,3 +81,32 @@ def test_solo_endpoint_identities():
         ep.broadcast_from_root(None)
     with pytest.raises(TransportError):
         ep.exchange([(1, torch.zeros(1))], [])
+
+
+def test_inproc_failure_aborts_peers_quickly():
+    """A raising rank aborts the others' pending collectives (transport.py:533-543); the original error
+    is the one re-raised, and nobody waits for the 30 s deadline."""
+    import time
+
+    from paper_2501_01628_b200.transport import run_collective
+
+    def body(ep):
+        if ep.rank == 1:
+            raise ValueError("boom")
+        ep.gather_to_root(b"x")  # rank 0 would wait for rank 1 forever
+
+    t0 = time.monotonic()
+    with pytest.raises(ValueError, match="boom"):
+        run_collective(2, body, timeout=30.0)
+    assert time.monotonic() - t0 < 5.0
+
+
+def test_inproc_timeout_names_the_peer():
+    from paper_2501_01628_b200.transport import run_collective
+
+    def body(ep):
+        if ep.rank == 0:
+            ep.gather_to_root(b"x")  # rank 1 never sends
+
+    with pytest.raises(TransportError, match="TILE from rank 1"):
+        run_collective(2, body, timeout=0.5)
