@@ -87,6 +87,22 @@ class RenderResult:
     order: Optional[List[int]] = None
 
 
+_TF_HASHES: "dict[int, tuple]" = {}
+
+
+def _tf_hash(tf: TransferFunction1D) -> str:
+    """sha256 of the table bytes, memoised per table object (the digest is computed every frame)."""
+    key = id(tf.table)
+    hit = _TF_HASHES.get(key)
+    if hit is not None and hit[0] is tf.table:
+        return hit[1]
+    h = hashlib.sha256(tf.as_f32().tobytes()).hexdigest()
+    if len(_TF_HASHES) > 64:
+        _TF_HASHES.clear()
+    _TF_HASHES[key] = (tf.table, h)
+    return h
+
+
 def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptions, tf: TransferFunction1D,
                   background: Vec3, decomposition: Decomposition) -> bytes:
     """sha256 of every collective render parameter (engine.py:410-424), extended with the transfer
@@ -97,7 +113,7 @@ def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptio
         "size": [width, height],
         "dt": options.dt, "ert": options.ert, "composite": options.composite,
         "skip": options.skip_empty, "disableCompositing": options.disable_compositing,
-        "tf": [hashlib.sha256(tf.as_f32().tobytes()).hexdigest(), tf.vmin, tf.vmax],
+        "tf": [_tf_hash(tf), tf.vmin, tf.vmax],
         "field": [list(f.dims), list(f.origin), list(f.spacing)],
         "bricks": [[list(lo), list(hi)] for lo, hi in decomposition.boxes],
         "background": list(background),
@@ -158,7 +174,7 @@ class VolumeRenderer:
         if options.composite not in COMPOSITE_MODES:
             raise UsageError(f"unknown composite mode {options.composite!r}; choose from {COMPOSITE_MODES}")
         stats = RankStats()
-        if verify:
+        if verify and self.ep.R > 1:  # one rank cannot diverge from itself
             verify_collective_digest(self.ep, render_digest(cam, width, height, options, self.tf,
                                                             self.background, self.decomposition))
         self._ensure(width, height, options.composite)
