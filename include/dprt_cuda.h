@@ -118,6 +118,12 @@ int dprt_brick_footprint(const DprtBrick* b, const DprtCamera* cam, int W, int H
 int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
                uint32_t* samples, int W, int H, void* stream);
 
+/* Single-rank frame (R == 1): the same march with the compositor's over-background and tone map fused
+ * into the ray's last step -- writes the (W*H*3) RGB8 frame directly, no RGBA partial, no composite pass.
+ * Equivalent to dprt_march + dprt_composite(P = 1, DPRT_COMPOSITE_TONEMAP). */
+int dprt_march_rgb8(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, const float bg[3],
+                    uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream);
+
 /* Sort-last 'over' of P contiguous fragments of npix pixels each, already in front-to-back order
  * (DESIGN.md §2.8).  Replaces the reference's order-independent (t, gid) min (bvh.py:246-248) plus
  * the final tone map (engine.py:500-502) for the pixels a rank owns (engine.py:216-221).  `inputs`

@@ -37,7 +37,7 @@ EXPORTS = (
     "dprt_cuda_version", "dprt_last_error", "dprt_device_count", "dprt_device_synchronize",
     "dprt_brick_create", "dprt_brick_stored", "dprt_brick_upload", "dprt_brick_download",
     "dprt_brick_generate", "dprt_brick_build_macrocells", "dprt_brick_destroy", "dprt_brick_footprint",
-    "dprt_march", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
+    "dprt_march", "dprt_march_rgb8", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
     "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters",
 )
 
@@ -85,6 +85,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_brick_destroy": ([P], I),
         "dprt_brick_footprint": ([P, P, I, I, P], I),
         "dprt_march": ([P, P, P, P, P, I, I, P], I),
+        "dprt_march_rgb8": ([P, P, P, P, P, P, I, I, P], I),
         "dprt_composite": ([I, P, I, ctypes.c_int64, P, I, P, P, P], I),
         "dprt_ipc_handle": ([I, P, P], I),
         "dprt_ipc_open": ([I, P, P], I),

@@ -272,9 +272,24 @@ int dprt_brick_footprint(const DprtBrick* b, const DprtCamera* cam, int W, int H
     return DPRT_OK;
 }
 
+static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
+                      const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream);
+
 int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
                uint32_t* samples, int W, int H, void* stream) {
-    if (!b || !cam || !p || !partial_rgba) return fail(DPRT_E_USAGE, "null march argument");
+    if (!partial_rgba) return fail(DPRT_E_USAGE, "null partial buffer");
+    return march_impl(b, cam, p, partial_rgba, nullptr, nullptr, samples, W, H, stream);
+}
+
+int dprt_march_rgb8(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, const float bg[3],
+                    uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream) {
+    if (!rgb8 || !bg) return fail(DPRT_E_USAGE, "null rgb8 frame or background");
+    return march_impl(b, cam, p, nullptr, bg, rgb8, samples, W, H, stream);
+}
+
+static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
+                      const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream) {
+    if (!b || !cam || !p) return fail(DPRT_E_USAGE, "null march argument");
     if (W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "frame size %dx%d must be positive", W, H);
     if (p->n_tf < 2 || p->n_tf > dprt::kMaxTf || !p->tf_rgba)
         return fail(DPRT_E_USAGE, "transfer function needs 2..%d entries (got %d)", dprt::kMaxTf, p->n_tf);
@@ -310,12 +325,19 @@ int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams*
     a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
+    if (rgb8) a.beam = 1;  // the fused RGB8 output exists in the beam marcher only
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
     a.n_tf = p->n_tf;
     a.vmin = (float)p->vmin;
     a.tf_scale = (float)((double)(p->n_tf - 1) / (p->vmax - p->vmin));
     a.ert = (float)p->ert;
     a.out = reinterpret_cast<float4*>(partial_rgba);
+    a.rgb8 = rgb8;
+    if (bg) {
+        a.bg[0] = bg[0];
+        a.bg[1] = bg[1];
+        a.bg[2] = bg[2];
+    }
     a.samples = samples;
     a.W = W;
     a.H = H;

@@ -72,6 +72,8 @@ struct MarchArgs {
     float vmin, tf_scale, ert;
     // output
     float4* __restrict__ out;
+    uint8_t* rgb8;  // non-null: write the tone-mapped frame over bg[] instead of the RGBA partial (R == 1)
+    float bg[3];
     uint32_t* __restrict__ samples;
     float4* rays;   // compacted ray queue: 2 float4 per ray {p0, pixel}, {step, n}
     int* counters;  // [0] rays queued by ray_setup, [1] rays taken by march

@@ -508,7 +508,18 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
             }
             if (j >= nn) live = false;
         }
-        if (nn > 0) a.out[pix] = make_float4(C0, C1, C2, A);
+        if (nn > 0) {
+            if (a.rgb8) {
+                // single-rank frame: the over-background + tone map of the compositor, fused (engine.py:500-502)
+                const float one = 1.f - A;
+                uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
+                dst[0] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[0], C0), 0.f), 1.f) * 255.f + 0.5f);
+                dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
+                dst[2] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[2], C2), 0.f), 1.f) * 255.f + 0.5f);
+            } else {
+                a.out[pix] = make_float4(C0, C1, C2, A);
+            }
+        }
     }
 #if DPRT_COUNTERS
     DPRT_COUNT(0, c_shade);
@@ -582,6 +593,32 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
     return cudaMemcpyAsync(b.skipd, tmp, (size_t)nmc, cudaMemcpyDeviceToDevice, stream);
 }
 
+// Background frame for the fused single-rank path: tone_map(bg) in every pixel, 4 pixels per thread.
+__global__ void fill_rgb8_kernel(uint8_t* __restrict__ rgb8, long long npix, float r, float g, float b) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long i0 = 4 * q;
+    if (i0 >= npix) return;
+    const uint32_t cr = (uint32_t)floorf(fminf(fmaxf(r, 0.f), 1.f) * 255.f + 0.5f);
+    const uint32_t cg = (uint32_t)floorf(fminf(fmaxf(g, 0.f), 1.f) * 255.f + 0.5f);
+    const uint32_t cb = (uint32_t)floorf(fminf(fmaxf(b, 0.f), 1.f) * 255.f + 0.5f);
+    uint8_t* dst = rgb8 + 3 * i0;
+    if (i0 + 4 <= npix && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+        const uint32_t w0 = cr | (cg << 8) | (cb << 16) | (cr << 24);
+        const uint32_t w1 = cg | (cb << 8) | (cr << 16) | (cg << 24);
+        const uint32_t w2 = cb | (cr << 8) | (cg << 16) | (cb << 24);
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+        d32[0] = w0;
+        d32[1] = w1;
+        d32[2] = w2;
+        return;
+    }
+    for (long long i = i0; i < npix && i < i0 + 4; ++i) {
+        rgb8[3 * i] = (uint8_t)cr;
+        rgb8[3 * i + 1] = (uint8_t)cg;
+        rgb8[3 * i + 2] = (uint8_t)cb;
+    }
+}
+
 cudaError_t read_counters(unsigned long long out[4], int reset) {
 #if DPRT_COUNTERS
     cudaError_t e = cudaMemcpyFromSymbol(out, g_counters, 4 * sizeof(unsigned long long));
@@ -613,8 +650,16 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = 2 * a.n_tf * sizeof(float4);
     if (a.beam) {
-        // pixels the beams do not write (misses, outside the footprint) must read as zero
-        e = cudaMemsetAsync(a.out, 0, (size_t)a.W * a.H * sizeof(float4), stream);
+        // pixels the beams do not write (misses, outside the footprint) must read as zero -- or as the
+        // tone-mapped background when the beams write the RGB8 frame directly
+        if (a.rgb8) {
+            const long long quads = ((long long)a.W * a.H + 3) / 4;
+            fill_rgb8_kernel<<<(unsigned)((quads + 255) / 256), 256, 0, stream>>>(a.rgb8, (long long)a.W * a.H,
+                                                                              a.bg[0], a.bg[1], a.bg[2]);
+            e = cudaGetLastError();
+        } else {
+            e = cudaMemsetAsync(a.out, 0, (size_t)a.W * a.H * sizeof(float4), stream);
+        }
         if (e == cudaSuccess && a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.W * a.H * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kTileX * kTileY, smem);

@@ -190,6 +190,25 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
     _lib.check(rc, "dprt_march")
 
 
+def march_rgb8(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, background,
+               rgb8: torch.Tensor, width: int, height: int, samples: Optional[torch.Tensor] = None,
+               skip: bool = True) -> None:
+    """dprt_march_rgb8: single-rank frame, over-background and tone map fused into the march."""
+    _require_cuda(rgb8, "rgb8", torch.uint8)
+    if rgb8.numel() != width * height * 3:
+        raise UsageError("rgb8 frame must hold 3 bytes per pixel")
+    sp = ctypes.c_void_p(0)
+    if samples is not None:
+        _require_cuda(samples, "samples", torch.int32)
+        sp = ctypes.c_void_p(samples.data_ptr())
+    p = tf.params(dt, ert, 0 if skip else _lib.MARCH_NO_SKIP)
+    c = camera_struct(cam)
+    bg = (ctypes.c_float * 3)(*[float(v) for v in background])
+    rc = _lib.lib().dprt_march_rgb8(brick.handle, ctypes.byref(c), ctypes.byref(p), bg,
+                                    ctypes.c_void_p(rgb8.data_ptr()), sp, width, height, _stream(brick.device))
+    _lib.check(rc, "dprt_march_rgb8")
+
+
 def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[torch.Tensor] = None,
               rgba: Optional[torch.Tensor] = None) -> None:
     """dprt_composite: front-to-back 'over' of equally sized RGBA fragments (already in visibility

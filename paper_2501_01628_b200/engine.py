@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import hashlib
 import json
+import os
 import time
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
@@ -180,6 +181,20 @@ class VolumeRenderer:
         self._ensure(width, height, options.composite)
         order = visibility_order(self.decomposition, cam.position)
         t0 = time.perf_counter()
+        if self.ep.R == 1 and not options.keep_float and os.environ.get("DPRT_FUSED_SINGLE", "1") != "0":
+            # one rank: the composite is just over-background + tone map -> fused into the march
+            if self._pending_copy is not None:
+                torch.cuda.current_stream(self.device).wait_event(self._pending_copy)
+                self._pending_copy = None
+            frame, _ = self.compositor._frame_buffers(False)
+            dev.march_rgb8(self.brick, cam, self.dtf, options.dt, options.ert, self.background, frame.view(-1),
+                           width, height, samples=self.samples if options.collect_samples else None,
+                           skip=options.skip_empty)
+            stats.record(options.frame_index, width * height, 0, (time.perf_counter() - t0) * 1e3)
+            res = RenderResult(rgb8=frame, stats=stats, order=order)
+            if options.collect_samples:
+                res.samples = self.samples.view(height, width)
+            return res
         dev.march(self.brick, cam, self.dtf, options.dt, options.ert, self.partial, width, height,
                   samples=self.samples if options.collect_samples else None, skip=options.skip_empty)
         if options.disable_compositing:

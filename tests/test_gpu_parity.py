@@ -191,3 +191,20 @@ def test_skip_cache_follows_tf_updates(cuda_device, oracle_lib):
         ref, _ = oracle_partials(vox, dec, cam, tf, 1.0, 0.99, W, H)
         _check_rgba(p.view(H, W, 4).cpu().numpy(), ref[0], "after TF update")
     b.close()
+
+
+def test_fused_single_rank_frame_equals_composited(cuda_device, oracle_lib, monkeypatch):
+    """R == 1: dprt_march_rgb8 (over-background + tone map fused into the march) gives the same bytes as
+    dprt_march + dprt_composite(P=1), and matches the oracle within 1 LSB."""
+    s = c1(P=1, W=200, H=150)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, _ = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H)
+    want = oracle.tone_map_rgb8(oracle.composite(ref, [0], s.background)).astype(np.int16)
+    brick = dev.DeviceBrick(s.dec.brick(0), cuda_device).generate(s.field)
+    r = VolumeRenderer(SoloEndpoint(cuda_device), brick, s.dec, s.tf, s.background)
+    fused = r.render(s.cam, s.W, s.H).rgb8.cpu().numpy().copy()
+    monkeypatch.setenv("DPRT_FUSED_SINGLE", "0")
+    plain = r.render(s.cam, s.W, s.H).rgb8.cpu().numpy().copy()
+    assert np.array_equal(fused, plain)
+    assert np.abs(fused.astype(np.int16) - want).max() <= RGB8_MAX_LSB
+    brick.close()
