@@ -154,6 +154,10 @@ class VolumeRenderer:
         self.compositor: Optional[Compositor] = None
         self._copy_stream = None
         self._pending_copy = None
+        self._fused_frames = None
+        self._fused_events = [None, None]
+        self._fused_next = 0
+        self._fused_slot = 0
 
     def set_tf(self, tf: TransferFunction1D) -> None:
         self.tf = tf
@@ -183,10 +187,18 @@ class VolumeRenderer:
         t0 = time.perf_counter()
         if self.ep.R == 1 and not options.keep_float and os.environ.get("DPRT_FUSED_SINGLE", "1") != "0":
             # one rank: the composite is just over-background + tone map -> fused into the march
-            if self._pending_copy is not None:
-                torch.cuda.current_stream(self.device).wait_event(self._pending_copy)
-                self._pending_copy = None
-            frame, _ = self.compositor._frame_buffers(False)
+            # two device frames alternate so the read-back of frame k overlaps the march of frame k+1
+            if self._fused_frames is None or tuple(self._fused_frames[0].shape) != (height, width, 3):
+                self._fused_frames = [torch.empty((height, width, 3), dtype=torch.uint8, device=self.device)
+                                      for _ in range(2)]
+                self._fused_events = [None, None]
+            slot = self._fused_next
+            self._fused_next ^= 1
+            if self._fused_events[slot] is not None:
+                torch.cuda.current_stream(self.device).wait_event(self._fused_events[slot])
+                self._fused_events[slot] = None
+            self._fused_slot = slot
+            frame = self._fused_frames[slot]
             dev.march_rgb8(self.brick, cam, self.dtf, options.dt, options.ert, self.background, frame.view(-1),
                            width, height, samples=self.samples if options.collect_samples else None,
                            skip=options.skip_empty)
@@ -238,7 +250,10 @@ class VolumeRenderer:
             host.copy_(res.rgb8, non_blocking=True)
         done = torch.cuda.Event()
         done.record(self._copy_stream)
-        self._pending_copy = done
+        if self._fused_frames is not None and res.rgb8 is self._fused_frames[self._fused_slot]:
+            self._fused_events[self._fused_slot] = done  # guards only that device frame
+        else:
+            self._pending_copy = done
         return HostFrame(host, done, res)
 
 
