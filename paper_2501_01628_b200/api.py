@@ -56,7 +56,7 @@ _PARAMS: Dict[str, Dict[str, object]] = {
     "camera": {"position": (0.0, 0.0, 3.0), "direction": (0.0, 0.0, -1.0),
                "up": (0.0, 1.0, 0.0), "fovY": 60.0, "aspect": 1.0},
     "renderer": {"background": (0.0, 0.0, 0.0), "dt": 1.0, "ert": 0.99, "composite": "auto",
-                 "skipEmpty": True, "disableCompositing": False},
+                 "skipEmpty": True, "disableCompositing": False, "mode": "dvr"},
     "frame": {"world": None, "camera": None, "renderer": None, "size": (256, 256)},
 }
 
@@ -353,7 +353,7 @@ def render_frame_collective(frame: Frame) -> RenderResult:
     r = renderer.committed
     options = RenderOptions(dt=float(r["dt"]), ert=float(r["ert"]), composite=str(r["composite"]),
                             skip_empty=bool(r["skipEmpty"]), disable_compositing=bool(r["disableCompositing"]),
-                            frame_index=frame.sequence)
+                            frame_index=frame.sequence, mode=str(r["mode"]))
     background = tuple(float(v) for v in r["background"])
     tf = world.volume.committed["transferFunction"].tf()
     vr = frame._renderer

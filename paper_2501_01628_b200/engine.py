@@ -60,6 +60,7 @@ class RenderOptions:
     frame_index: int = 0
     keep_float: bool = False           # also return the float RGB image before quantisation (rank 0)
     collect_samples: bool = False      # also return per-pixel owned sample counts (this rank)
+    mode: str = "dvr"                  # "dvr" or "rankcolor" (rank-ownership visualisation, engine.py:327-332)
 
 
 @dataclass
@@ -104,6 +105,16 @@ def _tf_hash(tf: TransferFunction1D) -> str:
     return h
 
 
+def rankcolor_tf(tf: TransferFunction1D, rank: int) -> TransferFunction1D:
+    """Rank-ownership visualisation (the reference's "rankcolor" mode, engine.py:327-332, RANK_PALETTE
+    engine.py:41-44): every entry that is visible in ``tf`` becomes opaque in this rank's palette colour,
+    so the composited frame shows, per pixel, the first brick in visibility order that holds visible data."""
+    t = tf.as_f32().copy()
+    t[:, :3] = RANK_PALETTE[rank % len(RANK_PALETTE)]
+    t[:, 3] = np.where(t[:, 3] > 0.0, 1.0, 0.0)
+    return TransferFunction1D(t.astype(np.float32), tf.vmin, tf.vmax)
+
+
 def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptions, tf: TransferFunction1D,
                   background: Vec3, decomposition: Decomposition) -> bytes:
     """sha256 of every collective render parameter (engine.py:410-424), extended with the transfer
@@ -113,7 +124,7 @@ def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptio
         "cam": [list(cam.position), list(cam.view_dir), list(cam.up), cam.fov_y, cam.aspect],
         "size": [width, height],
         "dt": options.dt, "ert": options.ert, "composite": options.composite,
-        "skip": options.skip_empty, "disableCompositing": options.disable_compositing,
+        "skip": options.skip_empty, "disableCompositing": options.disable_compositing, "mode": options.mode,
         "tf": [_tf_hash(tf), tf.vmin, tf.vmax],
         "field": [list(f.dims), list(f.origin), list(f.spacing)],
         "bricks": [[list(lo), list(hi)] for lo, hi in decomposition.boxes],
@@ -155,6 +166,8 @@ class VolumeRenderer:
         self._copy_stream = None
         self._pending_copy = None
         self._fused_frames = None
+        self._rank_dtf = None
+        self._rank_tf_src = None
         self._fused_events = [None, None]
         self._fused_next = 0
         self._fused_slot = 0
@@ -178,6 +191,16 @@ class VolumeRenderer:
                verify: bool = True) -> RenderResult:
         if options.composite not in COMPOSITE_MODES:
             raise UsageError(f"unknown composite mode {options.composite!r}; choose from {COMPOSITE_MODES}")
+        if options.mode not in ("dvr", "rankcolor"):
+            raise UsageError(f"unknown render mode {options.mode!r}; choose 'dvr' or 'rankcolor'")
+        if options.mode == "rankcolor":
+            rc = rankcolor_tf(self.tf, self.ep.rank)
+            if self._rank_dtf is None or self._rank_tf_src is not self.tf:
+                self._rank_dtf = dev.DeviceTF(rc, self.device)
+                self._rank_tf_src = self.tf
+            dtf = self._rank_dtf
+        else:
+            dtf = self.dtf
         stats = RankStats()
         if verify and self.ep.R > 1:  # one rank cannot diverge from itself
             verify_collective_digest(self.ep, render_digest(cam, width, height, options, self.tf,
@@ -199,7 +222,7 @@ class VolumeRenderer:
                 self._fused_events[slot] = None
             self._fused_slot = slot
             frame = self._fused_frames[slot]
-            dev.march_rgb8(self.brick, cam, self.dtf, options.dt, options.ert, self.background, frame.view(-1),
+            dev.march_rgb8(self.brick, cam, dtf, options.dt, options.ert, self.background, frame.view(-1),
                            width, height, samples=self.samples if options.collect_samples else None,
                            skip=options.skip_empty)
             stats.record(options.frame_index, width * height, 0, (time.perf_counter() - t0) * 1e3)
@@ -207,7 +230,7 @@ class VolumeRenderer:
             if options.collect_samples:
                 res.samples = self.samples.view(height, width)
             return res
-        dev.march(self.brick, cam, self.dtf, options.dt, options.ert, self.partial, width, height,
+        dev.march(self.brick, cam, dtf, options.dt, options.ert, self.partial, width, height,
                   samples=self.samples if options.collect_samples else None, skip=options.skip_empty)
         if options.disable_compositing:
             order = [self.ep.rank] if self.ep.R == 1 else order

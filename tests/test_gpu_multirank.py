@@ -150,3 +150,34 @@ def test_api_frame_matches_oracle_and_staging(cuda_device, oracle_lib, R, mode):
     want = oracle.tone_map_rgb8(oracle.composite(ref, dec.visibility_order(cam.position), (0.05, 0.06, 0.08)))
     got = np.frombuffer(pix1, np.uint8).reshape(H, W, 3)
     assert np.abs(got.astype(np.int16) - want.astype(np.int16)).max() <= RGB8_MAX_LSB
+
+
+def test_rankcolor_mode_shows_brick_ownership(cuda_device, oracle_lib):
+    """engine.py:327-332 analog: each rank's visible data drawn opaque in RANK_PALETTE[rank]; the frame
+    matches the oracle composite of the same rank-colour TFs and every rank's colour appears."""
+    from paper_2501_01628_b200.engine import RANK_PALETTE, rankcolor_tf
+
+    s = c1(P=3, W=120, H=96)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    order = s.dec.visibility_order(s.cam.position)
+    refs = []
+    for r in range(3):
+        t = rankcolor_tf(s.tf, r)
+        ob = __import__("scenes").oracle_brick(s.dec, r)
+        rgba, _ = oracle.render_brick(ob.extract(vox), ob, __import__("scenes").cam_array(s.cam), t.as_f32(),
+                                      t.vmin, t.vmax, 1.0, 0.99, s.W, s.H)
+        refs.append(rgba)
+    want = oracle.composite(refs, order, s.background)
+
+    def body(ep):
+        b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda_device).generate(s.field)
+        res = VolumeRenderer(ep, b, s.dec, s.tf, s.background).render(
+            s.cam, s.W, s.H, RenderOptions(mode="rankcolor", keep_float=True))
+        torch.cuda.synchronize()
+        return res.image
+
+    img = run_collective(3, body, device=cuda_device)[0]
+    assert np.abs(img - want).max() <= RGBA_ATOL
+    flat = img.reshape(-1, 3)
+    for r in range(3):
+        assert np.any(np.all(np.abs(flat - RANK_PALETTE[r]) < 1e-6, axis=1)), f"rank {r} colour missing"
