@@ -5,7 +5,7 @@ the hot path needs.
 Differences from the reference's facade, all deliberate:
 * new kinds ``spatialField``, ``volume``, ``transferFunction1D`` (the reference rejects "volume",
   api.py:38 / 238-240, pinned by test_api.py:226-231; that test is re-pointed at a genuinely unknown
-  kind in tests/test_api.py);
+  kind in tests/test_api_cpu.py);
 * ``World`` commit decomposes the field into one brick per rank (kd split, volume.decompose) and makes
   this rank's brick resident on its GPU -- the counterpart of the local BVH build (api.py:146-171);
   still purely local, no transport traffic (test_api.py:72-81's property holds);
@@ -152,16 +152,23 @@ class SpatialField(ApiObject):
 
 
 class TransferFunctionObject(ApiObject):
+    _tf: Optional[TransferFunction1D] = None
+
     def tf(self) -> TransferFunction1D:
+        """The committed table (built once per commit, so per-frame digests and uploads reuse it)."""
+        if self._tf is None:
+            self._tf = self._build()
+        return self._tf
+
+    def _build(self) -> TransferFunction1D:
         table = self.committed.get("table")
         lo, hi = self.committed.get("valueRange", (0.0, 1.0))
         if table is None:
-            base = default_tf()
-            return TransferFunction1D(base.table, float(lo), float(hi))
+            return TransferFunction1D(default_tf().table, float(lo), float(hi))
         return TransferFunction1D(np.asarray(table, np.float32), float(lo), float(hi))
 
     def _on_commit(self) -> None:
-        self.tf()
+        self._tf = self._build()
 
 
 class Volume(ApiObject):
