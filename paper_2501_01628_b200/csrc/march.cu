@@ -293,6 +293,32 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 #endif
 constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 
+#ifndef DPRT_BEAM_W
+#define DPRT_BEAM_W 4
+#endif
+constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
+#ifndef DPRT_LDQ
+#define DPRT_LDQ 0
+#endif
+// corner-quad load with an optional cache hint (build-time switch for experiments)
+__device__ __forceinline__ float4 ldq(const float4* q) {
+#if DPRT_LDQ == 1
+    float4 v;
+    asm volatile("ld.global.nc.L2::128B.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q));
+    return v;
+#elif DPRT_LDQ == 2
+    float4 v;
+    asm volatile("ld.global.nc.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q));
+    return v;
+#elif DPRT_LDQ == 3
+    float4 v;
+    asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q));
+    return v;
+#else
+    return __ldg(q);
+#endif
+}
+
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
 #ifndef DPRT_BEAM_MINBLOCKS
@@ -311,7 +337,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
     const unsigned FULL = 0xffffffffu;
     const int lane = tid & 31;
     const int rw = a.rect[2] - a.rect[0], rh = a.rect[3] - a.rect[1];
-    const int tiles_x = (rw + 7) >> 3, tiles_y = (rh + 3) >> 2;
+    const int tiles_x = (rw + kBeamW - 1) / kBeamW, tiles_y = (rh + kBeamH - 1) / kBeamH;
     const int ntiles = tiles_x * tiles_y;
     const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
     const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
@@ -328,8 +354,8 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
         if (lane == 0) tile = atomicAdd(a.counters + 1, 1);
         tile = __shfl_sync(FULL, tile, 0);
         if (tile >= ntiles) break;
-        const int px = a.rect[0] + (tile % tiles_x) * 8 + (lane & 7);
-        const int py = a.rect[1] + (tile / tiles_x) * 4 + (lane >> 3);
+        const int px = a.rect[0] + (tile % tiles_x) * kBeamW + (lane % kBeamW);
+        const int py = a.rect[1] + (tile / tiles_x) * kBeamH + (lane / kBeamW);
         int nn = 0, pix = 0;
         float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
         if (px < a.rect[2] && py < a.rect[3]) {
@@ -461,8 +487,8 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                         if ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix + sz >= (unsigned)(a.sd[0] * a.sd[1] * a.sd[2])) __trap();
 #endif
                         const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-                        qa[u] = __ldg(q);
-                        qb[u] = __ldg(q + sz);
+                        qa[u] = ldq(q);
+                        qb[u] = ldq(q + sz);
 #else
                         const float* pv = a.vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
                         qa[u] = make_float4(__ldg(pv), __ldg(pv + 1), __ldg(pv + sy), __ldg(pv + sy + 1));
