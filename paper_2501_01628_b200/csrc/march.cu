@@ -297,6 +297,9 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 #define DPRT_BEAM_W 4
 #endif
 constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
+#ifndef DPRT_RECOMPUTE_W
+#define DPRT_RECOMPUTE_W 0
+#endif
 #ifndef DPRT_LDQ
 #define DPRT_LDQ 0
 #endif
@@ -494,15 +497,29 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                         qa[u] = make_float4(__ldg(pv), __ldg(pv + 1), __ldg(pv + sy), __ldg(pv + sy + 1));
                         qb[u] = make_float4(__ldg(pv + sz), __ldg(pv + sz + 1), __ldg(pv + sz + sy), __ldg(pv + sz + sy + 1));
 #endif
+#if !DPRT_RECOMPUTE_W
                         wx[u] = __saturatef(ux - (float)ix);
                         wy[u] = __saturatef(uy - (float)iy);
                         wz[u] = __saturatef(uz - (float)iz);
+#endif
                     }
                 }
                 bool stop = false;
 #pragma unroll
                 for (int u = 0; u < kBeamUnroll; ++u) {
                     if (u < cnt && !stop) {
+#if DPRT_RECOMPUTE_W
+                        // weights recomputed after the loads: fewer live registers per batch, more warps
+                        {
+                            const float fs = (float)(j + u);
+                            const float ux = fmaf(fs, st[0], p0[0]);
+                            const float uy = fmaf(fs, st[1], p0[1]);
+                            const float uz = fmaf(fs, st[2], p0[2]);
+                            wx[u] = __saturatef(ux - (float)fl2cell(ux, chx));
+                            wy[u] = __saturatef(uy - (float)fl2cell(uy, chy));
+                            wz[u] = __saturatef(uz - (float)fl2cell(uz, chz));
+                        }
+#endif
                         const float e00 = fmaf(wx[u], qa[u].y - qa[u].x, qa[u].x);
                         const float e10 = fmaf(wx[u], qa[u].w - qa[u].z, qa[u].z);
                         const float e01 = fmaf(wx[u], qb[u].y - qb[u].x, qb[u].x);
