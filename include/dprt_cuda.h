@@ -142,6 +142,13 @@ int dprt_ipc_open(int device, const uint8_t handle[64], void** out_ptr);
 int dprt_ipc_close(int device, void* ptr);
 int dprt_enable_peer(int device, int peer);
 
+/* Known-answer entry points: the marcher's own device functions (slab interval, primary ray) applied to
+ * caller-supplied inputs, HOST arrays in and out.  Used to check the reference's golden vectors
+ * (geom.py:171-200, geom.py:240-259 via engine.gen_primary_batch) on the GPU code itself. */
+int dprt_kat_slab(int device, int n, const double* o, const double* d, const double* lo, const double* hi,
+                  double* t01, int32_t* hit);
+int dprt_kat_primary_dirs(int device, const DprtCamera* cam, int W, int H, double* out);
+
 /* Instrumented builds (-DDPRT_COUNTERS=1) count {shaded samples, contributing samples, skip steps, rays}
  * in march_kernel; other builds report zeros. */
 int dprt_march_counters(int device, uint64_t out[4], int reset);

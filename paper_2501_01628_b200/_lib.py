@@ -38,7 +38,7 @@ EXPORTS = (
     "dprt_brick_create", "dprt_brick_stored", "dprt_brick_upload", "dprt_brick_download",
     "dprt_brick_generate", "dprt_brick_build_macrocells", "dprt_brick_destroy", "dprt_brick_footprint",
     "dprt_march", "dprt_march_rgb8", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
-    "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters",
+    "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters", "dprt_kat_slab", "dprt_kat_primary_dirs",
 )
 
 c_double3 = ctypes.c_double * 3
@@ -94,6 +94,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_device_alloc": ([I, ctypes.c_uint64, P], I),
         "dprt_device_free": ([I, P], I),
         "dprt_march_counters": ([I, P, I], I),
+        "dprt_kat_slab": ([I, I, P, P, P, P, P, P], I),
+        "dprt_kat_primary_dirs": ([I, P, I, I, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

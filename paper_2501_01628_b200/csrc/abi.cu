@@ -20,6 +20,9 @@ cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cud
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream);
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream);
 cudaError_t read_counters(unsigned long long out[4], int reset);
+cudaError_t launch_kat_slab(const double* o, const double* d, const double* lo, const double* hi, int n, double* t01,
+                            int* hit);
+cudaError_t launch_kat_primary(const MarchArgs& a, double* out);
 }  // namespace dprt
 
 struct DprtBrick : dprt::DeviceBrick {};
@@ -406,6 +409,55 @@ int dprt_march_counters(int device, uint64_t out[4], int reset) {
     unsigned long long tmp[4];
     CK(dprt::read_counters(tmp, reset), "march counters");
     for (int i = 0; i < 4; ++i) out[i] = tmp[i];
+    return DPRT_OK;
+}
+
+int dprt_kat_slab(int device, int n, const double* o, const double* d, const double* lo, const double* hi,
+                  double* t01, int32_t* hit) {
+    if (n < 0 || (n > 0 && (!o || !d || !lo || !hi || !t01 || !hit))) return fail(DPRT_E_USAGE, "bad KAT arguments");
+    if (n == 0) return DPRT_OK;
+    int rc = bind(device);
+    if (rc) return rc;
+    double* buf = nullptr;
+    int* h = nullptr;
+    const size_t vec = (size_t)n * 3 * sizeof(double);
+    CK(cudaMalloc(&buf, 4 * vec + (size_t)n * 2 * sizeof(double)), "KAT buffers");
+    cudaError_t e = cudaMalloc(&h, (size_t)n * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(buf, o, vec, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(buf + 3 * n, d, vec, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(buf + 6 * n, lo, vec, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(buf + 9 * n, hi, vec, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = dprt::launch_kat_slab(buf, buf + 3 * n, buf + 6 * n, buf + 9 * n, n, buf + 12 * n, h);
+    if (e == cudaSuccess) e = cudaMemcpy(t01, buf + 12 * n, (size_t)n * 2 * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(hit, h, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    cudaFree(h);
+    if (e != cudaSuccess) return cuda_fail(e, "slab KAT");
+    return DPRT_OK;
+}
+
+int dprt_kat_primary_dirs(int device, const DprtCamera* cam, int W, int H, double* out) {
+    if (!cam || !out || W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "bad KAT arguments");
+    int rc = bind(device);
+    if (rc) return rc;
+    dprt::MarchArgs a;
+    memset(&a, 0, sizeof(a));
+    for (int i = 0; i < 3; ++i) {
+        a.f[i] = cam->fwd[i];
+        a.r[i] = cam->right[i];
+        a.u[i] = cam->up[i];
+    }
+    a.half_w = cam->half_w;
+    a.half_h = cam->half_h;
+    a.W = W;
+    a.H = H;
+    double* buf = nullptr;
+    const size_t bytes = (size_t)W * H * 3 * sizeof(double);
+    CK(cudaMalloc(&buf, bytes), "KAT buffer");
+    cudaError_t e = dprt::launch_kat_primary(a, buf);
+    if (e == cudaSuccess) e = cudaMemcpy(out, buf, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (e != cudaSuccess) return cuda_fail(e, "primary-ray KAT");
     return DPRT_OK;
 }
 

@@ -52,34 +52,82 @@ __device__ __forceinline__ void primary_dir(const MarchArgs& a, int px, int py, 
     d[2] = __ddiv_rn(dz, n);
 }
 
-// geom.py:171-200 + clip to [0, inf) (geom.py:203-209) + lattice range.
-__device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const double d[3], int64_t* k0) {
+// geom.py:171-200: slab interval of the ray against a box (empty box -> miss; a zero direction component
+// is inside-or-miss for that slab), every f64 op explicitly rounded, matching dvr_oracle.c.
+__device__ __forceinline__ bool slab_interval(const double o[3], const double d[3], const double lo[3],
+                                              const double hi[3], double* pt0, double* pt1) {
+    if (lo[0] > hi[0] || lo[1] > hi[1] || lo[2] > hi[2]) return false;
     double t0 = -INFINITY, t1 = INFINITY;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        double di = d[i], oi = a.o[i];
+        const double di = d[i], oi = o[i];
         if (di == 0.0) {
-            if (oi < a.blo[i] || oi > a.bhi[i]) return 0;
+            if (oi < lo[i] || oi > hi[i]) return false;
             continue;
         }
-        double inv = __ddiv_rn(1.0, di);
-        double ta = __dmul_rn(__dsub_rn(a.blo[i], oi), inv);
-        double tb = __dmul_rn(__dsub_rn(a.bhi[i], oi), inv);
+        const double inv = __ddiv_rn(1.0, di);
+        double ta = __dmul_rn(__dsub_rn(lo[i], oi), inv);
+        double tb = __dmul_rn(__dsub_rn(hi[i], oi), inv);
         if (ta > tb) {
-            double s = ta;
+            const double s = ta;
             ta = tb;
             tb = s;
         }
         if (ta > t0) t0 = ta;
         if (tb < t1) t1 = tb;
-        if (t1 < t0) return 0;
+        if (t1 < t0) return false;
     }
+    *pt0 = t0;
+    *pt1 = t1;
+    return true;
+}
+
+// clip to [0, inf) (geom.py:203-209) + lattice range.
+__device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const double d[3], int64_t* k0) {
+    double t0, t1;
+    if (!slab_interval(a.o, d, a.blo, a.bhi, &t0, &t1)) return 0;
     if (t0 < 0.0) t0 = 0.0;
     if (t1 < t0) return 0;
-    int64_t ka = (int64_t)ceil(__ddiv_rn(t0, a.dt));
-    int64_t kb = (int64_t)ceil(__ddiv_rn(t1, a.dt));
+    const int64_t ka = (int64_t)ceil(__ddiv_rn(t0, a.dt));
+    const int64_t kb = (int64_t)ceil(__ddiv_rn(t1, a.dt));
     *k0 = ka;
     return kb > ka ? kb - ka : 0;
+}
+
+// Known-answer kernels: the marcher's own device functions applied to caller-supplied rays, so the
+// reference's golden vectors (camera rays, slab intervals) are checked on the GPU code itself.
+__global__ void kat_slab_kernel(const double* __restrict__ o, const double* __restrict__ d,
+                                const double* __restrict__ lo, const double* __restrict__ hi, int n,
+                                double* __restrict__ t01, int* __restrict__ hit) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double t0 = 0.0, t1 = 0.0;
+    const bool h = slab_interval(o + 3 * i, d + 3 * i, lo + 3 * i, hi + 3 * i, &t0, &t1);
+    hit[i] = h ? 1 : 0;
+    t01[2 * i] = h ? t0 : 0.0;
+    t01[2 * i + 1] = h ? t1 : 0.0;
+}
+
+__global__ void kat_primary_kernel(const MarchArgs a, double* __restrict__ out) {
+    const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y;
+    if (px >= a.W) return;
+    double d[3];
+    primary_dir(a, px, py, d);
+    double* o = out + 3 * ((long long)py * a.W + px);
+    o[0] = d[0];
+    o[1] = d[1];
+    o[2] = d[2];
+}
+
+cudaError_t launch_kat_slab(const double* o, const double* d, const double* lo, const double* hi, int n, double* t01,
+                            int* hit) {
+    kat_slab_kernel<<<(n + 127) / 128, 128>>>(o, d, lo, hi, n, t01, hit);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kat_primary(const MarchArgs& a, double* out) {
+    kat_primary_kernel<<<dim3((a.W + 127) / 128, a.H), 128>>>(a, out);
+    return cudaGetLastError();
 }
 
 #ifndef DPRT_REFILL_BELOW
