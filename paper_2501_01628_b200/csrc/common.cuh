@@ -26,7 +26,10 @@ constexpr int kMacro = 1 << kMacroShift;  // macrocell edge in cells (empty-spac
 constexpr int kTileX = 16;         // marcher CTA screen tile: 16 x 16 pixels, warps are 8 x 4 pixel tiles
 constexpr int kTileY = 16;
 constexpr int kMaxTf = 1024;       // transfer-function entries held in shared memory
-constexpr int kSkipCap = 15;       // Chebyshev skip distances are capped at this many macrocells
+#ifndef DPRT_SKIP_CAP
+#define DPRT_SKIP_CAP 15
+#endif
+constexpr int kSkipCap = DPRT_SKIP_CAP;  // Chebyshev skip distances are capped at this many macrocells
 
 struct DeviceBrick {
     int device;

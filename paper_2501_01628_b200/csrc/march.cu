@@ -486,10 +486,12 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
             int dmin = 0;
             if (a.skip && B1 >= B0) {
                 const int nb = B1 - B0 + 1, nc = Cc1 - Cc0 + 1;
-                if (nb * nc <= 32) {
+                // lanes enumerate the nb x nc macrocells on a power-of-two row pitch (no integer division)
+                const int lg = nb > 1 ? 32 - __clz(nb - 1) : 0;
+                if ((nc << lg) <= 32) {
                     int dl = 255;
-                    if (lane < nb * nc) {
-                        const int mb = B0 + lane % nb, mc = Cc0 + lane / nb;
+                    if ((lane & ((1 << lg) - 1)) < nb && (lane >> lg) < nc) {
+                        const int mb = B0 + (lane & ((1 << lg) - 1)), mc = Cc0 + (lane >> lg);
                         const int mx = ka == 0 ? K : (kb == 0 ? mb : mc);
                         const int my = ka == 1 ? K : (kb == 1 ? mb : mc);
                         const int mz = ka == 2 ? K : (kb == 2 ? mb : mc);
