@@ -345,6 +345,9 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 #define DPRT_BEAM_W 4
 #endif
 constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
+#ifndef DPRT_BEAM_PROBE
+#define DPRT_BEAM_PROBE 0
+#endif
 #ifndef DPRT_RECOMPUTE_W
 #define DPRT_RECOMPUTE_W 0
 #endif
@@ -450,26 +453,63 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
         const bool ok = nn == 0 || ((sa > 0.f) == pos && sa != 0.f && fabsf(sb) <= fabsf(sa) && fabsf(sc) <= fabsf(sa));
         const bool dominant = __all_sync(FULL, ok);  // multi-slab jumps need |st_b|, |st_c| <= |st_a| on all rays
         const float isa = sa != 0.f ? 1.f / sa : 0.f;
+#if DPRT_BEAM_PROBE
+        float ist[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ist[i] = st[i] != 0.f ? 1.f / st[i] : 0.f;
+#endif
         int j = 0;
         float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
         bool live = nn > 0;
         while (true) {
             const unsigned livem = __ballot_sync(FULL, live);
             if (!livem) break;
-            // current slab: the nearest (in the march direction) slab holding a live lane's next sample
+#if DPRT_BEAM_PROBE
+            // per-lane probe: a lane whose next sample sits in an empty macrocell jumps over the empty
+            // Chebyshev cube around it on its own (exact); only lanes in non-empty macrocells go on to
+            // the slab step, which then needs no beam-wide emptiness test
+            bool samp = live;
+            if (live && a.skip) {
+                const float fj = (float)j;
+                const int mx = fl2cell(fmaf(fj, st[0], p0[0]), chx) >> kMacroShift;
+                const int my = fl2cell(fmaf(fj, st[1], p0[1]), chy) >> kMacroShift;
+                const int mz = fl2cell(fmaf(fj, st[2], p0[2]), chz) >> kMacroShift;
+                const int dist = (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx);
+                if (dist > 0) {
+                    float je = 3.0e38f;
+                    if (st[0] != 0.f)
+                        je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0]);
+                    if (st[1] != 0.f)
+                        je = fminf(je, ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << kMacroShift) - p0[1]) * ist[1]);
+                    if (st[2] != 0.f)
+                        je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2]);
+                    j = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;
+                    if (j >= nn) live = false;
+                    samp = false;
+#if DPRT_COUNTERS
+                    ++c_skip;
+#endif
+                }
+            }
+            if (!__any_sync(FULL, samp)) continue;
+#else
+            const bool samp = live;
+#endif
+            // current slab: the nearest (in the march direction) slab holding a sampling lane's next sample
             int ksl = 0;
-            if (live) ksl = fl2cell(fmaf((float)j, sa, pa), cha) >> kMacroShift;
-            const int key = live ? (pos ? ksl : -ksl) : 0x7fffffff;
+            if (samp) ksl = fl2cell(fmaf((float)j, sa, pa), cha) >> kMacroShift;
+            const int key = samp ? (pos ? ksl : -ksl) : 0x7fffffff;
             const int kmin = __reduce_min_sync(FULL, key);
             const int K = pos ? kmin : -kmin;
             // this lane's samples in slab K: j .. jend-1 (first sample past the slab's far face)
             int jend = j;
-            if (live) {
+            if (samp) {
                 const float face = (float)((pos ? K + 1 : K) << kMacroShift);
                 const float je = (face - pa) * isa;
                 jend = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;  // >= 1 sample: progress
                 if (ksl != K) jend = j;  // this ray is not in slab K yet
             }
+#if !DPRT_BEAM_PROBE
             // bound the beam's cells on the other two axes over all samples in the slab
             int b0 = 0x7fffffff, b1 = -1, c0 = 0x7fffffff, c1 = -1;
             if (jend > j) {
@@ -515,6 +555,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                 }
                 continue;
             }
+#endif
             // Shade this lane's samples in the slab, kBeamUnroll at a time: all their corner loads are
             // issued before the first is shaded, so each lane keeps several loads in flight.
             while (j < jend) {
