@@ -346,7 +346,7 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 #endif
 constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
 #ifndef DPRT_BEAM_PROBE
-#define DPRT_BEAM_PROBE 0
+#define DPRT_BEAM_PROBE 1
 #endif
 #ifndef DPRT_RECOMPUTE_W
 #define DPRT_RECOMPUTE_W 0
