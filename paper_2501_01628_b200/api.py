@@ -41,7 +41,6 @@ NOT_ROOT = _NotRoot()
 
 OBJECT_KINDS = ("world", "surface", "group", "instance", "camera", "renderer", "frame",
                 "spatialField", "volume", "transferFunction1D")
-_TRIANGLE_KINDS = ("surface", "group", "instance")
 
 _PARAMS: Dict[str, Dict[str, object]] = {
     "world": {"volumes": [], "surfaces": [], "instances": [], "lights": []},

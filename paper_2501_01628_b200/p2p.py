@@ -13,7 +13,7 @@ partial that is still being read.  This replaces both the reference's ring cycli
 
 from __future__ import annotations
 
-from typing import List, Optional, Sequence
+from typing import Optional, Sequence
 
 import torch
 
