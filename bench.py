@@ -310,16 +310,17 @@ def run_ours(args):
     h2d = pinned_tf.numel() * 4 + ctypes.sizeof(camera_struct(cam))
     d2h = W * H * 3 if rank == 0 else 0
 
-    host_frames = [host_frame, torch.empty((H, W, 3), dtype=torch.uint8).pin_memory()]
+    depth = 2  # frames in flight: the host waits for frame k-2's bytes while k-1 and k are queued
+    host_frames = [host_frame] + [torch.empty((H, W, 3), dtype=torch.uint8).pin_memory() for _ in range(depth)]
     inflight = []
 
     def e2e_step(k):
         # per step: TF H2D from pinned memory, collective render (digest verified), RGB8 frame D2H into
-        # pinned memory on a side stream; the host waits for frame k-1's bytes while frame k renders
+        # pinned memory on a side stream; the host waits for frame k-depth's bytes while later frames render
         renderer.dtf.update(tf, staging=pinned_tf)
-        hf = renderer.render_to_host(cam, W, H, host_frames[k % 2] if rank == 0 else None, opts, verify=True)
+        hf = renderer.render_to_host(cam, W, H, host_frames[k % (depth + 1)] if rank == 0 else None, opts, verify=True)
         inflight.append(hf)
-        if len(inflight) > 1:
+        if len(inflight) > depth:
             inflight.pop(0).wait()
 
     def drain():

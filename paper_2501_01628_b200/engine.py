@@ -28,6 +28,7 @@ from .transport import RankEndpoint
 from .volume import Decomposition, TransferFunction1D, visibility_order
 
 COMPOSITE_MODES = ("auto", "direct_send", "binary_swap", "p2p")
+FUSED_SLOTS = 3  # device RGB8 frames the fused single-rank path rotates through (read-back pipeline depth)
 
 # Distinct colours for rank-ownership visualisation, one per rank modulo 8 (engine.py:41-44).
 RANK_PALETTE = np.array([
@@ -168,7 +169,7 @@ class VolumeRenderer:
         self._fused_frames = None
         self._rank_dtf = None
         self._rank_tf_src = None
-        self._fused_events = [None, None]
+        self._fused_events = [None] * FUSED_SLOTS
         self._fused_next = 0
         self._fused_slot = 0
 
@@ -210,13 +211,13 @@ class VolumeRenderer:
         t0 = time.perf_counter()
         if self.ep.R == 1 and not options.keep_float and os.environ.get("DPRT_FUSED_SINGLE", "1") != "0":
             # one rank: the composite is just over-background + tone map -> fused into the march
-            # two device frames alternate so the read-back of frame k overlaps the march of frame k+1
+            # a ring of device frames so the read-backs of frames k-1, k-2 overlap the march of frame k
             if self._fused_frames is None or tuple(self._fused_frames[0].shape) != (height, width, 3):
                 self._fused_frames = [torch.empty((height, width, 3), dtype=torch.uint8, device=self.device)
-                                      for _ in range(2)]
-                self._fused_events = [None, None]
+                                      for _ in range(FUSED_SLOTS)]
+                self._fused_events = [None] * FUSED_SLOTS
             slot = self._fused_next
-            self._fused_next ^= 1
+            self._fused_next = (slot + 1) % FUSED_SLOTS
             if self._fused_events[slot] is not None:
                 torch.cuda.current_stream(self.device).wait_event(self._fused_events[slot])
                 self._fused_events[slot] = None
