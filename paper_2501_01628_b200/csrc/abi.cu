@@ -102,21 +102,25 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     }
     if (desc->ghost < 0) return fail(DPRT_E_USAGE, "ghost must be >= 0");
     {
-        long long nv = 1;
+        long long nv = 1, nq = 1;
         for (int a = 0; a < 3; ++a) {
             long long lo = desc->lo[a] - desc->ghost < 0 ? 0 : desc->lo[a] - desc->ghost;
             long long hi = desc->hi[a] + desc->ghost > desc->dims[a] - 1 ? desc->dims[a] - 1 : desc->hi[a] + desc->ghost;
             nv *= hi - lo + 1;
+            nq *= hi - lo + 3;
         }
-        // the marcher addresses voxels with 32-bit offsets: split larger fields into more bricks
-        if (nv >= (1LL << 31)) return fail(DPRT_E_USAGE, "brick stores %lld voxels; the limit is 2^31 - 1 per brick", nv);
+        // the marcher addresses voxels and (apron) quads with signed 32-bit offsets: split larger fields
+        // into more bricks
+        if (nq >= (1LL << 31))
+            return fail(DPRT_E_USAGE, "brick stores %lld voxels (%lld with the quad apron); the limit is 2^31 - 1",
+                        nv, nq);
     }
     int rc = bind(device);
     if (rc) return rc;
     DprtBrick* b = new DprtBrick();
     b->device = device;
     b->desc = *desc;
-    long long nvox = 1, nmc = 1;
+    long long nvox = 1, nmc = 1, nq = 1;
     for (int a = 0; a < 3; ++a) {
         long long lo = desc->lo[a] - desc->ghost;
         long long hi = desc->hi[a] + desc->ghost;
@@ -125,7 +129,9 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
         b->s_lo[a] = lo;
         b->sd[a] = hi - lo + 1;
         b->mcd[a] = (b->sd[a] - 1 + dprt::kMacro - 1) / dprt::kMacro;
+        b->qd[a] = b->sd[a] + 2;
         nvox *= b->sd[a];
+        nq *= b->qd[a];
         nmc *= b->mcd[a];
     }
     b->vox = nullptr;
@@ -138,10 +144,7 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     b->counters = nullptr;
     b->quad = nullptr;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
-#if DPRT_QUAD
-    // quad layout: 16 B per voxel; octet layout (DPRT_QUAD == 2): 32 B per voxel
-    if (e == cudaSuccess) e = cudaMalloc(&b->quad, (size_t)nvox * sizeof(float4) * (DPRT_QUAD == 2 ? 2 : 1));
-#endif
+    if (e == cudaSuccess) e = cudaMalloc(&b->quad, (size_t)nq * sizeof(float4));  // 16 B per apron-grid voxel
     if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc);
@@ -324,7 +327,9 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.sy = (long long)b->sd[0];
     a.sz = (long long)b->sd[0] * b->sd[1];
     a.vox = b->vox;
-    a.quad = b->quad;
+    a.qsy = (int)b->qd[0];
+    a.qsz = (int)(b->qd[0] * b->qd[1]);
+    a.qorg = b->quad + a.qsz + a.qsy + 1;
     a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
@@ -333,6 +338,8 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.n_tf = p->n_tf;
     a.vmin = (float)p->vmin;
     a.tf_scale = (float)((double)(p->n_tf - 1) / (p->vmax - p->vmin));
+    a.tf_ns = (float)(1.0 / (p->vmax - p->vmin));
+    a.tf_no = (float)(-p->vmin / (p->vmax - p->vmin));
     a.ert = (float)p->ert;
     a.out = reinterpret_cast<float4*>(partial_rgba);
     a.rgb8 = rgb8;

@@ -6,9 +6,6 @@
 
 #include "dprt_cuda.h"
 
-#ifndef DPRT_QUAD
-#define DPRT_QUAD 1
-#endif
 #ifndef DPRT_BEAM_DEFAULT
 #define DPRT_BEAM_DEFAULT 1
 #endif
@@ -37,7 +34,8 @@ struct DeviceBrick {
     int64_t s_lo[3];   // first stored voxel (global index)
     int64_t sd[3];     // stored voxel dims
     float* vox;        // sd[0]*sd[1]*sd[2] f32, x fastest
-    float4* quad;      // per voxel {v(i,j,k), v(i+1,j,k), v(i,j+1,k), v(i+1,j+1,k)} (edge-clamped), DPRT_QUAD
+    float4* quad;      // coefficient quads over the apron grid qd (field.cu quad_kernel)
+    int64_t qd[3];     // quad grid dims = sd + 2 (one apron voxel on every side)
     int64_t mcd[3];    // macrocell grid dims
     float2* macro;     // per macrocell (min, max) over its dilated voxel range
     uint8_t* skipd;    // per macrocell Chebyshev distance to the nearest non-empty macrocell (TF-dependent)
@@ -60,11 +58,12 @@ struct MarchArgs {
     // f32 march state
     float inv_spacing[3];
     double stored_lo_d[3];  // s_lo (local coordinate shift)
-    int clo[3], chi[3];    // local clamp range of the cell index
+    int clo[3], chi[3];    // local clamp range of the cell index (macrocell lookups)
     int sd[3];
     long long sy, sz;      // voxel strides
     const float* __restrict__ vox;
-    const float4* __restrict__ quad;
+    const float4* __restrict__ qorg;  // coefficient quad of stored voxel (0,0,0); apron at index -1 and sd
+    int qsy, qsz;                     // quad strides (apron grid)
     const uint8_t* __restrict__ skipd;
     int mcd[3];
     int skip;
@@ -73,6 +72,7 @@ struct MarchArgs {
     const float4* __restrict__ tf;
     int n_tf;
     float vmin, tf_scale, ert;
+    float tf_ns, tf_no;  // normalised TF coordinate = sat(v * tf_ns + tf_no), tf_ns = 1 / (vmax - vmin)
     // output
     float4* __restrict__ out;
     uint8_t* rgb8;  // non-null: write the tone-mapped frame over bg[] instead of the RGBA partial (R == 1)

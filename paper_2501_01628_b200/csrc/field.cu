@@ -77,50 +77,34 @@ __global__ void macrocell_kernel(const float* __restrict__ vox, long long sd0, l
     macro[((long long)mz * mc1 + my) * mc0 + mx] = make_float2(lo, hi);
 }
 
-// Quad layout (DPRT_QUAD): each voxel slot carries the 4 corners of the z-face of the cell it anchors,
-// so a trilinear sample is two 16-byte loads instead of eight 4-byte gathers (4x the voxel bytes).
+// Coefficient quads: the slot of voxel (x, y, z) holds the bilinear coefficients of the
+// z-face of the cell it anchors, {a, b - a, c - a, d - c - b + a} for the corners a = v(x, y), b = v(x+1, y),
+// c = v(x, y+1), d = v(x+1, y+1), so a face value is a + B fx + C fy + D fx fy (3 FFMA) and a trilinear
+// sample is two 16-byte loads.  The grid carries one apron voxel on every side (index -1 and sd along each
+// axis, coordinates clamped, hence zero slopes there): sample positions that float rounding puts a hair
+// outside the stored box need no clamp in the marcher and reproduce the oracle's clamped cell exactly.
 __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
                             float4* __restrict__ quad) {
-    const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long y = blockIdx.y, z = blockIdx.z;
-    if (x >= sd0) return;
-    const long long x1 = x + 1 < sd0 ? x + 1 : x;
-    const long long y1 = y + 1 < sd1 ? y + 1 : y;
-    const float* r0 = vox + (z * sd1 + y) * sd0;
+    const long long qd0 = sd0 + 2, qd1 = sd1 + 2;
+    const long long qx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (qx >= qd0) return;
+    const long long qy = blockIdx.y, qz = blockIdx.z;
+    auto cl = [](long long v, long long n) { return v < 0 ? 0 : (v >= n ? n - 1 : v); };
+    const long long x0 = cl(qx - 1, sd0), x1 = cl(qx, sd0);
+    const long long y0 = cl(qy - 1, sd1), y1 = cl(qy, sd1);
+    const long long z = cl(qz - 1, sd2);
+    const float* r0 = vox + (z * sd1 + y0) * sd0;
     const float* r1 = vox + (z * sd1 + y1) * sd0;
-    quad[(z * sd1 + y) * sd0 + x] = make_float4(r0[x], r0[x1], r1[x], r1[x1]);
-}
-
-// Octet layout (DPRT_QUAD == 2): the 8 corners of the cell a voxel anchors, 32 bytes, one 256-bit load.
-__global__ void octet_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
-                             float4* __restrict__ oct) {
-    const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long y = blockIdx.y, z = blockIdx.z;
-    if (x >= sd0) return;
-    const long long x1 = x + 1 < sd0 ? x + 1 : x;
-    const long long y1 = y + 1 < sd1 ? y + 1 : y;
-    const long long z1 = z + 1 < sd2 ? z + 1 : z;
-    const float* r00 = vox + (z * sd1 + y) * sd0;
-    const float* r10 = vox + (z * sd1 + y1) * sd0;
-    const float* r01 = vox + (z1 * sd1 + y) * sd0;
-    const float* r11 = vox + (z1 * sd1 + y1) * sd0;
-    const long long i = (z * sd1 + y) * sd0 + x;
-    oct[2 * i] = make_float4(r00[x], r00[x1], r10[x], r10[x1]);
-    oct[2 * i + 1] = make_float4(r01[x], r01[x1], r11[x], r11[x1]);
+    const float a = r0[x0], b = r0[x1], c = r1[x0], d = r1[x1];
+    quad[(qz * qd1 + qy) * qd0 + qx] = make_float4(a, b - a, c - a, (d - c) - (b - a));
 }
 
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream) {
-#if DPRT_QUAD
     {
         dim3 qb(256);
-        dim3 qg((unsigned)((b.sd[0] + 255) / 256), (unsigned)b.sd[1], (unsigned)b.sd[2]);
-#if DPRT_QUAD == 2
-        octet_kernel<<<qg, qb, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], b.quad);
-#else
+        dim3 qg((unsigned)((b.qd[0] + 255) / 256), (unsigned)b.qd[1], (unsigned)b.qd[2]);
         quad_kernel<<<qg, qb, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], b.quad);
-#endif
     }
-#endif
     dim3 block(64);
     dim3 grid((unsigned)((b.mcd[0] + 63) / 64), (unsigned)b.mcd[1], (unsigned)b.mcd[2]);
     macrocell_kernel<<<grid, block, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], (int)b.mcd[0], (int)b.mcd[1],

@@ -179,6 +179,37 @@ __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchA
     a.rays[2 * slot + 1] = make_float4(st[0], st[1], st[2], __int_as_float((int)n));
 }
 
+// One trilinear sample from the two coefficient quads of its cell (field.cu quad_kernel): each z-face is
+// a + B fx + C fy + D fx fy, then a lerp along z (DESIGN.md §2.5 / §4.1).
+__device__ __forceinline__ float trilerp(const float4 q0, const float4 q1, float fx, float fy, float fxy, float fz) {
+    const float e0 = fmaf(q0.w, fxy, fmaf(q0.z, fy, fmaf(q0.y, fx, q0.x)));
+    const float e1 = fmaf(q1.w, fxy, fmaf(q1.z, fy, fmaf(q1.y, fx, q1.x)));
+    return fmaf(fz, e1 - e0, e0);
+}
+
+// DPRT_BOUNDS_CHECK builds trap on a quad index (relative to qorg, both loads) outside the apron grid.
+__device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, int qi) {
+#if DPRT_BOUNDS_CHECK
+    const long long org = (long long)a.qsz + a.qsy + 1, total = (long long)a.qsz * (a.sd[2] + 2);
+    if (qi + org < 0 || qi + org + a.qsz >= total) __trap();
+#endif
+}
+
+// TF lookup and front-to-back premultiplied blend (§2.7) of one sample value.  s_tf holds
+// (entry, next - entry) pairs and the last entry's difference is zero, so x = n - 1 needs no index clamp.
+__device__ __forceinline__ void tf_blend(const float4* s_tf, float v, float tns, float tno, float top, float& C0,
+                                         float& C1, float& C2, float& A) {
+    const float x = __saturatef(fmaf(v, tns, tno)) * top;
+    const int ti = (int)x;
+    const float tfr = x - (float)ti;
+    const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+    const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+    C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+    C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+    C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+    A += w;
+}
+
 // Pass 2: persistent warps march the queued rays.
 #ifndef DPRT_MARCH_MINBLOCKS
 #define DPRT_MARCH_MINBLOCKS 4
@@ -199,13 +230,11 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
     const int lane = tid & 31;
     const int total = a.counters[0];  // written by ray_setup_kernel, which completed before this launch
     const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
-    const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
-    const float* __restrict__ vox = a.vox;
-    const float4* __restrict__ quad = a.quad;
+    const float4* __restrict__ qorg = a.qorg;
+    const int qsy = a.qsy, qsz = a.qsz;
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1], skip = a.skip;
-    const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
-    const int tmax = a.n_tf - 2;
+    const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
 
     bool have = false, exhausted = false;
     int pix = 0, nn = 0, j = 0;
@@ -287,44 +316,12 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                 continue;
             }
             // trilinear + TF (§2.6) + front-to-back blend (§2.7) of one sample
-            auto shade = [&](float4 qa, float4 qb, float wx, float wy, float wz) {
-                const float c00 = fmaf(wx, qa.y - qa.x, qa.x);
-                const float c10 = fmaf(wx, qa.w - qa.z, qa.z);
-                const float c01 = fmaf(wx, qb.y - qb.x, qb.x);
-                const float c11 = fmaf(wx, qb.w - qb.z, qb.z);
-                const float c0 = fmaf(wy, c10 - c00, c00);
-                const float c1 = fmaf(wy, c11 - c01, c01);
-                const float v = fmaf(wz, c1 - c0, c0);
-                const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
-                const int ti = min((int)x, tmax);
-                const float tfr = x - (float)ti;
-                const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
-                const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
-#if DPRT_COUNTERS
-                ++c_shade;
-                c_contrib += w > 0.f;
-#endif
-                C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
-                C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
-                C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-                A += w;
-            };
-#if DPRT_QUAD == 2
-            const float4* q = quad + 2u * ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-            const float4 qa = __ldg(q), qb = __ldg(q + 1);
-#elif DPRT_QUAD
-            // quad layout: one 16-byte load brings the 4 corners of a z-face of the cell
-#if DPRT_BOUNDS_CHECK
-            if ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix + sz >= (unsigned)(a.sd[0] * a.sd[1] * a.sd[2])) __trap();
-#endif
-            const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-            const float4 qa = __ldg(q), qb = __ldg(q + sz);
-#else
-            const float* p = vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-            const float4 qa = make_float4(__ldg(p), __ldg(p + 1), __ldg(p + sy), __ldg(p + sy + 1));
-            const float4 qb = make_float4(__ldg(p + sz), __ldg(p + sz + 1), __ldg(p + sz + sy), __ldg(p + sz + sy + 1));
-#endif
-            shade(qa, qb, __saturatef(ux - (float)ix), __saturatef(uy - (float)iy), __saturatef(uz - (float)iz));
+            const int qi = iz * qsz + iy * qsy + ix;
+            quad_bounds_check(a, qi);
+            const float4* q = qorg + qi;
+            const float fx = __saturatef(ux - (float)ix), fy = __saturatef(uy - (float)iy);
+            const float v = trilerp(__ldg(q), __ldg(q + qsz), fx, fy, fx * fy, __saturatef(uz - (float)iz));
+            tf_blend(s_tf, v, tns, tno, top, C0, C1, C2, A);
             ++j;
             if (A >= ert) j = nn;  // early ray termination: the next step finishes the ray
         }
@@ -348,31 +345,6 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #ifndef DPRT_BEAM_PROBE
 #define DPRT_BEAM_PROBE 1
 #endif
-#ifndef DPRT_RECOMPUTE_W
-#define DPRT_RECOMPUTE_W 0
-#endif
-#ifndef DPRT_LDQ
-#define DPRT_LDQ 0
-#endif
-// corner-quad load with an optional cache hint (build-time switch for experiments)
-__device__ __forceinline__ float4 ldq(const float4* q) {
-#if DPRT_LDQ == 1
-    float4 v;
-    asm volatile("ld.global.nc.L2::128B.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q));
-    return v;
-#elif DPRT_LDQ == 2
-    float4 v;
-    asm volatile("ld.global.nc.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q));
-    return v;
-#elif DPRT_LDQ == 3
-    float4 v;
-    asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q));
-    return v;
-#else
-    return __ldg(q);
-#endif
-}
-
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
 #ifndef DPRT_BEAM_MINBLOCKS
@@ -394,12 +366,12 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
     const int tiles_x = (rw + kBeamW - 1) / kBeamW, tiles_y = (rh + kBeamH - 1) / kBeamH;
     const int ntiles = tiles_x * tiles_y;
     const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
-    const unsigned sy = (unsigned)a.sy, sz = (unsigned)a.sz;
-    const float4* __restrict__ quad = a.quad;
+    const float4* __restrict__ qorg = a.qorg;
+    const float4* __restrict__ qorg1 = a.qorg + a.qsz;  // the cell's far z-face
+    const int qsy = a.qsy, qsz = a.qsz;
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1];
-    const float vmin = a.vmin, tscale = a.tf_scale, top = (float)(a.n_tf - 1), ert = a.ert;
-    const int tmax = a.n_tf - 2;
+    const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
@@ -562,75 +534,38 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
                 const int cnt = min(kBeamUnroll, jend - j);
                 float4 qa[kBeamUnroll], qb[kBeamUnroll];
                 float wx[kBeamUnroll], wy[kBeamUnroll], wz[kBeamUnroll];
+                const float fj = (float)j;  // exact: j < 2^24
 #pragma unroll
                 for (int u = 0; u < kBeamUnroll; ++u) {
                     if (u < cnt) {
-                        const float fs = (float)(j + u);
+                        const float fs = fj + (float)u;
                         const float ux = fmaf(fs, st[0], p0[0]);
                         const float uy = fmaf(fs, st[1], p0[1]);
                         const float uz = fmaf(fs, st[2], p0[2]);
-                        const int ix = fl2cell(ux, chx), iy = fl2cell(uy, chy), iz = fl2cell(uz, chz);
-#if DPRT_QUAD == 2
-                        const float4* q = quad + 2u * ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-                        asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-                                     : "=f"(qa[u].x), "=f"(qa[u].y), "=f"(qa[u].z), "=f"(qa[u].w), "=f"(qb[u].x),
-                                       "=f"(qb[u].y), "=f"(qb[u].z), "=f"(qb[u].w)
-                                     : "l"(q));
-#elif DPRT_QUAD
-#if DPRT_BOUNDS_CHECK
-                        if ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix + sz >= (unsigned)(a.sd[0] * a.sd[1] * a.sd[2])) __trap();
-#endif
-                        const float4* q = quad + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-                        qa[u] = ldq(q);
-                        qb[u] = ldq(q + sz);
-#else
-                        const float* pv = a.vox + ((unsigned)iz * sz + (unsigned)iy * sy + (unsigned)ix);
-                        qa[u] = make_float4(__ldg(pv), __ldg(pv + 1), __ldg(pv + sy), __ldg(pv + sy + 1));
-                        qb[u] = make_float4(__ldg(pv + sz), __ldg(pv + sz + 1), __ldg(pv + sz + sy), __ldg(pv + sz + sy + 1));
-#endif
-#if !DPRT_RECOMPUTE_W
+                        // no clamp: the quad grid's apron covers the cells rounding can reach (field.cu)
+                        const int ix = __float2int_rd(ux), iy = __float2int_rd(uy), iz = __float2int_rd(uz);
+                        const int qi = iz * qsz + iy * qsy + ix;
+                        quad_bounds_check(a, qi);
+                        qa[u] = __ldg(qorg + qi);
+                        qb[u] = __ldg(qorg1 + qi);
                         wx[u] = __saturatef(ux - (float)ix);
                         wy[u] = __saturatef(uy - (float)iy);
                         wz[u] = __saturatef(uz - (float)iz);
-#endif
                     }
                 }
                 bool stop = false;
 #pragma unroll
                 for (int u = 0; u < kBeamUnroll; ++u) {
                     if (u < cnt && !stop) {
-#if DPRT_RECOMPUTE_W
-                        // weights recomputed after the loads: fewer live registers per batch, more warps
-                        {
-                            const float fs = (float)(j + u);
-                            const float ux = fmaf(fs, st[0], p0[0]);
-                            const float uy = fmaf(fs, st[1], p0[1]);
-                            const float uz = fmaf(fs, st[2], p0[2]);
-                            wx[u] = __saturatef(ux - (float)fl2cell(ux, chx));
-                            wy[u] = __saturatef(uy - (float)fl2cell(uy, chy));
-                            wz[u] = __saturatef(uz - (float)fl2cell(uz, chz));
-                        }
+                        const float v = trilerp(qa[u], qb[u], wx[u], wy[u], wx[u] * wy[u], wz[u]);
+#if DPRT_COUNTERS
+                        const float a0 = A;
 #endif
-                        const float e00 = fmaf(wx[u], qa[u].y - qa[u].x, qa[u].x);
-                        const float e10 = fmaf(wx[u], qa[u].w - qa[u].z, qa[u].z);
-                        const float e01 = fmaf(wx[u], qb[u].y - qb[u].x, qb[u].x);
-                        const float e11 = fmaf(wx[u], qb[u].w - qb[u].z, qb[u].z);
-                        const float g0 = fmaf(wy[u], e10 - e00, e00);
-                        const float g1 = fmaf(wy[u], e11 - e01, e01);
-                        const float v = fmaf(wz[u], g1 - g0, g0);
-                        const float x = fminf(fmaxf((v - vmin) * tscale, 0.f), top);
-                        const int ti = min((int)x, tmax);
-                        const float tfr = x - (float)ti;
-                        const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
-                        const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
+                        tf_blend(s_tf, v, tns, tno, top, C0, C1, C2, A);
 #if DPRT_COUNTERS
                         ++c_shade;
-                        c_contrib += w > 0.f;
+                        c_contrib += A > a0;
 #endif
-                        C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
-                        C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
-                        C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-                        A += w;
                         if (A >= ert) stop = true;  // early ray termination
                     }
                 }
