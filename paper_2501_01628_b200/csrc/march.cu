@@ -195,14 +195,15 @@ __device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, int qi) {
 #endif
 }
 
-// TF lookup and front-to-back premultiplied blend (§2.7) of one sample value.  s_tf holds
-// (entry, next - entry) pairs and the last entry's difference is zero, so x = n - 1 needs no index clamp.
-__device__ __forceinline__ void tf_blend(const float4* s_tf, float v, float tns, float tno, float top, float& C0,
-                                         float& C1, float& C2, float& A) {
+// TF lookup and front-to-back premultiplied blend (§2.7) of one sample value.  Shared memory
+// holds the entries (s_tf) and, in a second array, next - entry (s_dtf; 16-byte strides keep neighbouring
+// lanes' LDS.128 on distinct banks); the last entry's difference is zero, so x = n - 1 needs no clamp.
+__device__ __forceinline__ void tf_blend(const float4* s_tf, const float4* s_dtf, float v, float tns, float tno,
+                                         float top, float& C0, float& C1, float& C2, float& A) {
     const float x = __saturatef(fmaf(v, tns, tno)) * top;
     const int ti = (int)x;
     const float tfr = x - (float)ti;
-    const float4 e0 = s_tf[2 * ti], de = s_tf[2 * ti + 1];
+    const float4 e0 = s_tf[ti], de = s_dtf[ti];
     const float w = (1.f - A) * fmaf(tfr, de.w, e0.w);
     C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
     C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
@@ -215,15 +216,15 @@ __device__ __forceinline__ void tf_blend(const float4* s_tf, float v, float tns,
 #define DPRT_MARCH_MINBLOCKS 4
 #endif
 __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_kernel(const MarchArgs a) {
-    // TF as (entry, next - entry) pairs: the lerp e0 + (e1 - e0) * f becomes one FMA per channel with the
-    // identical rounding (the difference is formed once here instead of per sample).
-    extern __shared__ float4 s_tf[];  // 2 * n_tf entries (dynamic)
+    // TF as entries + (next - entry) differences: the lerp e0 + (e1 - e0) * f becomes one FMA per channel
+    // (the difference is formed once here instead of per sample).
+    extern __shared__ float4 s_tf[];  // n_tf entries, then n_tf differences (dynamic)
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_tf; i += blockDim.x) {
         const float4 e0 = a.tf[i];
         const float4 e1 = i + 1 < a.n_tf ? a.tf[i + 1] : e0;
-        s_tf[2 * i] = e0;
-        s_tf[2 * i + 1] = make_float4(e1.x - e0.x, e1.y - e0.y, e1.z - e0.z, e1.w - e0.w);
+        s_tf[i] = e0;
+        s_tf[a.n_tf + i] = make_float4(e1.x - e0.x, e1.y - e0.y, e1.z - e0.z, e1.w - e0.w);
     }
     __syncthreads();
 
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             const float4* q = qorg + qi;
             const float fx = __saturatef(ux - (float)ix), fy = __saturatef(uy - (float)iy);
             const float v = trilerp(__ldg(q), __ldg(q + qsz), fx, fy, fx * fy, __saturatef(uz - (float)iz));
-            tf_blend(s_tf, v, tns, tno, top, C0, C1, C2, A);
+            tf_blend(s_tf, s_tf + a.n_tf, v, tns, tno, top, C0, C1, C2, A);
             ++j;
             if (A >= ert) j = nn;  // early ray termination: the next step finishes the ray
         }
@@ -356,8 +357,8 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
     for (int i = tid; i < a.n_tf; i += blockDim.x) {
         const float4 e0 = a.tf[i];
         const float4 e1 = i + 1 < a.n_tf ? a.tf[i + 1] : e0;
-        s_tf[2 * i] = e0;
-        s_tf[2 * i + 1] = make_float4(e1.x - e0.x, e1.y - e0.y, e1.z - e0.z, e1.w - e0.w);
+        s_tf[i] = e0;
+        s_tf[a.n_tf + i] = make_float4(e1.x - e0.x, e1.y - e0.y, e1.z - e0.z, e1.w - e0.w);
     }
     __syncthreads();
     const unsigned FULL = 0xffffffffu;
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_be
 #if DPRT_COUNTERS
                         const float a0 = A;
 #endif
-                        tf_blend(s_tf, v, tns, tno, top, C0, C1, C2, A);
+                        tf_blend(s_tf, s_tf + a.n_tf, v, tns, tno, top, C0, C1, C2, A);
 #if DPRT_COUNTERS
                         ++c_shade;
                         c_contrib += A > a0;
