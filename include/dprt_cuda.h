@@ -63,7 +63,9 @@ typedef struct DprtCamera {
 } DprtCamera;
 
 /* Synthetic field: kind 0 = blob mixture, `blobs` = host array of n_blobs x {cx, cy, cz, inv_rho2, amp}
- * in unit-cube coordinates (parameters drawn as scene.py:258-262). */
+ * in unit-cube coordinates (parameters drawn as scene.py:258-262).
+ * kind 1 = Marschner-Lobb over [-1, 1]^3, `blobs` = host array {f_M, alpha}, n_blobs = 1 (§2.2b).
+ * Both are evaluated in f64 with explicitly rounded ops, bit-identical to oracle/dvr_oracle.c. */
 typedef struct DprtFieldSpec {
     int32_t kind;
     int32_t n_blobs;

@@ -17,7 +17,9 @@ from .dvr import (  # noqa: F401
     build_oracle,
     camera_array,
     composite,
+    det_cos,
     generate_field,
+    generate_ml,
     kd_leaves,
     kd_order,
     lattice,

@@ -19,7 +19,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_build" / "libdvr_oracle.so"
-_ABI = 4
+_ABI = 5
 
 _lib = None
 
@@ -44,12 +44,11 @@ def load_oracle():
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB_PATH.exists():
-        build_oracle()
+    if (HERE / "dvr_oracle.c").exists():
+        build_oracle()  # rebuilds when the source is newer (before the first dlopen of this path)
     lib = ctypes.CDLL(str(LIB_PATH))
     if lib.dvr_oracle_version() != _ABI:
-        build_oracle(force=True)
-        lib = ctypes.CDLL(str(LIB_PATH))
+        raise RuntimeError(f"{LIB_PATH} has oracle ABI {lib.dvr_oracle_version()}, expected {_ABI}: rebuild it")
     P = ctypes.c_void_p
     lib.dvr_oracle_primary_dirs.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
     lib.dvr_oracle_slab.argtypes = [P, P, P, P, P]
@@ -57,6 +56,9 @@ def load_oracle():
     lib.dvr_oracle_lattice.argtypes = [P, P, P, P, ctypes.c_double, P]
     lib.dvr_oracle_lattice.restype = ctypes.c_int64
     lib.dvr_oracle_generate.argtypes = [P, P, P, ctypes.c_int, P, P, ctypes.c_int]
+    lib.dvr_oracle_generate_ml.argtypes = [P, P, P, P, P, ctypes.c_int]
+    lib.dvr_oracle_det_cos.argtypes = [ctypes.c_double]
+    lib.dvr_oracle_det_cos.restype = ctypes.c_double
     lib.dvr_oracle_render_brick.argtypes = [
         P, P, P, P, P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
         ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
@@ -133,9 +135,15 @@ def lattice(origin, direction, lo, hi, dt: float) -> Tuple[int, int]:
 # ---------------------------------------------------------------------------------------------
 # field + bricks
 
-def generate_field(dims, blobs: np.ndarray, stored_lo=(0, 0, 0), stored_dims=None,
+def generate_field(dims, blobs, stored_lo=(0, 0, 0), stored_dims=None,
                    nthreads: int = 0) -> np.ndarray:
-    """f32 voxels of the blob field over a stored region; array shape (sd_z, sd_y, sd_x)."""
+    """f32 voxels of the blob field over a stored region; array shape (sd_z, sd_y, sd_x).  ``blobs`` may
+    also be a FieldSpec-like object with ``kind`` / ``blobs`` / ``ml`` (Marschner-Lobb fields)."""
+    if hasattr(blobs, "kind"):
+        spec = blobs
+        if spec.kind == "marschnerLobb":
+            return generate_ml(dims, spec.ml, stored_lo, stored_dims, nthreads)
+        blobs = spec.blobs
     N = np.asarray(dims, np.int64)
     s_lo = np.asarray(stored_lo, np.int64)
     sd = np.asarray(stored_dims if stored_dims is not None else dims, np.int64)
@@ -143,6 +151,23 @@ def generate_field(dims, blobs: np.ndarray, stored_lo=(0, 0, 0), stored_dims=Non
     out = np.empty((int(sd[2]), int(sd[1]), int(sd[0])), np.float32)
     load_oracle().dvr_oracle_generate(_ptr(N), _ptr(s_lo), _ptr(sd), len(b), _ptr(b), _ptr(out), nthreads)
     return out
+
+
+def generate_ml(dims, params=(6.0, 0.25), stored_lo=(0, 0, 0), stored_dims=None,
+                nthreads: int = 0) -> np.ndarray:
+    """f32 voxels of the Marschner-Lobb field (params = (f_M, alpha)), DESIGN.md §2.2b."""
+    N = np.asarray(dims, np.int64)
+    s_lo = np.asarray(stored_lo, np.int64)
+    sd = np.asarray(stored_dims if stored_dims is not None else dims, np.int64)
+    prm = np.ascontiguousarray(params, np.float64)
+    out = np.empty((int(sd[2]), int(sd[1]), int(sd[0])), np.float32)
+    load_oracle().dvr_oracle_generate_ml(_ptr(N), _ptr(s_lo), _ptr(sd), _ptr(prm), _ptr(out), nthreads)
+    return out
+
+
+def det_cos(a: float) -> float:
+    """The oracle's reproducible cosine (range reduction + Taylor polynomial) used by generate_ml."""
+    return float(load_oracle().dvr_oracle_det_cos(float(a)))
 
 
 @dataclass

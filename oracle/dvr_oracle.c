@@ -26,7 +26,7 @@
 #include <omp.h>
 #endif
 
-#define ORACLE_ABI_VERSION 4
+#define ORACLE_ABI_VERSION 5
 
 int dvr_oracle_version(void) { return ORACLE_ABI_VERSION; }
 
@@ -138,6 +138,60 @@ void dvr_oracle_generate(const int64_t* N, const int64_t* s_lo, const int64_t* s
             float* row = out + (z * sd[1] + y) * sd[0];
             for (int64_t x = 0; x < sd[0]; ++x)
                 row[x] = field_value(N, s_lo[0] + x, s_lo[1] + y, s_lo[2] + z, nb, blobs);
+        }
+}
+
+/* the Marschner-Lobb test signal (Marschner & Lobb, 1994) on [-1, 1]^3,
+ *   rho(x, y, z) = (1 - sin(pi z / 2) + alpha (1 + cos(2 pi f_M cos(pi r / 2)))) / (2 (1 + alpha)),
+ *   r = sqrt(x^2 + y^2),
+ * the smooth high-frequency stress field of SURVEY.md §8(d).  libm's sin/cos are not reproducible between
+ * the CPU and the GPU, so the cosine here is a fixed recipe -- reduction by 2pi (hi + lo), then a 14-term
+ * even Taylor polynomial in Horner form -- and the GPU generator (field.cu) repeats it operation for
+ * operation with explicitly rounded ops: voxels agree bit for bit.  |error| vs libm < 1e-13 on the
+ * arguments used (|a| < 2 pi f_M + pi). */
+static const double kMlCos[14] = {1.0, -0.5, 0.041666666666666664, -0.001388888888888889, 2.48015873015873e-05,
+                                  -2.755731922398589e-07, 2.08767569878681e-09, -1.1470745597729725e-11,
+                                  4.779477332387385e-14, -1.5619206968586225e-16, 4.110317623312165e-19,
+                                  -8.896791392450574e-22, 1.6117375710961184e-24, -2.4795962632247976e-27};
+#define ML_TWO_PI 6.283185307179586
+#define ML_TWO_PI_LO 2.4492935982947064e-16
+#define ML_INV_TWO_PI 0.15915494309189535
+#define ML_HALF_PI 1.5707963267948966
+
+double dvr_oracle_det_cos(double a) {
+    const double k = floor(a * ML_INV_TWO_PI + 0.5);
+    const double r = (a - k * ML_TWO_PI) - k * ML_TWO_PI_LO;
+    const double r2 = r * r;
+    double p = kMlCos[13];
+    for (int i = 12; i >= 0; --i) p = p * r2 + kMlCos[i];
+    return p;
+}
+
+static float ml_value(const int64_t N[3], int64_t i, int64_t j, int64_t k, double fm, double alpha) {
+    const double x = 2.0 * (N[0] > 1 ? (double)i / (double)(N[0] - 1) : 0.0) - 1.0;
+    const double y = 2.0 * (N[1] > 1 ? (double)j / (double)(N[1] - 1) : 0.0) - 1.0;
+    const double z = 2.0 * (N[2] > 1 ? (double)k / (double)(N[2] - 1) : 0.0) - 1.0;
+    const double r = sqrt(x * x + y * y);
+    const double pr = dvr_oracle_det_cos((ML_TWO_PI * fm) * dvr_oracle_det_cos(ML_HALF_PI * r));
+    const double sz = dvr_oracle_det_cos(ML_HALF_PI * z - ML_HALF_PI); /* sin(pi z / 2) */
+    double v = ((1.0 - sz) + alpha * (1.0 + pr)) / (2.0 * (1.0 + alpha));
+    if (v < 0.0) v = 0.0;
+    if (v > 1.0) v = 1.0;
+    return (float)v;
+}
+
+/* Marschner-Lobb voxels over the stored region (params = {f_M, alpha}), layout as dvr_oracle_generate. */
+void dvr_oracle_generate_ml(const int64_t* N, const int64_t* s_lo, const int64_t* sd, const double* params,
+                            float* out, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < sd[2]; ++z)
+        for (int64_t y = 0; y < sd[1]; ++y) {
+            float* row = out + (z * sd[1] + y) * sd[0];
+            for (int64_t x = 0; x < sd[0]; ++x)
+                row[x] = ml_value(N, s_lo[0] + x, s_lo[1] + y, s_lo[2] + z, params[0], params[1]);
         }
 }
 

@@ -48,7 +48,8 @@ _PARAMS: Dict[str, Dict[str, object]] = {
     "group": {"surfaces": []},
     "instance": {"group": None},
     "spatialField": {"dims": (64, 64, 64), "origin": (0.0, 0.0, 0.0), "spacing": (1.0, 1.0, 1.0),
-                     "generator": "blobs", "seed": 1, "blobCount": 16, "lopsided": False, "data": None},
+                     "generator": "blobs", "seed": 1, "blobCount": 16, "lopsided": False,
+                     "frequency": 6.0, "alpha": 0.25, "data": None},
     "transferFunction1D": {"table": None, "valueRange": (0.0, 1.0)},
     "volume": {"field": None, "transferFunction": None, "decomposition": "even", "ghost": 1,
                "massThreshold": 0.1},
@@ -128,7 +129,8 @@ def _triple(value, name: str, kind=float) -> Tuple:
 
 
 class SpatialField(ApiObject):
-    """Vertex-centred scalar grid; values from the seeded blob generator or a host array (z, y, x)."""
+    """Vertex-centred scalar grid; values from a generator ("blobs": seeded blob mixture; "marschnerLobb":
+    the Marschner-Lobb signal with ``frequency`` / ``alpha``) or a host array (z, y, x)."""
 
     def field_spec(self) -> Tuple[FieldSpec, Optional[np.ndarray]]:
         c = self.committed
@@ -139,6 +141,9 @@ class SpatialField(ApiObject):
             if arr.shape != tuple(reversed(dims)):
                 raise UsageError(f"spatialField data {arr.shape} does not match dims {dims} (z, y, x)")
             blobs = np.zeros((0, 5))
+        elif c["generator"] == "marschnerLobb":
+            return FieldSpec(dims, np.zeros((0, 5)), _triple(c["origin"], "origin"), _triple(c["spacing"], "spacing"),
+                             "marschnerLobb", (float(c["frequency"]), float(c["alpha"]))), None
         else:
             if c["generator"] != "blobs":
                 raise UsageError(f"unknown spatialField generator {c['generator']!r}")

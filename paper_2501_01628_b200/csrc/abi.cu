@@ -206,9 +206,13 @@ int dprt_brick_download(const DprtBrick* b, float* dst, int dst_is_device, void*
 
 int dprt_brick_generate(DprtBrick* b, const DprtFieldSpec* spec, void* stream) {
     if (!b || !spec) return fail(DPRT_E_USAGE, "null brick or field spec");
-    if (spec->kind != 0) return fail(DPRT_E_USAGE, "unknown field kind %d", spec->kind);
-    if (spec->n_blobs < 0 || spec->n_blobs > DPRT_MAX_BLOBS || (spec->n_blobs > 0 && !spec->blobs))
+    if (spec->kind != 0 && spec->kind != 1) return fail(DPRT_E_USAGE, "unknown field kind %d", spec->kind);
+    if (spec->kind == 1) {
+        if (!spec->blobs || !(spec->blobs[0] > 0.0) || !(spec->blobs[1] >= 0.0))
+            return fail(DPRT_E_USAGE, "Marschner-Lobb field needs {f_M > 0, alpha >= 0}");
+    } else if (spec->n_blobs < 0 || spec->n_blobs > DPRT_MAX_BLOBS || (spec->n_blobs > 0 && !spec->blobs)) {
         return fail(DPRT_E_USAGE, "n_blobs %d outside [0, %d]", spec->n_blobs, DPRT_MAX_BLOBS);
+    }
     int rc = bind(b->device);
     if (rc) return rc;
     CK(dprt::launch_generate(*b, *spec, (cudaStream_t)stream), "generate kernel launch");

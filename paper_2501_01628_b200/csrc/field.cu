@@ -13,9 +13,42 @@ struct GenArgs {
     long long N[3];
     long long s_lo[3];
     long long sd[3];
+    int kind;  // 0 blob mixture, 1 Marschner-Lobb (blobs[0..1] = f_M, alpha)
     int nb;
     double blobs[DPRT_MAX_BLOBS * 5];
 };
+
+// The oracle's reproducible cosine (oracle/dvr_oracle.c dvr_oracle_det_cos): 2pi reduction (hi + lo) and a
+// 14-term even Taylor polynomial, each op one explicitly rounded f64 op in the oracle's order.
+__constant__ double kMlCos[14] = {1.0, -0.5, 0.041666666666666664, -0.001388888888888889, 2.48015873015873e-05,
+                                  -2.755731922398589e-07, 2.08767569878681e-09, -1.1470745597729725e-11,
+                                  4.779477332387385e-14, -1.5619206968586225e-16, 4.110317623312165e-19,
+                                  -8.896791392450574e-22, 1.6117375710961184e-24, -2.4795962632247976e-27};
+constexpr double kTwoPi = 6.283185307179586, kTwoPiLo = 2.4492935982947064e-16;
+constexpr double kInvTwoPi = 0.15915494309189535, kHalfPi = 1.5707963267948966;
+
+__device__ double det_cos(double a) {
+    const double k = floor(__dadd_rn(__dmul_rn(a, kInvTwoPi), 0.5));
+    const double r = __dsub_rn(__dsub_rn(a, __dmul_rn(k, kTwoPi)), __dmul_rn(k, kTwoPiLo));
+    const double r2 = __dmul_rn(r, r);
+    double p = kMlCos[13];
+#pragma unroll
+    for (int i = 12; i >= 0; --i) p = __dadd_rn(__dmul_rn(p, r2), kMlCos[i]);
+    return p;
+}
+
+// Marschner-Lobb, operation for operation as ml_value in oracle/dvr_oracle.c.
+__device__ double ml_value(double ux, double uy, double uz, double fm, double alpha) {
+    const double x = __dsub_rn(__dmul_rn(2.0, ux), 1.0);
+    const double y = __dsub_rn(__dmul_rn(2.0, uy), 1.0);
+    const double z = __dsub_rn(__dmul_rn(2.0, uz), 1.0);
+    const double r = __dsqrt_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+    const double pr = det_cos(__dmul_rn(__dmul_rn(kTwoPi, fm), det_cos(__dmul_rn(kHalfPi, r))));
+    const double sz = det_cos(__dsub_rn(__dmul_rn(kHalfPi, z), kHalfPi));
+    double v = __ddiv_rn(__dadd_rn(__dsub_rn(1.0, sz), __dmul_rn(alpha, __dadd_rn(1.0, pr))),
+                         __dmul_rn(2.0, __dadd_rn(1.0, alpha)));
+    return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+}
 
 __global__ void generate_kernel(const GenArgs g, float* __restrict__ out) {
     const long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -26,6 +59,10 @@ __global__ void generate_kernel(const GenArgs g, float* __restrict__ out) {
     const double ux = g.N[0] > 1 ? __ddiv_rn((double)i, (double)(g.N[0] - 1)) : 0.0;
     const double uy = g.N[1] > 1 ? __ddiv_rn((double)j, (double)(g.N[1] - 1)) : 0.0;
     const double uz = g.N[2] > 1 ? __ddiv_rn((double)k, (double)(g.N[2] - 1)) : 0.0;
+    if (g.kind == 1) {
+        out[(z * g.sd[1] + y) * g.sd[0] + x] = __double2float_rn(ml_value(ux, uy, uz, g.blobs[0], g.blobs[1]));
+        return;
+    }
     double f = 0.0;
     for (int b = 0; b < g.nb; ++b) {
         const double* p = g.blobs + 5 * b;
@@ -45,8 +82,15 @@ cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cud
         g.s_lo[a] = b.s_lo[a];
         g.sd[a] = b.sd[a];
     }
-    g.nb = spec.n_blobs;
-    for (int i = 0; i < 5 * spec.n_blobs; ++i) g.blobs[i] = spec.blobs[i];
+    g.kind = spec.kind;
+    if (spec.kind == 1) {
+        g.nb = 0;
+        g.blobs[0] = spec.blobs[0];
+        g.blobs[1] = spec.blobs[1];
+    } else {
+        g.nb = spec.n_blobs;
+        for (int i = 0; i < 5 * spec.n_blobs; ++i) g.blobs[i] = spec.blobs[i];
+    }
     dim3 block(256);
     dim3 grid((unsigned)((b.sd[0] + 255) / 256), (unsigned)b.sd[1], (unsigned)b.sd[2]);
     generate_kernel<<<grid, block, 0, stream>>>(g, b.vox);

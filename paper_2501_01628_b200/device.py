@@ -80,8 +80,12 @@ class DeviceBrick:
     def generate(self, f: FieldSpec) -> "DeviceBrick":
         if tuple(f.dims) != tuple(self.desc.dims):
             raise UsageError(f"field dims {f.dims} != brick grid {self.desc.dims}")
-        blobs = np.ascontiguousarray(f.blobs, np.float64)
-        spec = _lib.FieldSpec(0, blobs.shape[0], ctypes.c_void_p(blobs.ctypes.data))
+        if f.kind == "marschnerLobb":
+            blobs = np.ascontiguousarray(f.ml, np.float64)  # {f_M, alpha}
+            spec = _lib.FieldSpec(1, 1, ctypes.c_void_p(blobs.ctypes.data))
+        else:
+            blobs = np.ascontiguousarray(f.blobs, np.float64)
+            spec = _lib.FieldSpec(0, blobs.shape[0], ctypes.c_void_p(blobs.ctypes.data))
         _lib.check(_lib.lib().dprt_brick_generate(self.handle, ctypes.byref(spec), _stream(self.device)),
                    "dprt_brick_generate")
         return self

@@ -17,7 +17,8 @@ Document::
     {"format": "dprt-volume", "version": 1,
      "field": {"dims": [nx, ny, nz], "origin": [..], "spacing": [..],
                "data": {"binary": "step0.f32", "dtype": "<f4"}            # raw sidecar, x fastest
-                    | {"generator": "blobs", "seed": 1, "blobCount": 16, "lopsided": false}},
+                    | {"generator": "blobs", "seed": 1, "blobCount": 16, "lopsided": false}
+                    | {"generator": "marschnerLobb", "frequency": 6.0, "alpha": 0.25}},
      "transferFunction": {"table": [[r, g, b, a], ...] | {"binary": "tf.f32", "count": n},
                           "valueRange": [0, 1]},
      "background": [r, g, b],
@@ -129,9 +130,17 @@ def parse_volume_scene(document: bytes, base_dir=None) -> VolumeScene:
         lop = bool(data.get("lopsided", False))
         blobs = blob_mixture(seed, count, lop)
         generator = {"generator": "blobs", "seed": seed, "blobCount": count, "lopsided": lop}
+    elif data.get("generator") == "marschnerLobb":
+        fm, alpha = data.get("frequency", 6.0), data.get("alpha", 0.25)
+        _expect(isinstance(fm, (int, float)) and fm > 0, "field.data.frequency", "must be a number > 0")
+        _expect(isinstance(alpha, (int, float)) and alpha >= 0, "field.data.alpha", "must be a number >= 0")
+        generator = {"generator": "marschnerLobb", "frequency": float(fm), "alpha": float(alpha)}
     else:
-        raise SceneFormatError('field.data: needs "binary" or "generator": "blobs"')
-    fs = FieldSpec(dims, blobs, origin, spacing)
+        raise SceneFormatError('field.data: needs "binary" or "generator": "blobs" | "marschnerLobb"')
+    if generator is not None and generator["generator"] == "marschnerLobb":
+        fs = FieldSpec(dims, blobs, origin, spacing, "marschnerLobb", (generator["frequency"], generator["alpha"]))
+    else:
+        fs = FieldSpec(dims, blobs, origin, spacing)
 
     t = doc.get("transferFunction", {})
     _expect(isinstance(t, dict), "transferFunction", "expected an object")

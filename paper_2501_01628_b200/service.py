@@ -103,9 +103,14 @@ def build_rank_objects(ep: RankEndpoint, scene: VolumeScene, composite: str = "a
         sf.set_param("data", scene.voxels())  # memory map: each rank copies only its brick
     else:
         g = scene.generator or {}
-        sf.set_param("seed", g.get("seed", 1))
-        sf.set_param("blobCount", g.get("blobCount", 16))
-        sf.set_param("lopsided", g.get("lopsided", False))
+        sf.set_param("generator", g.get("generator", "blobs"))
+        if g.get("generator") == "marschnerLobb":
+            sf.set_param("frequency", g["frequency"])
+            sf.set_param("alpha", g["alpha"])
+        else:
+            sf.set_param("seed", g.get("seed", 1))
+            sf.set_param("blobCount", g.get("blobCount", 16))
+            sf.set_param("lopsided", g.get("lopsided", False))
     sf.commit()
     tf = d.create("transferFunction1D")
     tf.set_param("table", scene.tf.as_f32())

@@ -23,23 +23,33 @@ from .geom import Aabb, Vec3
 # field
 
 
+FIELD_KINDS = ("blobs", "marschnerLobb")
+
+
 @dataclass(frozen=True)
 class FieldSpec:
     """Vertex-centred scalar field: dims voxels, voxel (i,j,k) at origin + (i,j,k)*spacing.
-    ``blobs`` (K x 5: cx, cy, cz, inv_rho2, amp in unit-cube coordinates) defines the synthetic
-    blob-mixture values."""
+    ``kind`` "blobs": ``blobs`` (K x 5: cx, cy, cz, inv_rho2, amp in unit-cube coordinates) defines the
+    synthetic blob-mixture values.  ``kind`` "marschnerLobb": the Marschner-Lobb test
+    signal over [-1, 1]^3 with ``ml`` = (f_M, alpha) (``blobs`` unused)."""
 
     dims: Tuple[int, int, int]
     blobs: np.ndarray = field(repr=False)
     origin: Vec3 = (0.0, 0.0, 0.0)
     spacing: Vec3 = (1.0, 1.0, 1.0)
+    kind: str = "blobs"
+    ml: Tuple[float, float] = (6.0, 0.25)
 
     def __post_init__(self) -> None:
         if len(self.dims) != 3 or any(int(d) < 2 for d in self.dims):
             raise UsageError(f"field dims must be three integers >= 2, got {self.dims}")
+        if self.kind not in FIELD_KINDS:
+            raise UsageError(f"unknown field kind {self.kind!r}; choose from {FIELD_KINDS}")
         b = np.asarray(self.blobs, np.float64)
         if b.ndim != 2 or b.shape[1] != 5 or b.shape[0] > 64:
             raise UsageError(f"blobs must be a (K <= 64, 5) array, got {b.shape}")
+        if self.kind == "marschnerLobb" and not (float(self.ml[0]) > 0.0 and float(self.ml[1]) >= 0.0):
+            raise UsageError(f"Marschner-Lobb needs f_M > 0 and alpha >= 0, got {self.ml}")
 
     def bounds(self) -> Aabb:
         hi = tuple(self.origin[a] + float(self.dims[a] - 1) * self.spacing[a] for a in range(3))
@@ -76,6 +86,13 @@ def blob_field(dims, seed: int = 1, n_blobs: int = 16, spacing=(1.0, 1.0, 1.0), 
                lopsided: bool = False) -> FieldSpec:
     return FieldSpec(tuple(int(d) for d in dims), blob_mixture(seed, n_blobs, lopsided),
                      tuple(float(o) for o in origin), tuple(float(s) for s in spacing))
+
+
+def marschner_lobb_field(dims, f_m: float = 6.0, alpha: float = 0.25, spacing=(1.0, 1.0, 1.0),
+                         origin=(0.0, 0.0, 0.0)) -> FieldSpec:
+    """The Marschner-Lobb signal (smooth, high-frequency stress for trilinear + TF)."""
+    return FieldSpec(tuple(int(d) for d in dims), np.zeros((0, 5)), tuple(float(o) for o in origin),
+                     tuple(float(s) for s in spacing), "marschnerLobb", (float(f_m), float(alpha)))
 
 
 # ------------------------------------------------------------------------------------------------

@@ -77,6 +77,22 @@ def test_field_data_shape_is_validated():
         sf.commit()
 
 
+def test_field_generators():
+    sf = _device().create("spatialField")
+    sf.set_param("dims", (9, 8, 7))
+    sf.set_param("generator", "marschnerLobb")
+    sf.set_param("frequency", 4.0)
+    sf.commit()
+    spec, data = sf.field_spec()
+    assert data is None and spec.kind == "marschnerLobb" and spec.ml == (4.0, 0.25)
+    sf.set_param("frequency", -1.0)
+    with pytest.raises(UsageError, match="f_M > 0"):
+        sf.commit()
+    sf.set_param("generator", "noise")
+    with pytest.raises(UsageError, match="unknown spatialField generator"):
+        sf.commit()
+
+
 def test_frame_commit_requires_children_and_size():
     dev = _device()
     frame = dev.create("frame")

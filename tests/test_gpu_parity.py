@@ -208,3 +208,50 @@ def test_fused_single_rank_frame_equals_composited(cuda_device, oracle_lib, monk
     assert np.array_equal(fused, plain)
     assert np.abs(fused.astype(np.int16) - want).max() <= RGB8_MAX_LSB
     brick.close()
+
+
+# ---- Marschner-Lobb field: high-frequency stress for trilinear + TF -------------
+
+def _peak_tf(n: int = 256, centre: float = 0.5, width: float = 0.06):
+    """An iso-surface-like TF: a narrow opacity peak around ``centre`` on a colour ramp."""
+    from paper_2501_01628_b200.volume import TransferFunction1D
+
+    x = np.linspace(0.0, 1.0, n)
+    a = 0.35 * np.exp(-(((x - centre) / width) ** 2))
+    t = np.column_stack([0.2 + 0.8 * x, 1.0 - 0.7 * x, 0.3 + 0.4 * np.sin(3 * x), a]).astype(np.float32)
+    return TransferFunction1D(t, 0.0, 1.0)
+
+
+def test_marschner_lobb_generation_bit_exact(cuda_device, oracle_lib):
+    from paper_2501_01628_b200.volume import marschner_lobb_field
+
+    for f in (marschner_lobb_field((41, 37, 33)), marschner_lobb_field((129, 129, 129), f_m=9.0, alpha=0.1)):
+        hi = tuple(d - 1 for d in f.dims)
+        for lo, hi_, g in [((0, 0, 0), hi, 0), ((5, 3, 7), (20, hi[1], 15), 1), ((0, 10, 0), (hi[0], 20, hi[2]), 2)]:
+            desc = BrickDesc(f.dims, lo, hi_, g)
+            b = dev.DeviceBrick(desc, cuda_device).generate(f)
+            got = b.download()
+            ref = oracle.generate_ml(f.dims, f.ml, desc.stored_lo, desc.stored_dims)
+            assert np.array_equal(got, ref), f"{f.dims} brick {lo}-{hi_}"
+            b.close()
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_marschner_lobb_frame_matches_oracle(cuda_device, oracle_lib, P):
+    from paper_2501_01628_b200.volume import marschner_lobb_field
+
+    f = marschner_lobb_field((65, 65, 65))
+    vox = oracle.generate_ml(f.dims, f.ml)
+    dec = decompose(f, P)
+    W, H = 128, 112
+    for cam, tf in [(auto_camera(f.bounds(), W, H), _peak_tf()),
+                    (orbit_camera(f.bounds().center(), 110.0, 0.7, 0.4, 40.0, W / H), _peak_tf(centre=0.3)),
+                    (auto_camera(f.bounds(), W, H), dense_tf())]:
+        ref, rs = oracle_partials(vox, dec, cam, tf, 1.0, 0.99, W, H)
+        parts, samples = _gpu_partials(dec, cam, tf, 1.0, 0.99, W, H, cuda_device)
+        for r in range(P):
+            assert np.array_equal(samples[r].view(H, W).cpu().numpy().astype(np.uint32), rs[r]), f"rank {r}"
+            _check_rgba(parts[r].view(H, W, 4).cpu().numpy(), ref[r], f"ML P={P} rank {r}")
+        order = dec.visibility_order(cam.position)
+        img = oracle.composite(ref, order, (0.1, 0.1, 0.1))
+        assert img.max() > 0.15, "the peak TF must make the field visible"

@@ -29,6 +29,15 @@ def test_generated_document_round_trip():
     assert np.array_equal(again.tf.as_f32(), s.tf.as_f32())
 
 
+def test_marschner_lobb_document_round_trip():
+    s = parse_volume_scene(_doc(field={"dims": [9, 8, 7], "data": {"generator": "marschnerLobb", "frequency": 3}}))
+    assert s.field.kind == "marschnerLobb" and s.field.ml == (3.0, 0.25)
+    again = parse_volume_scene(serialize_volume_scene(s))
+    assert again.field.kind == "marschnerLobb" and again.field.ml == (3.0, 0.25)
+    with pytest.raises(SceneFormatError, match="frequency"):
+        parse_volume_scene(_doc(field={"dims": [9, 8, 7], "data": {"generator": "marschnerLobb", "frequency": 0}}))
+
+
 def test_binary_sidecar_and_brick_extraction(tmp_path):
     f = blob_field((21, 17, 13), seed=2)
     vox = oracle.generate_field(f.dims, f.blobs)

@@ -17,9 +17,15 @@ ap.add_argument("--H", type=int, default=1080)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--no-skip", action="store_true")
 ap.add_argument("--threshold", type=float, default=0.1)
+ap.add_argument("--field", choices=["blobs", "ml"], default="blobs")
 args = ap.parse_args()
 d = torch.device("cuda", 0)
-f = blob_field((args.edge + 1,) * 3, seed=1)
+if args.field == "ml":
+    from paper_2501_01628_b200.volume import marschner_lobb_field
+
+    f = marschner_lobb_field((args.edge + 1,) * 3)
+else:
+    f = blob_field((args.edge + 1,) * 3, seed=1)
 dec = decompose(f, 1)
 cam = auto_camera(f.bounds(), args.W, args.H)
 tf = default_tf(threshold=args.threshold)
