@@ -351,7 +351,11 @@ __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int
 #ifndef DPRT_BEAM_MINBLOCKS
 #define DPRT_BEAM_MINBLOCKS 3
 #endif
-__global__ void __launch_bounds__(kTileX * kTileY, DPRT_BEAM_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
+#ifndef DPRT_BEAM_BLOCK
+#define DPRT_BEAM_BLOCK 256
+#endif
+constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are independent beams)
+__global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_tf; i += blockDim.x) {
@@ -732,9 +736,9 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
         }
         if (e == cudaSuccess && a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.W * a.H * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kTileX * kTileY, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kBeamBlock, smem);
         if (per_sm < 1) per_sm = 1;
-        march_beam_kernel<<<sms * per_sm, block, smem, stream>>>(a);
+        march_beam_kernel<<<sms * per_sm, kBeamBlock, smem, stream>>>(a);
         return cudaGetLastError();
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, kTileX * kTileY, smem);
