@@ -472,6 +472,39 @@ int dprt_kat_primary_dirs(int device, const DprtCamera* cam, int W, int H, doubl
     return DPRT_OK;
 }
 
+namespace {
+// SM-driven copy of a small input block from mapped pinned host memory (16-byte vectors + byte tail).
+__global__ void stage_input_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, unsigned long long n) {
+    const unsigned long long nv = n / 16;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = __ldcv(reinterpret_cast<const uint4*>(src) + i);  // no stale cache lines
+    if (blockIdx.x == 0 && threadIdx.x < n % 16) dst[nv * 16 + threadIdx.x] = src[nv * 16 + threadIdx.x];
+}
+}  // namespace
+
+int dprt_stage_input(int device, void* dst_dev, const void* src_pinned, uint64_t bytes, void* stream) {
+    if (!dst_dev || !src_pinned) return fail(DPRT_E_USAGE, "null staging pointer");
+    if (bytes == 0) return DPRT_OK;
+    if (bytes > (1ull << 20)) return fail(DPRT_E_USAGE, "dprt_stage_input is for small inputs (%llu bytes > 1 MiB)",
+                                          (unsigned long long)bytes);
+    if (((uintptr_t)dst_dev | (uintptr_t)src_pinned) & 15u) return fail(DPRT_E_USAGE, "staging pointers must be 16-byte aligned");
+    int rc = bind(device);
+    if (rc) return rc;
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, src_pinned) != cudaSuccess || pa.type != cudaMemoryTypeHost ||
+        !pa.devicePointer) {
+        cudaGetLastError();
+        return fail(DPRT_E_USAGE, "dprt_stage_input source is not page-locked host memory");
+    }
+    const unsigned long long nv = (bytes + 15) / 16;
+    const unsigned blocks = (unsigned)((nv + 255) / 256);
+    stage_input_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(dst_dev),
+                                                                 static_cast<const uint8_t*>(pa.devicePointer), bytes);
+    CK(cudaGetLastError(), "stage_input kernel launch");
+    return DPRT_OK;
+}
+
 int dprt_device_alloc(int device, uint64_t bytes, void** out_ptr) {
     if (!out_ptr || bytes == 0) return fail(DPRT_E_USAGE, "bad allocation request");
     *out_ptr = nullptr;

@@ -142,13 +142,19 @@ class DeviceTF:
     """A transfer function table resident on one device (4 KiB for 256 entries).
 
     ``version`` tags the table contents for the bricks' cached skip distances; ``update`` re-uploads
-    and bumps it only when the contents change."""
+    and bumps it only when the contents change.  Uploads from a pinned staging buffer alternate between
+    two device tables and run on a side stream (``dprt_stage_input``, SM-driven): frame k's table is
+    staged while frame k-1 still marches out of the other one, and the march of frame k waits on it."""
 
     def __init__(self, tf: TransferFunction1D, device: torch.device):
         self.tf = tf
         self._host = tf.as_f32().reshape(-1).copy()
         self.table = torch.from_numpy(self._host.copy()).to(device)
         self.version = next(_TF_VERSIONS)
+        self._tables = None        # the two staging targets (allocated on the first staged update)
+        self._slot = 0
+        self._side = None          # side stream for the staging copies
+        self._marker = None        # main-stream event recorded at the previous staged update
 
     def update(self, tf: TransferFunction1D, staging: Optional[torch.Tensor] = None) -> None:
         """New table contents (optionally copied from a pinned host staging tensor)."""
@@ -159,9 +165,37 @@ class DeviceTF:
             self._host = host.copy()
             if host.shape[0] != self.table.numel():
                 self.table = torch.empty(host.shape[0], dtype=torch.float32, device=self.table.device)
+                self._tables = None
         self.tf = tf
+        if staging is not None and staging.is_pinned() and staging.numel() == host.shape[0] and \
+                staging.dtype == torch.float32:
+            self._stage(staging)
+            return
         src = staging if staging is not None else torch.from_numpy(self._host)
         self.table.copy_(src, non_blocking=staging is not None)
+
+    def _stage(self, staging: torch.Tensor) -> None:
+        d = self.table.device
+        main = torch.cuda.current_stream(d)
+        if self._tables is None:
+            self._tables = [self.table, torch.empty_like(self.table)]
+            self._side = torch.cuda.Stream(d)
+            self._marker = None
+        self._slot ^= 1
+        dst = self._tables[self._slot]
+        # the slot was last read by the march enqueued before the previous staged update: wait for
+        # exactly that work (the marker), not for the march still running out of the other slot
+        if self._marker is not None:
+            self._side.wait_event(self._marker)
+        self._marker = torch.cuda.Event()
+        self._marker.record(main)
+        _lib.check(_lib.lib().dprt_stage_input(d.index, ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(staging.data_ptr()),
+                                               dst.numel() * 4, ctypes.c_void_p(self._side.cuda_stream)),
+                   "dprt_stage_input")
+        ready = torch.cuda.Event()
+        ready.record(self._side)
+        main.wait_event(ready)
+        self.table = dst
 
     def params(self, dt: float, ert: float, flags: int = 0) -> _lib.MarchParams:
         return _lib.MarchParams(ctypes.c_void_p(self.table.data_ptr()), self.tf.n, flags, float(self.tf.vmin),

@@ -255,3 +255,43 @@ def test_marschner_lobb_frame_matches_oracle(cuda_device, oracle_lib, P):
         order = dec.visibility_order(cam.position)
         img = oracle.composite(ref, order, (0.1, 0.1, 0.1))
         assert img.max() > 0.15, "the peak TF must make the field visible"
+
+
+def test_stage_input_from_pinned_memory(cuda_device):
+    """dprt_stage_input: SM-driven copy from mapped pinned memory (any size, byte tail), usage errors."""
+    import ctypes
+
+    from paper_2501_01628_b200 import _lib
+    from paper_2501_01628_b200.errors import UsageError
+
+    for n in (16, 4096, 4099, 65536 + 5):
+        src = torch.randint(0, 256, (n,), dtype=torch.uint8).pin_memory()
+        dst = torch.zeros(n + 16, dtype=torch.uint8, device=cuda_device)
+        _lib.check(_lib.lib().dprt_stage_input(cuda_device.index or 0, ctypes.c_void_p(dst.data_ptr()),
+                                               ctypes.c_void_p(src.data_ptr()), n, None), "stage")
+        torch.cuda.synchronize()
+        assert torch.equal(dst[:n].cpu(), src) and int(dst[n:].sum()) == 0
+    plain = torch.zeros(64, dtype=torch.uint8)  # pageable: refused
+    with pytest.raises(UsageError, match="page-locked"):
+        _lib.check(_lib.lib().dprt_stage_input(0, ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(plain.data_ptr()),
+                                               64, None), "stage")
+
+
+def test_tf_update_through_pinned_staging_matches_oracle(cuda_device, oracle_lib):
+    """DeviceTF.update(staging=pinned) (the e2e path) re-renders with the new table, frame after frame."""
+    f = blob_field((40, 36, 32), seed=3)
+    vox = oracle.generate_field(f.dims, f.blobs)
+    dec = decompose(f, 1)
+    W, H = 64, 56
+    cam = auto_camera(f.bounds(), W, H)
+    b = dev.DeviceBrick(dec.brick(0), cuda_device).generate(f)
+    dtf = dev.DeviceTF(default_tf(), cuda_device)
+    p = torch.empty(H * W * 4, dtype=torch.float32, device=cuda_device)
+    for tf in (dense_tf(), default_tf(), dense_tf(64)):
+        staging = torch.from_numpy(tf.as_f32().reshape(-1).copy()).pin_memory()
+        dtf.update(tf, staging=staging)
+        dev.march(b, cam, dtf, 1.0, 0.99, p, W, H)
+        torch.cuda.synchronize()
+        ref, _ = oracle_partials(vox, dec, cam, tf, 1.0, 0.99, W, H)
+        _check_rgba(p.view(H, W, 4).cpu().numpy(), ref[0], f"staged TF n={tf.n}")
+    b.close()
