@@ -252,9 +252,14 @@ class DistEndpoint(RankEndpoint):
                     pass
 
     def device_barrier(self) -> None:
+        """Every rank's stream-ordered work issued so far is complete before any rank's later work.
+        NCCL: a 4-byte all-reduce on the current stream (stream ordered, the host does not block).
+        Other backends (gloo with CUDA buffers): drain this rank's stream, then a host all-reduce."""
         if self._token is None:
             dev = self.device if self.backend == "nccl" else torch.device("cpu")
             self._token = torch.zeros(1, dtype=torch.int32, device=dev)
+        if self.backend != "nccl" and self.device is not None and self.device.type == "cuda":
+            torch.cuda.current_stream(self.device).synchronize()
         dist.all_reduce(self._token, group=self.group)
 
 

@@ -47,13 +47,15 @@ def run_ranks(world: int, fn, *args, timeout: float = 120.0):
     for p in procs:
         p.start()
     results, errors = {}, {}
-    for _ in range(world):
-        rank, status, val = q.get(timeout=timeout)
-        (results if status == "ok" else errors)[rank] = val
-    for p in procs:
-        p.join(timeout=30)
-        if p.is_alive():
-            p.kill()
+    try:
+        for _ in range(world):
+            rank, status, val = q.get(timeout=timeout)
+            (results if status == "ok" else errors)[rank] = val
+    finally:
+        for p in procs:  # exactly the processes started here
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
     if errors:
         raise RuntimeError("rank failures:\n" + "\n".join(f"rank {r}: {e}" for r, e in sorted(errors.items())))
     return [results[r] for r in range(world)]

@@ -1,0 +1,59 @@
+"""Two PROCESSES sharing the one GPU of the test box, gloo control plane: the fused p2p compositor's real
+CUDA IPC path (export a handle per rank, map the peer's partial and rank 0's frame in the other process,
+composite through the mapped pointers).  In-process rank threads (test_gpu_multirank.py) share one
+address space and never exercise IPC.  No kernel waits on another process: the device barriers drain the
+stream and meet on the host (DistEndpoint.device_barrier, non-NCCL branch)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from dist_util import run_ranks
+from scenes import RGB8_MAX_LSB, RGBA_ATOL, c1, oracle_partials
+
+pytestmark = pytest.mark.gpu
+
+
+def _rank_body(ep, mode, W, H):
+    import torch
+
+    from paper_2501_01628_b200 import device as dev
+    from paper_2501_01628_b200.engine import RenderOptions, VolumeRenderer
+    from paper_2501_01628_b200.transport import DistEndpoint
+
+    cuda = torch.device("cuda", 0)
+    ep = DistEndpoint(device=cuda)
+    s = c1(P=ep.R, W=W, H=H)
+    b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda).generate(s.field)
+    vr = VolumeRenderer(ep, b, s.dec, s.tf, s.background)
+    out = []
+    for frame in range(2):
+        res = vr.render(s.cam, W, H, RenderOptions(composite=mode, keep_float=True, frame_index=frame))
+        torch.cuda.synchronize()
+        out.append((None if res.image is None else np.asarray(res.image),
+                    None if res.rgb8 is None else res.rgb8.cpu().numpy()))
+    used = vr.compositor.mode
+    vr.compositor = None
+    b.close()
+    return used, out
+
+
+@pytest.mark.parametrize("mode,R", [("p2p", 2), ("auto", 3)])
+def test_ipc_p2p_frame_across_processes(cuda_device, oracle_lib, mode, R):
+    W, H = 160, 122
+    results = run_ranks(R, _rank_body, mode, W, H, timeout=240.0)
+    s = c1(P=R, W=W, H=H)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, _ = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, W, H)
+    want = oracle.composite(ref, s.dec.visibility_order(s.cam.position), s.background)
+    for r, (used, frames) in enumerate(results):
+        assert used == "p2p", f"rank {r} fell back to {used}: the IPC mapping failed"
+        for image, rgb8 in frames:
+            if r == 0:
+                assert np.abs(image - want).max() <= RGBA_ATOL
+                q = rgb8.astype(np.int16) - oracle.tone_map_rgb8(want).astype(np.int16)
+                assert np.abs(q).max() <= RGB8_MAX_LSB
+            else:
+                assert image is None and rgb8 is None
