@@ -207,8 +207,19 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
-        ep = init_dist("nccl")
-        device = ep.device
+        backend = os.environ.get("DPRT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            ep = init_dist("nccl")
+            device = ep.device
+        else:
+            # functional test hook only (tests/test_gpu_multiprocess.py): gloo control plane, ranks
+            # possibly sharing a GPU -- never a measurement
+            from paper_2501_01628_b200.transport import DistEndpoint
+
+            device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
+            torch.cuda.set_device(device)
+            dist.init_process_group(backend)
+            ep = DistEndpoint(device=device)
     else:
         device = torch.device("cuda", 0)
         torch.cuda.set_device(device)

@@ -57,3 +57,28 @@ def test_ipc_p2p_frame_across_processes(cuda_device, oracle_lib, mode, R):
                 assert np.abs(q).max() <= RGB8_MAX_LSB
             else:
                 assert image is None and rgb8 is None
+
+
+def test_bench_multi_rank_code_path(tmp_path):
+    """bench.py's N > 1 leg (weak-scaled bricks, compositor roofline, e2e, max over ranks) run as two
+    torchrun processes on this box's one GPU with the gloo control plane (DPRT_BENCH_BACKEND=gloo): a
+    functional check of the code the 8-GPU scaling run executes, not a measurement."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DPRT_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", str(root / "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3"]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["compositor_roofline"]["mode"] in ("p2p", "direct_send")
+    assert line["config"]["bricks"] == 2
