@@ -318,6 +318,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
         a.origin[i] = b->desc.origin[i];
         a.spacing[i] = b->desc.spacing[i];
         a.inv_spacing[i] = (float)(1.0 / b->desc.spacing[i]);
+        a.inv_spacing_d[i] = 1.0 / b->desc.spacing[i];
         a.stored_lo_d[i] = (double)b->s_lo[i];
         a.clo[i] = 0;
         a.chi[i] = (int)(b->sd[i] - 2);
@@ -328,6 +329,10 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.half_w = cam->half_w;
     a.half_h = cam->half_h;
     a.dt = p->dt;
+    {
+        int ex;
+        a.inv_dt_pow2 = (frexp(p->dt, &ex) == 0.5) ? 1.0 / p->dt : 0.0;  // exact inverse of a power of two
+    }
     a.sy = (long long)b->sd[0];
     a.sz = (long long)b->sd[0] * b->sd[1];
     a.vox = b->vox;

@@ -55,6 +55,8 @@ struct MarchArgs {
     double blo[3], bhi[3];
     double origin[3], spacing[3];
     double dt;
+    double inv_dt_pow2;       // 1 / dt when dt is a power of two (t / dt == t * inv exactly), else 0
+    double inv_spacing_d[3];  // 1 / spacing (start positions only; not on the exact ownership path)
     // f32 march state
     float inv_spacing[3];
     double stored_lo_d[3];  // s_lo (local coordinate shift)

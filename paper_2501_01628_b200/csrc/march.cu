@@ -88,8 +88,9 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
     if (!slab_interval(a.o, d, a.blo, a.bhi, &t0, &t1)) return 0;
     if (t0 < 0.0) t0 = 0.0;
     if (t1 < t0) return 0;
-    const int64_t ka = (int64_t)ceil(__ddiv_rn(t0, a.dt));
-    const int64_t kb = (int64_t)ceil(__ddiv_rn(t1, a.dt));
+    // t / dt: for a power-of-two dt the product with the exact inverse is the identical IEEE result
+    const int64_t ka = (int64_t)ceil(a.inv_dt_pow2 != 0.0 ? __dmul_rn(t0, a.inv_dt_pow2) : __ddiv_rn(t0, a.dt));
+    const int64_t kb = (int64_t)ceil(a.inv_dt_pow2 != 0.0 ? __dmul_rn(t1, a.inv_dt_pow2) : __ddiv_rn(t1, a.dt));
     *k0 = ka;
     return kb > ka ? kb - ka : 0;
 }
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kTileX * kTileY) ray_setup_kernel(const MarchA
     float p0[3], st[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const double p = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
+        const double p = (a.o[i] + t0 * d[i] - a.origin[i]) * a.inv_spacing_d[i];
         p0[i] = (float)(p - a.stored_lo_d[i]);
         st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
     }
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                 const double t0 = __dmul_rn((double)k0, a.dt);
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    const double pw = (a.o[i] + t0 * d[i] - a.origin[i]) / a.spacing[i];
+                    const double pw = (a.o[i] + t0 * d[i] - a.origin[i]) * a.inv_spacing_d[i];
                     p0[i] = (float)(pw - a.stored_lo_d[i]);
                     st[i] = (float)(a.dt * d[i]) * a.inv_spacing[i];
                 }
