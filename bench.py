@@ -73,7 +73,8 @@ def workload(n_ranks: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + clock-event (throttle) reasons DURING the timed region: NVML polled every 1 ms from a
+    thread (the timed region is only milliseconds long), plus the recipe's nvidia-smi -lms 200 stream."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -83,8 +84,52 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.nvml = []          # (sm_mhz, max_mhz, reason bitmask)
+        self._stop = threading.Event()
+        self._poll = None
+        self.error = None
+
+    def _nvml_handle(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:
+            import torch
+
+            bus = getattr(torch.cuda.get_device_properties(self.index), "pci_bus_id", None)
+            if bus is not None:
+                dom = getattr(torch.cuda.get_device_properties(self.index), "pci_domain_id", 0)
+                dev = getattr(torch.cuda.get_device_properties(self.index), "pci_device_id", 0)
+                return pynvml.nvmlDeviceGetHandleByPciBusId(f"{dom:08x}:{bus:02x}:{dev:02x}.0")
+        except Exception:  # noqa: BLE001 - fall back to the index
+            pass
+        return pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _sample(self):
+        import pynvml
+
+        self.nvml.append((pynvml.nvmlDeviceGetClockInfo(self._h, pynvml.NVML_CLOCK_SM), self._mx,
+                          pynvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)))
+
+    def _poll_nvml(self):
+        try:
+            while not self._stop.is_set():
+                self._sample()
+                time.sleep(0.001)
+        except Exception as exc:  # noqa: BLE001 - NVML unavailable: the nvidia-smi stream remains
+            self.error = f"{type(exc).__name__}: {exc}"
 
     def __enter__(self):
+        try:  # NVML set up synchronously, so polling covers the whole timed region
+            import pynvml
+
+            self._h = self._nvml_handle()
+            self._mx = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self._poll = threading.Thread(target=self._poll_nvml, daemon=True)
+            self._poll.start()
+        except Exception as exc:  # noqa: BLE001
+            self.error = f"{type(exc).__name__}: {exc}"
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
@@ -100,6 +145,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self._stop.set()
+        if self._poll is not None:
+            self._poll.join(1)
+            try:
+                self._sample()  # the clock right at the end of the timed region
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
@@ -123,9 +175,17 @@ class ClockSampler:
             for n, v in zip(names, parts[3:7]):
                 if v.lower() == "active":
                     reasons.add(n)
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        if self.nvml:
+            for _, _, r in self.nvml:
+                reasons.update(n for n, b in bits.items() if r & b)
+            return {"sm_mhz": statistics.median(c for c, _, _ in self.nvml), "sm_max_mhz": float(self.nvml[0][1]),
+                    "reasons": sorted(reasons), "samples": len(self.nvml), "source": "nvml 1 ms poll + nvidia-smi",
+                    "smi_samples": len(sm)}
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi", "nvml_error": self.error}
 
 
 def cpu_baseline(vox: np.ndarray, dec, cam, tf, target_s: float = 12.0):
