@@ -347,6 +347,9 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #ifndef DPRT_BEAM_PROBE
 #define DPRT_BEAM_PROBE 1
 #endif
+#ifndef DPRT_BRANCHFREE
+#define DPRT_BRANCHFREE 1  // 0: per-slot branches (the v5 loop), kept for comparison
+#endif
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
 #ifndef DPRT_BEAM_MINBLOCKS
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1];
     const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
+    const float4* __restrict__ s_dtf = s_tf + a.n_tf;
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
@@ -536,6 +540,57 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
 #endif
             // Shade this lane's samples in the slab, kBeamUnroll at a time: all their corner loads are
             // issued before the first is shaded, so each lane keeps several loads in flight.
+#if DPRT_BRANCHFREE
+            // branch-free batches: slots past the lane's last sample in the slab re-load that sample (same
+            // address, an L1 hit) and contribute w = 0; ERT masks the rest of the batch the same way
+            const float fend = (float)(jend - 1);
+            while (j < jend) {
+                float4 qa[kBeamUnroll], qb[kBeamUnroll];
+                float wx[kBeamUnroll], wy[kBeamUnroll], wz[kBeamUnroll];
+                const float fj = (float)j;  // exact: j < 2^24
+#pragma unroll
+                for (int u = 0; u < kBeamUnroll; ++u) {
+                    const float fs = fminf(fj + (float)u, fend);
+                    const float ux = fmaf(fs, st[0], p0[0]);
+                    const float uy = fmaf(fs, st[1], p0[1]);
+                    const float uz = fmaf(fs, st[2], p0[2]);
+                    const int ix = __float2int_rd(ux), iy = __float2int_rd(uy), iz = __float2int_rd(uz);
+                    const int qi = iz * qsz + iy * qsy + ix;
+                    quad_bounds_check(a, qi);
+                    qa[u] = __ldg(qorg + qi);
+                    qb[u] = __ldg(qorg1 + qi);
+                    wx[u] = __saturatef(ux - (float)ix);
+                    wy[u] = __saturatef(uy - (float)iy);
+                    wz[u] = __saturatef(uz - (float)iz);
+                }
+                const int cnt = min(kBeamUnroll, jend - j);
+                float m = 1.f;  // 1 while the slot is a real sample of a live ray, then 0
+#pragma unroll
+                for (int u = 0; u < kBeamUnroll; ++u) {
+                    if (u >= cnt) m = 0.f;
+                    const float v = trilerp(qa[u], qb[u], wx[u], wy[u], wx[u] * wy[u], wz[u]);
+                    const float x = __saturatef(fmaf(v, tns, tno)) * top;
+                    const int ti = (int)x;
+                    const float tfr = x - (float)ti;
+                    const float4 e0 = s_tf[ti], de = s_dtf[ti];
+                    const float w = m * ((1.f - A) * fmaf(tfr, de.w, e0.w));
+                    A += w;
+                    C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+                    C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+                    C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+#if DPRT_COUNTERS
+                    c_shade += m != 0.f;
+                    c_contrib += w > 0.f;
+#endif
+                    if (A >= ert) m = 0.f;  // early ray termination: the rest of the batch adds nothing
+                }
+                j += cnt;
+                if (A >= ert) {
+                    live = false;
+                    break;
+                }
+            }
+#else
             while (j < jend) {
                 const int cnt = min(kBeamUnroll, jend - j);
                 float4 qa[kBeamUnroll], qb[kBeamUnroll];
@@ -581,6 +636,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                     break;
                 }
             }
+#endif
             if (j >= nn) live = false;
         }
         if (nn > 0) {
