@@ -350,6 +350,7 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #ifndef DPRT_BRANCHFREE
 #define DPRT_BRANCHFREE 1  // 0: per-slot branches (the v5 loop), kept for comparison
 #endif
+
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
 #ifndef DPRT_BEAM_MINBLOCKS
