@@ -347,6 +347,10 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #ifndef DPRT_BEAM_PROBE
 #define DPRT_BEAM_PROBE 1
 #endif
+#ifndef DPRT_SLAB_SHIFT
+#define DPRT_SLAB_SHIFT DPRT_MACRO_SHIFT  // slab thickness (cells, log2) of the probe-mode beam step
+#endif
+constexpr int kSlabShift = DPRT_SLAB_SHIFT;
 #ifndef DPRT_BRANCHFREE
 #define DPRT_BRANCHFREE 1  // 0: per-slot branches (the v5 loop), kept for comparison
 #endif
@@ -480,14 +484,14 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
 #endif
             // current slab: the nearest (in the march direction) slab holding a sampling lane's next sample
             int ksl = 0;
-            if (samp) ksl = fl2cell(fmaf((float)j, sa, pa), cha) >> kMacroShift;
+            if (samp) ksl = fl2cell(fmaf((float)j, sa, pa), cha) >> kSlabShift;
             const int key = samp ? (pos ? ksl : -ksl) : 0x7fffffff;
             const int kmin = __reduce_min_sync(FULL, key);
             const int K = pos ? kmin : -kmin;
             // this lane's samples in slab K: j .. jend-1 (first sample past the slab's far face)
             int jend = j;
             if (samp) {
-                const float face = (float)((pos ? K + 1 : K) << kMacroShift);
+                const float face = (float)((pos ? K + 1 : K) << kSlabShift);
                 const float je = (face - pa) * isa;
                 jend = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;  // >= 1 sample: progress
                 if (ksl != K) jend = j;  // this ray is not in slab K yet
