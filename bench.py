@@ -326,24 +326,31 @@ def run_ours(args):
     if R > 1:
         order = renderer.decomposition.visibility_order(cam.position)
         comp = renderer.compositor
+        # the step's exchange: footprint-row bands when the mode clips them (RenderOptions.clip_exchange)
+        bands = renderer._bands(cam, W, H) if comp.clips_bands() else None
         cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         barrier()
         for a_, b_ in cev:
             a_.record(stream)
-            comp.composite(renderer.partial, order, BACKGROUND)
+            comp.composite(renderer.partial, order, BACKGROUND, bands=bands)
             b_.record(stream)
         barrier()
         cms = torch.tensor([sum(a_.elapsed_time(b_) for a_, b_ in cev) / len(cev)], dtype=torch.float64,
                            device=device)
         dist.all_reduce(cms, op=dist.ReduceOp.MAX)
         comp_ms = float(cms.item())
-        frag_bytes = int((1 - 1 / R) * W * H * 16)          # RGBA f32 fragments each rank sends
+        # fragment bytes this rank moved (sent, or read from peers in p2p mode) + its RGB8 tile; max over ranks
+        moved = torch.tensor([float(comp.last_bytes)], dtype=torch.float64, device=device)
+        dist.all_reduce(moved, op=dist.ReduceOp.MAX)
+        frag_bytes = int(moved.item())
+        full_bytes = int((1 - 1 / R) * W * H * 16)          # unclipped RGBA f32 fragments per rank
         gather_bytes = int((R - 1) / R * W * H * 3)          # RGB8 tiles into rank 0
         achieved_nv = frag_bytes / (comp_ms * 1e-3) / 1e9
         nvlink = {"bound": "nvlink", "achieved": achieved_nv, "peak": 770.0, "unit": "GB/s",
                   "frac": achieved_nv / 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                  "composite_ms": comp_ms, "fragment_bytes_per_rank": frag_bytes, "rgb8_into_root": gather_bytes,
-                  "mode": comp.mode}
+                  "composite_ms": comp_ms, "fragment_bytes_per_rank": frag_bytes,
+                  "unclipped_fragment_bytes_per_rank": full_bytes, "rgb8_into_root": gather_bytes,
+                  "mode": comp.mode, "clipped_to_footprint_rows": bands is not None}
 
     # ---- marcher alone, CUDA events on its launch stream (roofline)
     # (the same call the step makes: the fused RGB8 march at one rank, the RGBA-partial march otherwise)

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 3
+#define DPRT_ABI_VERSION 4
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -90,6 +90,8 @@ typedef struct DprtMarchParams {
 #define DPRT_MARCH_FULL_FRAME 2   /* march every pixel instead of the brick's screen footprint */
 #define DPRT_MARCH_BEAM 4         /* force the warp-beam marcher (8x4 pixel beams, slab-wise skipping) */
 #define DPRT_MARCH_QUEUE 8        /* force the ray-queue marcher (persistent warps, per-lane refill) */
+#define DPRT_MARCH_BAND_CLEAR 16  /* beam marcher: clear only the footprint's row band of the partial; rows
+                                     outside it are left as they were (for band-clipped compositing) */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
 #define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */
@@ -113,6 +115,9 @@ int dprt_brick_destroy(DprtBrick* b);
 
 /* Screen footprint [x0, y0, x1, y1) of the owned box under `cam` (whole frame if the eye is too close). */
 int dprt_brick_footprint(const DprtBrick* b, const DprtCamera* cam, int W, int H, int32_t rect[4]);
+/* The same rectangle from a descriptor alone (host-only, no device): every rank computes every brick's
+ * footprint locally, so the compositor can clip the exchange without communicating rectangles. */
+int dprt_desc_footprint(const DprtBrickDesc* desc, const DprtCamera* cam, int W, int H, int32_t rect[4]);
 
 /* Per-rank local work: replaces trace_local_round -> trace_nearest_batch (engine.py:254-279,
  * bvh.py:284-296).  Writes the full-frame premultiplied RGBA partial (W*H*4 f32, zero outside the
@@ -134,6 +139,13 @@ int dprt_march_rgb8(const DprtBrick* b, const DprtCamera* cam, const DprtMarchPa
  * rgba_out (npix*4) may also be peer pointers (fused gather into rank 0's frame). */
 int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, const float bg[3], int flags,
                    uint8_t* rgb8, float* rgba_out, void* stream);
+
+/* The same with per-fragment pixel ranges (HOST array of P {lo, hi} pairs within [0, npix)): fragment i
+ * covers tile pixels [lo_i, hi_i) only -- inputs[i] points at its element for pixel lo_i -- and is clear
+ * elsewhere (never read).  Lets the exchange move only the rows of each rank's screen footprint
+ * (DESIGN.md §6); ranges = NULL means every fragment covers the whole tile. */
+int dprt_composite_ranged(int device, const float* const* inputs, const int64_t* ranges, int P, int64_t npix,
+                          const float bg[3], int flags, uint8_t* rgb8, float* rgba_out, void* stream);
 
 /* Peer memory over NVLink for the fused direct-send compositor (one process per GPU).  Buffers that peers
  * map must come from dprt_device_alloc so the IPC handle covers exactly [ptr, ptr + bytes). */

@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -30,6 +30,7 @@ MARCH_NO_SKIP = 1
 MARCH_FULL_FRAME = 2
 MARCH_BEAM = 4
 MARCH_QUEUE = 8
+MARCH_BAND_CLEAR = 16
 COMPOSITE_TONEMAP = 1
 COMPOSITE_RGBA = 2
 
@@ -39,7 +40,7 @@ EXPORTS = (
     "dprt_brick_generate", "dprt_brick_build_macrocells", "dprt_brick_destroy", "dprt_brick_footprint",
     "dprt_march", "dprt_march_rgb8", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
     "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters", "dprt_kat_slab", "dprt_kat_primary_dirs",
-    "dprt_stage_input",
+    "dprt_stage_input", "dprt_composite_ranged", "dprt_desc_footprint",
 )
 
 c_double3 = ctypes.c_double * 3
@@ -98,6 +99,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_kat_slab": ([I, I, P, P, P, P, P, P], I),
         "dprt_kat_primary_dirs": ([I, P, I, I, P], I),
         "dprt_stage_input": ([I, P, P, ctypes.c_uint64, P], I),
+        "dprt_composite_ranged": ([I, P, P, I, ctypes.c_int64, P, I, P, P, P], I),
+        "dprt_desc_footprint": ([P, P, I, I, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

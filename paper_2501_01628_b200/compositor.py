@@ -30,6 +30,12 @@ from .errors import TransportError, UsageError
 from .transport import RankEndpoint
 
 
+def clip_rows(rows: Tuple[int, int], band: Tuple[int, int]) -> Optional[Tuple[int, int]]:
+    """rows ∩ band, or None when empty."""
+    lo, hi = max(rows[0], band[0]), min(rows[1], band[1])
+    return (lo, hi) if hi > lo else None
+
+
 def assign_rows(height: int, P: int) -> List[Tuple[int, int]]:
     """Row blocks [b*H//P, (b+1)*H//P) -- engine.py:216-221."""
     return [(b * height // P, (b + 1) * height // P) for b in range(P)]
@@ -89,9 +95,9 @@ class CudaBlender:
         dev.composite(frags, None, rgba=out_rgba)
 
     def over_tonemap(self, frags: Sequence[torch.Tensor], background, out_rgb8: torch.Tensor,
-                     out_rgba: Optional[torch.Tensor] = None) -> None:
+                     out_rgba: Optional[torch.Tensor] = None, ranges=None, npix: Optional[int] = None) -> None:
         from . import device as dev
-        dev.composite(frags, background, rgb8=out_rgb8, rgba=out_rgba)
+        dev.composite(frags, background, rgb8=out_rgb8, rgba=out_rgba, ranges=ranges, npix=npix)
 
 
 @dataclass
@@ -146,9 +152,15 @@ class Compositor:
     def _rows(self, flat: torch.Tensor, rows: Tuple[int, int], ch: int) -> torch.Tensor:
         return flat[rows[0] * self.W * ch: rows[1] * self.W * ch]
 
+    def clips_bands(self) -> bool:
+        """True when this mode reads only each rank's footprint row band (``bands`` in composite)."""
+        return self.mode in ("direct_send", "p2p")
+
     # ------------------------------------------------------------------------------------------
     def composite(self, partial: torch.Tensor, order: Sequence[int], background, keep_float: bool = False,
-                  solo: bool = False) -> CompositeOutput:
+                  solo: bool = False, bands: Optional[Sequence[Tuple[int, int]]] = None) -> CompositeOutput:
+        """``bands``: per rank, the rows [y0, y1) outside which its partial is clear (its screen footprint):
+        direct-send and p2p then move and read only those rows."""
         order = list(order)
         if sorted(order) != list(range(self.ep.R)):
             raise UsageError(f"visibility order {order} is not a permutation of {self.ep.R} ranks")
@@ -157,11 +169,13 @@ class Compositor:
             self.shared_partial()  # resolves auto collectively
         if self.mode == "single" or solo:
             return self._single(partial, background, keep_float)
+        if bands is not None and len(bands) != self.ep.R:
+            raise UsageError(f"need one row band per rank, got {len(bands)}")
         if self.mode == "direct_send":
-            return self._direct_send(partial, order, background, keep_float)
+            return self._direct_send(partial, order, background, keep_float, bands)
         if self.mode == "binary_swap":
             return self._binary_swap(partial, order, background, keep_float)
-        return self._p2p_composite(partial, order, background, keep_float)
+        return self._p2p_composite(partial, order, background, keep_float, bands)
 
     def _single(self, partial, background, keep_float) -> CompositeOutput:
         if self.ep.rank != 0:
@@ -202,22 +216,42 @@ class Compositor:
         self.last_bytes += sum(t.numel() * t.element_size() for _, t in sends)
         return CompositeOutput(None, None)
 
-    def _direct_send(self, partial, order, background, keep_float) -> CompositeOutput:
+    def _direct_send(self, partial, order, background, keep_float, bands=None) -> CompositeOutput:
         ep = self.ep
         P, r = ep.R, ep.rank
         plan = direct_send_plan(self.H, P, r)
         rows = plan.own_rows
         n_own = (rows[1] - rows[0]) * self.W
-        inbox = {j: self._buf(f"in{j}", n_own * 4) for j in plan.recvs}
-        sends = [(j, self._rows(partial, rr, 4)) for j, rr in plan.sends if rr[1] > rr[0]]
-        recvs = [(j, inbox[j]) for j in plan.recvs] if n_own else []
+        full = (0, self.H)
+        band = [full] * P if bands is None else list(bands)
+        # every rank derives the same clipped row ranges from the same bands: no sizes are exchanged
+        sends = []
+        for j, rr in plan.sends:
+            c = clip_rows(rr, band[r])
+            if c:
+                sends.append((j, self._rows(partial, c, 4)))
+        clips = {s: clip_rows(rows, band[s]) for s in range(P)}
+        inbox = {s: self._buf(f"in{s}", (clips[s][1] - clips[s][0]) * self.W * 4)[: (clips[s][1] - clips[s][0]) * self.W * 4]
+                 for s in plan.recvs if clips[s]}
+        recvs = [(s, inbox[s]) for s in plan.recvs if clips[s]]
         ep.exchange(sends, recvs)
         self.last_bytes += sum(t.numel() * 4 for _, t in sends)
-        frags = [self._rows(partial, rows, 4) if s == r else inbox[s] for s in order]
+        frags, ranges = [], []
+        for s in order:
+            c = clips[s]
+            if not c:
+                continue  # this rank's footprint misses my rows: its fragment is clear
+            frags.append(self._rows(partial, c, 4) if s == r else inbox[s])
+            ranges.append(((c[0] - rows[0]) * self.W, (c[1] - rows[0]) * self.W))
         tile = self._buf("tile8", n_own * 3, torch.uint8)
         tile_f = self._buf("tilef", n_own * 4) if keep_float else None
         if n_own:
-            self.blender.over_tonemap(frags, background, tile, tile_f)
+            if not frags:  # every fragment clear: the background alone
+                frags, ranges = [self._buf("tilef0", 4)], [(0, 0)]
+            if bands is None:
+                self.blender.over_tonemap(frags, background, tile, tile_f)
+            else:
+                self.blender.over_tonemap(frags, background, tile, tile_f, ranges=ranges, npix=n_own)
         return self._gather_tiles(rows, tile, tile_f, assign_rows(self.H, P), keep_float)
 
     def _binary_swap(self, partial, order, background, keep_float) -> CompositeOutput:
@@ -285,7 +319,7 @@ class Compositor:
             self._p2p_impl = impl
         return self._p2p_impl
 
-    def _p2p_composite(self, partial, order, background, keep_float) -> CompositeOutput:
-        out = self._p2p().composite(partial, order, background, keep_float)
+    def _p2p_composite(self, partial, order, background, keep_float, bands=None) -> CompositeOutput:
+        out = self._p2p().composite(partial, order, background, keep_float, bands)
         self.last_bytes = self._p2p_impl.last_bytes
         return out

@@ -234,17 +234,32 @@ int dprt_brick_destroy(DprtBrick* b) {
     return DPRT_OK;
 }
 
-static void owned_box(const DprtBrick* b, double lo[3], double hi[3]) {
+static void owned_box_desc(const DprtBrickDesc* d, double lo[3], double hi[3]) {
     for (int a = 0; a < 3; ++a) {
-        lo[a] = b->desc.origin[a] + (double)b->desc.lo[a] * b->desc.spacing[a];
-        hi[a] = b->desc.origin[a] + (double)b->desc.hi[a] * b->desc.spacing[a];
+        lo[a] = d->origin[a] + (double)d->lo[a] * d->spacing[a];
+        hi[a] = d->origin[a] + (double)d->hi[a] * d->spacing[a];
     }
 }
+
+static void owned_box(const DprtBrick* b, double lo[3], double hi[3]) { owned_box_desc(&b->desc, lo, hi); }
+
+static int box_footprint(const double lo[3], const double hi[3], const DprtCamera* cam, int W, int H, int32_t rect[4]);
 
 int dprt_brick_footprint(const DprtBrick* b, const DprtCamera* cam, int W, int H, int32_t rect[4]) {
     if (!b || !cam || !rect || W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "bad footprint arguments");
     double lo[3], hi[3];
     owned_box(b, lo, hi);
+    return box_footprint(lo, hi, cam, W, H, rect);
+}
+
+int dprt_desc_footprint(const DprtBrickDesc* desc, const DprtCamera* cam, int W, int H, int32_t rect[4]) {
+    if (!desc || !cam || !rect || W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "bad footprint arguments");
+    double lo[3], hi[3];
+    owned_box_desc(desc, lo, hi);
+    return box_footprint(lo, hi, cam, W, H, rect);
+}
+
+static int box_footprint(const double lo[3], const double hi[3], const DprtCamera* cam, int W, int H, int32_t rect[4]) {
     double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
     bool full = false;
     for (int c = 0; c < 8 && !full; ++c) {
@@ -341,6 +356,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.qorg = b->quad + a.qsz + a.qsy + 1;
     a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
+    a.band_clear = (p->flags & DPRT_MARCH_BAND_CLEAR) ? 1 : 0;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
     if (rgb8) a.beam = 1;  // the fused RGB8 output exists in the beam marcher only
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
@@ -388,8 +404,8 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     return DPRT_OK;
 }
 
-int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, const float bg[3], int flags,
-                   uint8_t* rgb8, float* rgba_out, void* stream) {
+int dprt_composite_ranged(int device, const float* const* inputs, const int64_t* ranges, int P, int64_t npix,
+                          const float bg[3], int flags, uint8_t* rgb8, float* rgba_out, void* stream) {
     if (!inputs || P < 1 || P > DPRT_MAX_PARTS) return fail(DPRT_E_USAGE, "need 1..%d fragments (got %d)", DPRT_MAX_PARTS, P);
     if (npix < 0) return fail(DPRT_E_USAGE, "negative pixel count");
     if ((flags & DPRT_COMPOSITE_TONEMAP) && (!rgb8 || !bg)) return fail(DPRT_E_USAGE, "tone map needs rgb8 and bg");
@@ -400,9 +416,14 @@ int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, 
     dprt::CompositeArgs a;
     memset(&a, 0, sizeof(a));
     for (int i = 0; i < P; ++i) {
-        if (!inputs[i]) return fail(DPRT_E_USAGE, "fragment %d is null", i);
+        const int64_t lo = ranges ? ranges[2 * i] : 0, hi = ranges ? ranges[2 * i + 1] : npix;
+        if (lo < 0 || hi > npix || lo > hi) return fail(DPRT_E_USAGE, "fragment %d range [%lld, %lld) outside [0, %lld)",
+                                                        i, (long long)lo, (long long)hi, (long long)npix);
+        if (hi > lo && !inputs[i]) return fail(DPRT_E_USAGE, "fragment %d is null", i);
         if (reinterpret_cast<uintptr_t>(inputs[i]) & 15) return fail(DPRT_E_USAGE, "fragment %d not 16-byte aligned", i);
         a.in[i] = reinterpret_cast<const float4*>(inputs[i]);
+        a.lo[i] = lo;
+        a.hi[i] = hi;
     }
     a.P = P;
     a.npix = npix;
@@ -416,6 +437,11 @@ int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, 
     a.rgba = reinterpret_cast<float4*>(rgba_out);
     CK(dprt::launch_composite(a, (cudaStream_t)stream), "composite kernel launch");
     return DPRT_OK;
+}
+
+int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, const float bg[3], int flags,
+                   uint8_t* rgb8, float* rgba_out, void* stream) {
+    return dprt_composite_ranged(device, inputs, nullptr, P, npix, bg, flags, rgb8, rgba_out, stream);
 }
 
 int dprt_march_counters(int device, uint64_t out[4], int reset) {

@@ -69,6 +69,7 @@ struct MarchArgs {
     const uint8_t* __restrict__ skipd;
     int mcd[3];
     int skip;
+    int band_clear;  // clear only the footprint's row band of the partial (DPRT_MARCH_BAND_CLEAR)
     int beam;  // 1: march_beam_kernel (warp beams, per-pixel ray records); 0: ray queue + march_kernel
     // transfer function
     const float4* __restrict__ tf;
@@ -87,7 +88,8 @@ struct MarchArgs {
 };
 
 struct CompositeArgs {
-    const float4* in[DPRT_MAX_PARTS];
+    const float4* in[DPRT_MAX_PARTS];  // fragment i's element for tile pixel p is in[i][p - lo[i]]
+    long long lo[DPRT_MAX_PARTS], hi[DPRT_MAX_PARTS];  // tile pixels [lo, hi) fragment i covers (else clear)
     int P;
     long long npix;
     float bg[3];

@@ -33,24 +33,32 @@ __device__ __forceinline__ uint32_t pack_rgb8(const float4 c, const float bg[3],
 
 // Each thread composites 4 consecutive pixels: per fragment it issues the four 16-byte loads together
 // (and the next fragment's before blending, via unrolling), so P fragments keep 4-8 loads in flight;
-// the 12 RGB8 bytes leave as three aligned 32-bit stores.
+// the 12 RGB8 bytes leave as three aligned 32-bit stores.  A fragment covers only the tile pixels
+// [lo, hi) (a rank's footprint rows): outside them it is clear and is not read at all.
 __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long i0 = q * 4;
     if (i0 >= a.npix) return;
     if (i0 + 4 <= a.npix) {
         float4 acc[4];
-        const float4* f0 = a.in[0] + i0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k] = __ldg(f0 + k);
+        for (int k = 0; k < 4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 2
-        for (int p = 1; p < a.P; ++p) {
-            const float4* fp = a.in[p] + i0;
-            float4 f[4];
+        for (int p = 0; p < a.P; ++p) {
+            const long long lo = a.lo[p], hi = a.hi[p];
+            if (i0 + 4 <= lo || i0 >= hi) continue;  // clear here: nothing to read
+            const float4* fp = a.in[p] + (i0 - lo);
+            if (i0 >= lo && i0 + 4 <= hi) {
+                float4 f[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) f[k] = __ldg(fp + k);
+                for (int k = 0; k < 4; ++k) f[k] = __ldg(fp + k);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) over(acc[k], f[k]);
+                for (int k = 0; k < 4; ++k) over(acc[k], f[k]);
+            } else {  // a range edge inside this group of 4 (frame width not a multiple of 4)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (i0 + k >= lo && i0 + k < hi) over(acc[k], __ldg(fp + k));
+            }
         }
         if (a.flags & DPRT_COMPOSITE_RGBA) {
 #pragma unroll
@@ -77,8 +85,9 @@ __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
     }
     // tail: fewer than 4 pixels left
     for (long long i = i0; i < a.npix; ++i) {
-        float4 acc = __ldg(a.in[0] + i);
-        for (int p = 1; p < a.P; ++p) over(acc, __ldg(a.in[p] + i));
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int p = 0; p < a.P; ++p)
+            if (i >= a.lo[p] && i < a.hi[p]) over(acc, __ldg(a.in[p] + (i - a.lo[p])));
         if (a.flags & DPRT_COMPOSITE_RGBA) a.rgba[i] = acc;
         if (a.flags & DPRT_COMPOSITE_TONEMAP)
             for (int ch = 0; ch < 3; ++ch) a.rgb8[3 * i + ch] = (uint8_t)pack_rgb8(acc, a.bg, ch);

@@ -793,6 +793,10 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
             fill_rgb8_kernel<<<(unsigned)((quads + 255) / 256), 256, 0, stream>>>(a.rgb8, (long long)a.W * a.H,
                                                                               a.bg[0], a.bg[1], a.bg[2]);
             e = cudaGetLastError();
+        } else if (a.band_clear) {
+            // the caller reads only the footprint's row band (band-clipped compositing)
+            e = cudaMemsetAsync(a.out + (size_t)a.rect[1] * a.W, 0,
+                                (size_t)(a.rect[3] - a.rect[1]) * a.W * sizeof(float4), stream);
         } else {
             e = cudaMemsetAsync(a.out, 0, (size_t)a.W * a.H * sizeof(float4), stream);
         }

@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import itertools
 import os
-from typing import Optional, Sequence
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -32,6 +32,27 @@ def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype) -> None:
         raise UsageError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise UsageError(f"{name} must be contiguous")
+
+
+def desc_struct(desc: BrickDesc) -> _lib.BrickDesc:
+    d = _lib.BrickDesc()
+    d.dims[:] = list(desc.dims)
+    d.lo[:] = list(desc.lo)
+    d.hi[:] = list(desc.hi)
+    d.ghost = desc.ghost
+    d.origin[:] = [float(v) for v in desc.origin]
+    d.spacing[:] = [float(v) for v in desc.spacing]
+    return d
+
+
+def desc_footprint(desc: BrickDesc, cam: CameraSpec, width: int, height: int) -> Tuple[int, int, int, int]:
+    """Screen rectangle [x0, y0, x1, y1) of a brick's owned box (host-only: any rank, any brick)."""
+    rect = (ctypes.c_int32 * 4)()
+    c = camera_struct(cam)
+    d = desc_struct(desc)
+    _lib.check(_lib.lib().dprt_desc_footprint(ctypes.byref(d), ctypes.byref(c), width, height, rect),
+               "dprt_desc_footprint")
+    return tuple(rect)
 
 
 def camera_struct(cam: CameraSpec) -> _lib.Camera:
@@ -60,13 +81,7 @@ class DeviceBrick:
         self.desc = desc
         self.device = device
         self.index = device.index if device.index is not None else torch.cuda.current_device()
-        d = _lib.BrickDesc()
-        d.dims[:] = list(desc.dims)
-        d.lo[:] = list(desc.lo)
-        d.hi[:] = list(desc.hi)
-        d.ghost = desc.ghost
-        d.origin[:] = [float(v) for v in desc.origin]
-        d.spacing[:] = [float(v) for v in desc.spacing]
+        d = desc_struct(desc)
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().dprt_brick_create(self.index, ctypes.byref(d), ctypes.byref(h)), "dprt_brick_create")
         self._h = h
@@ -204,8 +219,9 @@ class DeviceTF:
 
 def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, partial: torch.Tensor,
           width: int, height: int, samples: Optional[torch.Tensor] = None, skip: bool = True,
-          footprint: bool = True) -> None:
-    """dprt_march: the brick's full-frame premultiplied RGBA partial into ``partial`` (H*W*4 f32)."""
+          footprint: bool = True, band_clear: bool = False) -> None:
+    """dprt_march: the brick's full-frame premultiplied RGBA partial into ``partial`` (H*W*4 f32).
+    ``band_clear``: only the footprint's row band is defined afterwards (band-clipped compositing)."""
     _require_cuda(partial, "partial", torch.float32)
     if partial.numel() != width * height * 4:
         raise UsageError(f"partial holds {partial.numel()} floats, need {width * height * 4}")
@@ -216,6 +232,8 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
             raise UsageError("samples buffer must hold one count per pixel")
         sp = ctypes.c_void_p(samples.data_ptr())
     flags = (0 if skip else _lib.MARCH_NO_SKIP) | (0 if footprint else _lib.MARCH_FULL_FRAME)
+    if band_clear:
+        flags |= _lib.MARCH_BAND_CLEAR
     variant = os.environ.get("DPRT_MARCHER", "")
     if variant == "beam":
         flags |= _lib.MARCH_BEAM
@@ -248,19 +266,31 @@ def march_rgb8(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert
 
 
 def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[torch.Tensor] = None,
-              rgba: Optional[torch.Tensor] = None) -> None:
-    """dprt_composite: front-to-back 'over' of equally sized RGBA fragments (already in visibility
-    order); writes tone-mapped RGB8 (needs ``background``) and/or the blended RGBA."""
+              rgba: Optional[torch.Tensor] = None, ranges: Optional[Sequence[Tuple[int, int]]] = None,
+              npix: Optional[int] = None) -> None:
+    """dprt_composite: front-to-back 'over' of RGBA fragments (already in visibility order); writes
+    tone-mapped RGB8 (needs ``background``) and/or the blended RGBA.  Without ``ranges`` the fragments
+    are equally sized and cover the whole tile; with ``ranges`` fragment i holds only the tile pixels
+    [lo_i, hi_i) (clear elsewhere) and ``npix`` is the tile size (dprt_composite_ranged)."""
     if not frags:
         raise UsageError("nothing to composite")
-    n = frags[0].numel()
-    if n % 4:
-        raise UsageError("fragments must hold whole RGBA pixels")
-    for i, f in enumerate(frags):
-        _require_cuda(f, f"fragment {i}", torch.float32)
-        if f.numel() != n:
-            raise UsageError("fragments differ in size")
-    npix = n // 4
+    if ranges is None:
+        n = frags[0].numel()
+        if n % 4:
+            raise UsageError("fragments must hold whole RGBA pixels")
+        for i, f in enumerate(frags):
+            _require_cuda(f, f"fragment {i}", torch.float32)
+            if f.numel() != n:
+                raise UsageError("fragments differ in size")
+        npix = n // 4
+    else:
+        if npix is None or len(ranges) != len(frags):
+            raise UsageError("ranged composite needs npix and one (lo, hi) range per fragment")
+        for i, (f, (lo, hi)) in enumerate(zip(frags, ranges)):
+            _require_cuda(f, f"fragment {i}", torch.float32)
+            if f.numel() < 4 * (hi - lo):
+                raise UsageError(f"fragment {i} holds {f.numel() // 4} pixels, range needs {hi - lo}")
+        n = npix * 4
     flags = 0
     bg_arr = None
     rgb_ptr = ctypes.c_void_p(0)
@@ -282,21 +312,24 @@ def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[tor
         flags |= _lib.COMPOSITE_RGBA
         rgba_ptr = ctypes.c_void_p(rgba.data_ptr())
     ptrs = (ctypes.c_void_p * len(frags))(*[f.data_ptr() for f in frags])
+    rng = None if ranges is None else (ctypes.c_int64 * (2 * len(ranges)))(*[int(v) for r in ranges for v in r])
     dev = frags[0].device
-    rc = _lib.lib().dprt_composite(dev.index if dev.index is not None else torch.cuda.current_device(), ptrs,
-                                   len(frags), npix, bg_arr, flags, rgb_ptr, rgba_ptr, _stream(dev))
+    rc = _lib.lib().dprt_composite_ranged(dev.index if dev.index is not None else torch.cuda.current_device(), ptrs,
+                                          rng, len(frags), npix, bg_arr, flags, rgb_ptr, rgba_ptr, _stream(dev))
     _lib.check(rc, "dprt_composite")
 
 
 def composite_ptrs(device_index: int, ptrs: Sequence[int], npix: int, background, rgb8_ptr: int = 0,
-                   rgba_ptr: int = 0, stream: Optional[int] = None) -> None:
+                   rgba_ptr: int = 0, stream: Optional[int] = None,
+                   ranges: Optional[Sequence[Tuple[int, int]]] = None) -> None:
     """Raw-pointer form for peer (IPC-mapped) fragments and outputs: the fused NVLink compositor."""
     flags = (_lib.COMPOSITE_TONEMAP if rgb8_ptr else 0) | (_lib.COMPOSITE_RGBA if rgba_ptr else 0)
     bg_arr = (ctypes.c_float * 3)(*[float(c) for c in background]) if background is not None else None
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    rng = None if ranges is None else (ctypes.c_int64 * (2 * len(ranges)))(*[int(v) for r in ranges for v in r])
     s = ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream(device_index).cuda_stream)
-    rc = _lib.lib().dprt_composite(device_index, arr, len(ptrs), npix, bg_arr, flags, ctypes.c_void_p(rgb8_ptr),
-                                   ctypes.c_void_p(rgba_ptr), s)
+    rc = _lib.lib().dprt_composite_ranged(device_index, arr, rng, len(ptrs), npix, bg_arr, flags,
+                                          ctypes.c_void_p(rgb8_ptr), ctypes.c_void_p(rgba_ptr), s)
     _lib.check(rc, "dprt_composite")
 
 

@@ -62,6 +62,8 @@ class RenderOptions:
     keep_float: bool = False           # also return the float RGB image before quantisation (rank 0)
     collect_samples: bool = False      # also return per-pixel owned sample counts (this rank)
     mode: str = "dvr"                  # "dvr" or "rankcolor" (rank-ownership visualisation, engine.py:327-332)
+    clip_exchange: bool = True         # direct-send / p2p move only each rank's footprint rows;
+                                       # RenderResult.partial is then defined only inside this rank's band
 
 
 @dataclass
@@ -126,6 +128,7 @@ def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptio
         "size": [width, height],
         "dt": options.dt, "ert": options.ert, "composite": options.composite,
         "skip": options.skip_empty, "disableCompositing": options.disable_compositing, "mode": options.mode,
+        "clipExchange": options.clip_exchange,
         "tf": [_tf_hash(tf), tf.vmin, tf.vmax],
         "field": [list(f.dims), list(f.origin), list(f.spacing)],
         "bricks": [[list(lo), list(hi)] for lo, hi in decomposition.boxes],
@@ -172,6 +175,8 @@ class VolumeRenderer:
         self._fused_events = [None] * FUSED_SLOTS
         self._fused_next = 0
         self._fused_slot = 0
+        self._band_key = None
+        self._band_cache = None
 
     def set_tf(self, tf: TransferFunction1D) -> None:
         self.tf = tf
@@ -187,6 +192,16 @@ class VolumeRenderer:
             shared = self.compositor.shared_partial()
             self.partial = shared if shared is not None else torch.empty(height * width * 4, dtype=torch.float32,
                                                                           device=self.device)
+
+    def _bands(self, cam: CameraSpec, width: int, height: int):
+        """Every rank's footprint row band [y0, y1) (host geometry, identical on all ranks; cached)."""
+        key = (cam, width, height)
+        if self._band_key != key:
+            dec = self.decomposition
+            self._band_cache = [tuple(dev.desc_footprint(dec.brick(s), cam, width, height)[1::2])
+                                for s in range(self.ep.R)]
+            self._band_key = key
+        return self._band_cache
 
     def render(self, cam: CameraSpec, width: int, height: int, options: RenderOptions = RenderOptions(),
                verify: bool = True) -> RenderResult:
@@ -231,8 +246,13 @@ class VolumeRenderer:
             if options.collect_samples:
                 res.samples = self.samples.view(height, width)
             return res
+        bands = None
+        if options.clip_exchange and self.ep.R > 1 and not options.disable_compositing and \
+                self.compositor.clips_bands():
+            bands = self._bands(cam, width, height)
         dev.march(self.brick, cam, dtf, options.dt, options.ert, self.partial, width, height,
-                  samples=self.samples if options.collect_samples else None, skip=options.skip_empty)
+                  samples=self.samples if options.collect_samples else None, skip=options.skip_empty,
+                  band_clear=bands is not None)
         if options.disable_compositing:
             order = [self.ep.rank] if self.ep.R == 1 else order
         if self._pending_copy is not None:
@@ -240,7 +260,7 @@ class VolumeRenderer:
             torch.cuda.current_stream(self.device).wait_event(self._pending_copy)
             self._pending_copy = None
         out = self.compositor.composite(self.partial, order, self.background,
-                                        keep_float=options.keep_float, solo=options.disable_compositing)
+                                        keep_float=options.keep_float, solo=options.disable_compositing, bands=bands)
         nbytes = self.compositor.last_bytes
         stats.bytes_exchanged += nbytes
         stats.record(options.frame_index, width * height, nbytes, (time.perf_counter() - t0) * 1e3)

@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import torch
 
 from . import device as dev
-from .compositor import CompositeOutput, assign_rows
+from .compositor import CompositeOutput, assign_rows, clip_rows
 from .transport import RankEndpoint
 
 
@@ -63,8 +63,8 @@ class P2PCompositor:
             self.frame_rgba = dev.DeviceBuffer(self.device, self.W * self.H * 4)
         self.root_rgba = self.ep.share_pointers(self.index, self.frame_rgba.ptr if self.frame_rgba else 0)[0]
 
-    def composite(self, partial: torch.Tensor, order: Sequence[int], background, keep_float: bool = False
-                  ) -> CompositeOutput:
+    def composite(self, partial: torch.Tensor, order: Sequence[int], background, keep_float: bool = False,
+                  bands=None) -> CompositeOutput:
         ep = self.ep
         if keep_float:
             self._ensure_rgba()
@@ -75,11 +75,27 @@ class P2PCompositor:
         npix = (rows[1] - rows[0]) * self.W
         if npix:
             off = rows[0] * self.W
-            ptrs = [self.peer_partials[s] + 16 * off for s in order]
+            if bands is None:
+                ptrs = [self.peer_partials[s] + 16 * off for s in order]
+                ranges = None
+            else:  # read each peer only inside its footprint rows (the rest of its partial is clear)
+                ptrs, ranges = [], []
+                for s in order:
+                    c = clip_rows(rows, bands[s])
+                    if c:
+                        ptrs.append(self.peer_partials[s] + 16 * c[0] * self.W)
+                        ranges.append(((c[0] - rows[0]) * self.W, (c[1] - rows[0]) * self.W))
+                if not ptrs:
+                    ptrs, ranges = [self.peer_partials[ep.rank]], [(0, 0)]
             dev.composite_ptrs(self.index, ptrs, npix, background, rgb8_ptr=self.root_frame + 3 * off,
-                               rgba_ptr=(self.root_rgba + 16 * off) if keep_float else 0)
+                               rgba_ptr=(self.root_rgba + 16 * off) if keep_float else 0, ranges=ranges)
         ep.device_barrier()  # every tile has landed in rank 0's frame
-        self.last_bytes = 16 * npix * (ep.R - 1) + (3 * npix if ep.rank else 0)
+        if bands is None:
+            self.last_bytes = 16 * npix * (ep.R - 1) + (3 * npix if ep.rank else 0)
+        else:
+            read = sum((c[1] - c[0]) * self.W for s in range(ep.R) if s != ep.rank
+                       for c in [clip_rows(rows, bands[s])] if c)
+            self.last_bytes = 16 * read + (3 * npix if ep.rank else 0)
         if ep.rank != 0:
             return CompositeOutput(None, None)
         frame = self.frame.tensor.view(self.H, self.W, 3)

@@ -30,7 +30,14 @@ class TorchBlender:
     def over(self, frags, out_rgba):
         out_rgba.view(-1, 4).copy_(self._over(frags))
 
-    def over_tonemap(self, frags, background, out_rgb8, out_rgba=None):
+    def over_tonemap(self, frags, background, out_rgb8, out_rgba=None, ranges=None, npix=None):
+        if ranges is not None:  # ranged fragments: clear outside [lo, hi) of the tile
+            full = []
+            for f, (lo, hi) in zip(frags, ranges):
+                t = torch.zeros(npix * 4, dtype=torch.float32)
+                t[lo * 4: hi * 4] = f.view(-1)[: (hi - lo) * 4]
+                full.append(t)
+            frags = full
         acc = self._over(frags)
         bg = torch.tensor(background, dtype=torch.float32)
         rgb = acc[:, :3] + (1.0 - acc[:, 3:4]) * bg
@@ -81,6 +88,42 @@ def test_exchange_matches_oracle(mode, P):
     # fragment bytes per non-root rank: (1 - 1/P) of the frame in RGBA f32 + its RGB8 (+RGBA) tile to root
     for r in range(1, P):
         assert res[r][1] > 0
+
+
+def _banded_body(ep, W, H, order, bg, bands):
+    parts = _partials(ep.R, W, H)
+    for s, (y0, y1) in enumerate(bands):  # each rank's partial is clear outside its footprint rows
+        parts[s, :y0] = 0.0
+        parts[s, y1:] = 0.0
+    mine = torch.from_numpy(parts[ep.rank].reshape(-1).copy())
+    comp = Compositor(ep, W, H, "direct_send", torch.device("cpu"), blender=TorchBlender())
+    out = comp.composite(mine, order, bg, keep_float=True, bands=bands)
+    clipped = comp.last_bytes
+    full = comp.composite(mine, order, bg, keep_float=True)
+    if ep.rank == 0:
+        return out.rgb8.numpy().copy(), out.rgba.numpy().copy(), full.rgba.numpy().copy(), clipped, comp.last_bytes
+    return None, None, None, clipped, comp.last_bytes
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_band_clipped_direct_send_equals_full_exchange(P):
+    """Band-clipped direct-send (only footprint rows move) gives the same frame as the full exchange and
+    sends fewer bytes; bands may be empty, cover everything, or miss whole row blocks."""
+    W, H = 20, 23
+    bands = [(3, 11), (0, 23), (9, 9), (15, 23)][:P]
+    order = list(reversed(range(P)))
+    bg = (0.1, 0.2, 0.3)
+    res = run_ranks(P, _banded_body, W, H, order, bg, bands)
+    rgb8, rgba, rgba_full, _, _ = res[0]
+    assert np.array_equal(rgba, rgba_full)
+    parts = _partials(P, W, H).astype(np.float64)
+    for s, (y0, y1) in enumerate(bands):
+        parts[s, :y0] = 0.0
+        parts[s, y1:] = 0.0
+    ref = oracle.composite(list(parts), order, bg)
+    img = rgba.reshape(H, W, 4).astype(np.float64)
+    assert np.abs(img[..., :3] + (1 - img[..., 3:4]) * np.asarray(bg) - ref).max() < 1e-5
+    assert sum(r[3] for r in res) < sum(r[4] for r in res)
 
 
 def test_direct_send_plan_covers_every_block_once():

@@ -55,6 +55,29 @@ def test_sort_last_frame_matches_oracle(cuda_device, oracle_lib, mode, R):
                 assert image is None and rgb8 is None
 
 
+@pytest.mark.parametrize("mode,R", [("direct_send", 4), ("p2p", 3), ("binary_swap", 2)])
+def test_band_clipped_exchange_is_bit_identical(cuda_device, mode, R):
+    """clip_exchange (only footprint rows move, partials cleared only inside their bands) changes the
+    bytes exchanged, never the frame: RGB8 and float frames equal the unclipped exchange bit for bit."""
+    s = c1(P=R, W=176, H=130)
+
+    def body(ep):
+        b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda_device).generate(s.field)
+        vr = VolumeRenderer(ep, b, s.dec, s.tf, s.background)
+        out = []
+        for clip in (False, True, False):
+            res = vr.render(s.cam, s.W, s.H, RenderOptions(composite=mode, keep_float=True, clip_exchange=clip))
+            torch.cuda.synchronize()
+            out.append((None if res.rgb8 is None else res.rgb8.cpu().numpy(), res.image, res.stats.bytes_exchanged))
+        return out
+
+    res = run_collective(R, body, device=cuda_device)
+    (a8, af, ab), (b8, bf, bb), (c8, cf, _) = res[0]
+    assert np.array_equal(a8, b8) and np.array_equal(af, bf) and np.array_equal(a8, c8)
+    if mode != "binary_swap":
+        assert sum(r[1][2] for r in res) < sum(r[0][2] for r in res)
+
+
 def test_disable_compositing_shows_only_root_brick(cuda_device, oracle_lib):
     """Negative test (engine.py:172 analog): without compositing the frame is rank 0's brick alone."""
     s = c1(P=2, W=96, H=96)

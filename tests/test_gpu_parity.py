@@ -125,6 +125,36 @@ def test_composite_kernel_random_partials(cuda_device, oracle_lib):
     assert np.abs(q - oracle.tone_map_rgb8(ref).astype(np.int16)).max() <= 1
 
 
+def test_ranged_composite_kernel(cuda_device, oracle_lib):
+    """dprt_composite_ranged: fragments clear outside [lo, hi) (edges not multiples of 4, empty and full
+    ranges) equal the full-size composite of the zero-padded fragments, bit for bit."""
+    rng = np.random.default_rng(12)
+    P, npix = 6, 4097 * 3 + 2
+    a = rng.uniform(0, 0.5, (P, npix, 1))
+    parts = np.concatenate([rng.uniform(0, 1, (P, npix, 3)) * a, a], axis=2).astype(np.float32)
+    ranges = [(0, npix), (5, 4001), (4001, 4001), (1234, npix), (0, 7), (333, 9998)]
+    padded = np.zeros_like(parts)
+    for i, (lo, hi) in enumerate(ranges):
+        padded[i, lo:hi] = parts[i, lo:hi]
+    bg = (0.2, 0.3, 0.4)
+    full = [torch.from_numpy(padded[i].reshape(-1)).to(cuda_device) for i in range(P)]
+    clip = [torch.from_numpy(parts[i, lo:hi].reshape(-1).copy() if hi > lo else np.zeros(4, np.float32)).to(cuda_device)
+            for i, (lo, hi) in enumerate(ranges)]
+    out = []
+    for frags, rg in ((full, None), (clip, ranges)):
+        rgb8 = torch.empty(npix * 3, dtype=torch.uint8, device=cuda_device)
+        rgba = torch.empty(npix * 4, dtype=torch.float32, device=cuda_device)
+        dev.composite(frags, bg, rgb8=rgb8, rgba=rgba, ranges=rg, npix=npix)
+        torch.cuda.synchronize()
+        out.append((rgb8.cpu().numpy(), rgba.cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    from paper_2501_01628_b200.errors import UsageError
+
+    with pytest.raises(UsageError, match="range"):
+        dev.composite(clip, bg, rgb8=torch.empty(npix * 3, dtype=torch.uint8, device=cuda_device),
+                      ranges=[(0, npix + 1)] + ranges[1:], npix=npix)
+
+
 def test_engine_single_rank_frame(cuda_device, oracle_lib):
     """The public per-rank driver at R=1 (render_with slot): RGB8 frame + float image vs oracle."""
     s = c1(P=1, W=160, H=120)
