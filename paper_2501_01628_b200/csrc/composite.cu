@@ -46,19 +46,20 @@ __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
 #pragma unroll 2
         for (int p = 0; p < a.P; ++p) {
             const long long lo = a.lo[p], hi = a.hi[p];
-            if (i0 + 4 <= lo || i0 >= hi) continue;  // clear here: nothing to read
             const float4* fp = a.in[p] + (i0 - lo);
+            float4 f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) f[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // clear: over adds exact 0
             if (i0 >= lo && i0 + 4 <= hi) {
-                float4 f[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) f[k] = __ldg(fp + k);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) over(acc[k], f[k]);
-            } else {  // a range edge inside this group of 4 (frame width not a multiple of 4)
+            } else if (i0 + 4 > lo && i0 < hi) {  // a range edge inside this group (width not a multiple of 4)
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (i0 + k >= lo && i0 + k < hi) over(acc[k], __ldg(fp + k));
+                    if (i0 + k >= lo && i0 + k < hi) f[k] = __ldg(fp + k);
             }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) over(acc[k], f[k]);
         }
         if (a.flags & DPRT_COMPOSITE_RGBA) {
 #pragma unroll
