@@ -64,6 +64,7 @@ class RenderOptions:
     mode: str = "dvr"                  # "dvr" or "rankcolor" (rank-ownership visualisation, engine.py:327-332)
     clip_exchange: bool = True         # direct-send / p2p move only each rank's footprint rows;
                                        # RenderResult.partial is then defined only inside this rank's band
+    timing: bool = False               # CUDA events around march and composite (RankStats.device_times())
 
 
 @dataclass
@@ -74,6 +75,27 @@ class RankStats:
     bytes_exchanged: int = 0
     rounds: int = 0
     records: List[str] = field(default_factory=list)
+    events: Optional[tuple] = None     # (march start, march end, composite end) with RenderOptions.timing
+    brick_bytes: int = 0
+    _samples_dev: Optional[torch.Tensor] = None
+
+    def device_times(self) -> dict:
+        """Device milliseconds of this rank's march and composite (waits for them) and the march's
+        whole-brick byte rate; needs RenderOptions.timing."""
+        if self.events is None:
+            raise UsageError("render with RenderOptions(timing=True) to time the kernels")
+        e0, e1, e2 = self.events
+        e2.synchronize()
+        march = e0.elapsed_time(e1)
+        return {"march_ms": march, "composite_ms": e1.elapsed_time(e2),
+                "brick_GBps": self.brick_bytes / (march * 1e-3) / 1e9 if march > 0 else None}
+
+    def owned_samples(self) -> int:
+        """Owned lattice samples of this rank's brick in the frame (needs collect_samples; waits)."""
+        if self._samples_dev is not None:
+            self.samples = int(self._samples_dev.sum(dtype=torch.int64).item())
+            self._samples_dev = None
+        return self.samples
 
     def record(self, frame: int, rays: int, nbytes: int, millis: float, **extra) -> None:
         tail = "".join(f" {k}={v}" for k, v in extra.items())
@@ -224,6 +246,11 @@ class VolumeRenderer:
         self._ensure(width, height, options.composite)
         order = visibility_order(self.decomposition, cam.position)
         t0 = time.perf_counter()
+        ev = None
+        if options.timing:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(torch.cuda.current_stream(self.device))
+            stats.brick_bytes = self.brick.desc.stored_bytes
         if self.ep.R == 1 and not options.keep_float and os.environ.get("DPRT_FUSED_SINGLE", "1") != "0":
             # one rank: the composite is just over-background + tone map -> fused into the march
             # a ring of device frames so the read-backs of frames k-1, k-2 overlap the march of frame k
@@ -241,10 +268,15 @@ class VolumeRenderer:
             dev.march_rgb8(self.brick, cam, dtf, options.dt, options.ert, self.background, frame.view(-1),
                            width, height, samples=self.samples if options.collect_samples else None,
                            skip=options.skip_empty)
+            if ev is not None:
+                ev[1].record(torch.cuda.current_stream(self.device))
+                ev[2].record(torch.cuda.current_stream(self.device))
+                stats.events = tuple(ev)
             stats.record(options.frame_index, width * height, 0, (time.perf_counter() - t0) * 1e3)
             res = RenderResult(rgb8=frame, stats=stats, order=order)
             if options.collect_samples:
                 res.samples = self.samples.view(height, width)
+                stats._samples_dev = res.samples
             return res
         bands = None
         if options.clip_exchange and self.ep.R > 1 and not options.disable_compositing and \
@@ -253,6 +285,8 @@ class VolumeRenderer:
         dev.march(self.brick, cam, dtf, options.dt, options.ert, self.partial, width, height,
                   samples=self.samples if options.collect_samples else None, skip=options.skip_empty,
                   band_clear=bands is not None)
+        if ev is not None:
+            ev[1].record(torch.cuda.current_stream(self.device))
         if options.disable_compositing:
             order = [self.ep.rank] if self.ep.R == 1 else order
         if self._pending_copy is not None:
@@ -261,6 +295,9 @@ class VolumeRenderer:
             self._pending_copy = None
         out = self.compositor.composite(self.partial, order, self.background,
                                         keep_float=options.keep_float, solo=options.disable_compositing, bands=bands)
+        if ev is not None:
+            ev[2].record(torch.cuda.current_stream(self.device))
+            stats.events = tuple(ev)
         nbytes = self.compositor.last_bytes
         stats.bytes_exchanged += nbytes
         stats.record(options.frame_index, width * height, nbytes, (time.perf_counter() - t0) * 1e3)
@@ -272,6 +309,7 @@ class VolumeRenderer:
             res.image = rgba[..., :3] + (1.0 - rgba[..., 3:4]) * bg
         if options.collect_samples:
             res.samples = self.samples.view(height, width)
+            stats._samples_dev = res.samples
         return res
 
     def render_to_host(self, cam: CameraSpec, width: int, height: int, host: Optional[torch.Tensor],

@@ -325,3 +325,23 @@ def test_tf_update_through_pinned_staging_matches_oracle(cuda_device, oracle_lib
         ref, _ = oracle_partials(vox, dec, cam, tf, 1.0, 0.99, W, H)
         _check_rgba(p.view(H, W, 4).cpu().numpy(), ref[0], f"staged TF n={tf.n}")
     b.close()
+
+
+def test_render_stats_device_times_and_samples(cuda_device, oracle_lib):
+    """RenderOptions(timing=True) / collect_samples fill RankStats' device timings and the owned sample
+    total (the reference's per-rank counters, engine.py:177-193, extended for DVR)."""
+    s = c1(P=1, W=96, H=80)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    _, rs = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H)
+    b = dev.DeviceBrick(s.dec.brick(0), cuda_device).generate(s.field)
+    vr = VolumeRenderer(SoloEndpoint(cuda_device), b, s.dec, s.tf, s.background)
+    for keep in (False, True):  # fused single-rank path and march + composite path
+        res = vr.render(s.cam, s.W, s.H, RenderOptions(timing=True, collect_samples=True, keep_float=keep))
+        t = res.stats.device_times()
+        assert t["march_ms"] > 0 and t["composite_ms"] >= 0 and t["brick_GBps"] > 0
+        assert res.stats.owned_samples() == int(rs[0].sum())
+    from paper_2501_01628_b200.errors import UsageError
+
+    with pytest.raises(UsageError, match="timing"):
+        vr.render(s.cam, s.W, s.H, RenderOptions()).stats.device_times()
+    b.close()
