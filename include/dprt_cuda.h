@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 4
+#define DPRT_ABI_VERSION 5
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -84,6 +84,8 @@ typedef struct DprtMarchParams {
     double dt;
     double ert;
     uint64_t tf_version;
+    int32_t row0, row1; /* row1 > row0: march only pixel rows [row0, row1); partial_rgba and samples then
+                           hold just those rows (pixel (x, y) at index (y - row0) * W + x).  0, 0: all rows */
 } DprtMarchParams;
 
 #define DPRT_MARCH_NO_SKIP 1      /* disable exact empty-space skipping (macrocell skip distances) */
@@ -92,6 +94,9 @@ typedef struct DprtMarchParams {
 #define DPRT_MARCH_QUEUE 8        /* force the ray-queue marcher (persistent warps, per-lane refill) */
 #define DPRT_MARCH_BAND_CLEAR 16  /* beam marcher: clear only the footprint's row band of the partial; rows
                                      outside it are left as they were (for band-clipped compositing) */
+#define DPRT_MARCH_ACCUM 32       /* ray cycling: partial_rgba holds each ray's accumulated front-to-back
+                                     state; the march continues from it (ERT on the accumulated alpha, rays
+                                     already at ERT are skipped) and writes it back; nothing is cleared */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
 #define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */

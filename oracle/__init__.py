@@ -17,6 +17,7 @@ from .dvr import (  # noqa: F401
     build_oracle,
     camera_array,
     composite,
+    cycle_frame,
     det_cos,
     generate_field,
     generate_ml,
@@ -27,6 +28,7 @@ from .dvr import (  # noqa: F401
     max_threads,
     primary_dirs,
     render_brick,
+    render_brick_accum,
     sample_counts,
     slab,
     tone_map_rgb8,

@@ -19,7 +19,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_build" / "libdvr_oracle.so"
-_ABI = 5
+_ABI = 6
 
 _lib = None
 
@@ -64,6 +64,10 @@ def load_oracle():
         ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
         ctypes.c_int]
     lib.dvr_oracle_render_brick.restype = ctypes.c_int
+    lib.dvr_oracle_render_brick_accum.argtypes = [
+        P, P, P, P, P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+        ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
+    lib.dvr_oracle_render_brick_accum.restype = ctypes.c_int
     lib.dvr_oracle_max_threads.restype = ctypes.c_int
     lib.dvr_oracle_sample_counts.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_int, P, ctypes.c_int]
     _lib = lib
@@ -235,6 +239,57 @@ def render_brick(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.nd
     if rc != 0:
         raise ValueError(f"oracle render_brick failed with code {rc}")
     return out, samples
+
+
+def render_brick_accum(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.ndarray, vmin: float,
+                       vmax: float, dt: float, ert: float, width: int, height: int, state: np.ndarray,
+                       rows: Tuple[int, int], nthreads: int = 0) -> None:
+    """Ray cycling: continue the accumulated state (H, W, 4) f64 of rows [r0, r1) through
+    one brick, in place (ERT on the accumulated alpha)."""
+    vox = np.ascontiguousarray(vox, np.float32)
+    if tuple(vox.shape) != tuple(reversed(brick.stored_dims)):
+        raise ValueError(f"voxel array {vox.shape} does not match stored dims {brick.stored_dims}")
+    if state.dtype != np.float64 or state.shape != (height, width, 4) or not state.flags["C_CONTIGUOUS"]:
+        raise ValueError("state must be a C-contiguous (H, W, 4) float64 array")
+    geo = np.array([*brick.stored_lo, *brick.stored_dims, *brick.dims, *brick.lo, *brick.hi], np.int64)
+    wgeo = np.array([*brick.origin, *brick.spacing], np.float64)
+    tf = np.ascontiguousarray(tf, np.float32).reshape(-1, 4)
+    tf_scale = (tf.shape[0] - 1) / (float(vmax) - float(vmin))
+    rc = load_oracle().dvr_oracle_render_brick_accum(
+        _ptr(vox), _ptr(geo), _ptr(wgeo), _ptr(np.ascontiguousarray(cam, np.float64)), _ptr(tf), tf.shape[0],
+        float(vmin), float(tf_scale), float(dt), float(ert), width, height, int(rows[0]), int(rows[1]), _ptr(state),
+        nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle render_brick_accum failed with code {rc}")
+
+
+def cycle_frame(bricks_vox: Sequence[np.ndarray], bricks: Sequence[OracleBrick], order: Sequence[int],
+                row_blocks: Sequence[Tuple[int, int]], cam: np.ndarray, tf: np.ndarray, vmin: float, vmax: float,
+                dt: float, ert: float, width: int, height: int, background) -> np.ndarray:
+    """The ray-cycling frame, restated serially: the batch of rank b's rows starts at b's
+    position p0 in the visibility order and visits positions p0, p0+1, ..., R-1 (back segment, state B)
+    then 0, ..., p0-1 (front segment, state F); the frame is F over B over the background."""
+    R = len(bricks)
+    pos = {s: i for i, s in enumerate(order)}
+    out = np.zeros((height, width, 3), np.float64)
+    for b in range(R):
+        r0, r1 = row_blocks[b]
+        if r1 <= r0:
+            continue
+        B = np.zeros((height, width, 4), np.float64)
+        F = np.zeros((height, width, 4), np.float64)
+        p0 = pos[b]
+        for k in range(R):
+            q = (p0 + k) % R
+            s = order[q]
+            render_brick_accum(bricks_vox[s], bricks[s], cam, tf, vmin, vmax, dt, ert, width, height,
+                               B if q >= p0 else F, (r0, r1))
+        acc = F.copy()
+        acc[..., :3] += (1.0 - F[..., 3:4]) * B[..., :3]
+        acc[..., 3:4] += (1.0 - F[..., 3:4]) * B[..., 3:4]
+        img = acc[..., :3] + (1.0 - acc[..., 3:4]) * np.asarray(background, np.float64)
+        out[r0:r1] = img[r0:r1]
+    return out
 
 
 # ---------------------------------------------------------------------------------------------

@@ -26,7 +26,7 @@
 #include <omp.h>
 #endif
 
-#define ORACLE_ABI_VERSION 5
+#define ORACLE_ABI_VERSION 6
 
 int dvr_oracle_version(void) { return ORACLE_ABI_VERSION; }
 
@@ -250,13 +250,24 @@ static void tf_lookup(const Brick* b, double v, double out[4]) {
 }
 
 /* One pixel of one brick: returns the owned lattice sample count; rgba = premultiplied partial. */
-static int64_t march_pixel(const Brick* b, const double* cam, int px, int py, int W, int H, double rgba[4]) {
+/* accum = 0: the brick's own partial from a clear ray (sort-last).  accum = 1: continue the ray's
+ * accumulated state in rgba (ray cycling): ERT on the accumulated alpha, a ray already at
+ * ERT adds nothing. */
+static int64_t march_pixel(const Brick* b, const double* cam, int px, int py, int W, int H, double rgba[4],
+                           int accum) {
     double d[3];
     primary_dir(cam, px, py, W, H, d);
     const double* o = cam;
     int64_t k0 = 0;
     int64_t n = lattice_range(o, d, b->lo_w, b->hi_w, b->dt, &k0);
     double C0 = 0.0, C1 = 0.0, C2 = 0.0, A = 0.0;
+    if (accum) {
+        C0 = rgba[0];
+        C1 = rgba[1];
+        C2 = rgba[2];
+        A = rgba[3];
+        if (A >= b->ert) return n;
+    }
     for (int64_t k = k0; k < k0 + n; ++k) {
         double t = (double)k * b->dt;
         double u[3];
@@ -284,35 +295,42 @@ static int64_t march_pixel(const Brick* b, const double* cam, int px, int py, in
 /* Render rows row0, row0+row_step, ... < row1 of the full W x H frame for one brick.
  * geo: s_lo[3] sd[3] N[3] lo[3] hi[3] (int64); wgeo: origin[3] spacing[3] (double).
  * out_rgba: H*W*4 doubles (full-frame indexing); samples: H*W uint32 (may be NULL). */
+static int brick_setup(Brick* b, const float* vox, const int64_t* geo, const double* wgeo, const float* tf, int n_tf,
+                       double vmin, double tf_scale, double dt, double ert) {
+    b->vox = vox;
+    for (int a = 0; a < 3; ++a) {
+        b->s_lo[a] = geo[a];
+        b->sd[a] = geo[3 + a];
+        b->N[a] = geo[6 + a];
+        int64_t lo = geo[9 + a], hi = geo[12 + a];
+        b->origin[a] = wgeo[a];
+        b->spacing[a] = wgeo[3 + a];
+        b->lo_w[a] = b->origin[a] + (double)lo * b->spacing[a];
+        b->hi_w[a] = b->origin[a] + (double)hi * b->spacing[a];
+        int64_t clo = b->s_lo[a] > 0 ? b->s_lo[a] : 0;
+        int64_t chi = b->s_lo[a] + b->sd[a] - 2;
+        if (chi > b->N[a] - 2) chi = b->N[a] - 2;
+        if (chi < clo) return -2; /* every axis needs >= 2 stored voxels */
+        b->clo[a] = clo;
+        b->chi[a] = chi;
+    }
+    b->tf = tf;
+    b->n_tf = n_tf;
+    b->vmin = vmin;
+    b->tf_scale = tf_scale;
+    b->dt = dt;
+    b->ert = ert;
+    return 0;
+}
+
 int dvr_oracle_render_brick(const float* vox, const int64_t* geo, const double* wgeo, const double* cam,
                             const float* tf, int n_tf, double vmin, double tf_scale, double dt, double ert,
                             int W, int H, int row0, int row1, int row_step, double* out_rgba,
                             uint32_t* samples, int nthreads) {
     if (n_tf < 2 || !(dt > 0.0) || W <= 0 || H <= 0 || row_step <= 0) return -1;
     Brick b;
-    b.vox = vox;
-    for (int a = 0; a < 3; ++a) {
-        b.s_lo[a] = geo[a];
-        b.sd[a] = geo[3 + a];
-        b.N[a] = geo[6 + a];
-        int64_t lo = geo[9 + a], hi = geo[12 + a];
-        b.origin[a] = wgeo[a];
-        b.spacing[a] = wgeo[3 + a];
-        b.lo_w[a] = b.origin[a] + (double)lo * b.spacing[a];
-        b.hi_w[a] = b.origin[a] + (double)hi * b.spacing[a];
-        int64_t clo = b.s_lo[a] > 0 ? b.s_lo[a] : 0;
-        int64_t chi = b.s_lo[a] + b.sd[a] - 2;
-        if (chi > b.N[a] - 2) chi = b.N[a] - 2;
-        if (chi < clo) return -2; /* every axis needs >= 2 stored voxels */
-        b.clo[a] = clo;
-        b.chi[a] = chi;
-    }
-    b.tf = tf;
-    b.n_tf = n_tf;
-    b.vmin = vmin;
-    b.tf_scale = tf_scale;
-    b.dt = dt;
-    b.ert = ert;
+    int rc = brick_setup(&b, vox, geo, wgeo, tf, n_tf, vmin, tf_scale, dt, ert);
+    if (rc) return rc;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
@@ -323,7 +341,7 @@ int dvr_oracle_render_brick(const float* vox, const int64_t* geo, const double* 
         for (int px = 0; px < W; ++px) {
             int64_t pix = (int64_t)py * W + px;
             double rgba[4];
-            int64_t n = march_pixel(&b, cam, px, py, W, H, rgba);
+            int64_t n = march_pixel(&b, cam, px, py, W, H, rgba, 0);
             double* dst = out_rgba + 4 * pix;
             dst[0] = rgba[0];
             dst[1] = rgba[1];
@@ -332,6 +350,24 @@ int dvr_oracle_render_brick(const float* vox, const int64_t* geo, const double* 
             if (samples) samples[pix] = (uint32_t)n;
         }
     }
+    return 0;
+}
+
+/* Ray cycling: continue the accumulated front-to-back state of rows row0 <= y < row1
+ * through this brick.  state: H*W*4 doubles (full-frame indexing), read and written in place. */
+int dvr_oracle_render_brick_accum(const float* vox, const int64_t* geo, const double* wgeo, const double* cam,
+                                  const float* tf, int n_tf, double vmin, double tf_scale, double dt, double ert,
+                                  int W, int H, int row0, int row1, double* state, int nthreads) {
+    if (n_tf < 2 || !(dt > 0.0) || W <= 0 || H <= 0 || row0 < 0 || row1 > H) return -1;
+    Brick b;
+    int rc = brick_setup(&b, vox, geo, wgeo, tf, n_tf, vmin, tf_scale, dt, ert);
+    if (rc) return rc;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int py = row0; py < row1; ++py)
+        for (int px = 0; px < W; ++px) march_pixel(&b, cam, px, py, W, H, state + 4 * ((int64_t)py * W + px), 1);
     return 0;
 }
 

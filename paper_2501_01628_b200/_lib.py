@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -31,6 +31,7 @@ MARCH_FULL_FRAME = 2
 MARCH_BEAM = 4
 MARCH_QUEUE = 8
 MARCH_BAND_CLEAR = 16
+MARCH_ACCUM = 32
 COMPOSITE_TONEMAP = 1
 COMPOSITE_RGBA = 2
 
@@ -64,7 +65,8 @@ class FieldSpec(ctypes.Structure):
 class MarchParams(ctypes.Structure):
     _fields_ = [("tf_rgba", ctypes.c_void_p), ("n_tf", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("vmin", ctypes.c_double), ("vmax", ctypes.c_double), ("dt", ctypes.c_double),
-                ("ert", ctypes.c_double), ("tf_version", ctypes.c_uint64)]
+                ("ert", ctypes.c_double), ("tf_version", ctypes.c_uint64), ("row0", ctypes.c_int32),
+                ("row1", ctypes.c_int32)]
 
 
 _lib: Optional[ctypes.CDLL] = None

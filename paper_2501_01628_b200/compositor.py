@@ -131,9 +131,9 @@ class Compositor:
             return "auto"  # p2p if every rank can map its peers (decided collectively), else direct_send
         if mode == "binary_swap" and P & (P - 1):
             raise UsageError(f"binary_swap needs a power-of-two rank count, got {P}")
-        if mode not in ("direct_send", "binary_swap", "p2p"):
+        if mode not in ("direct_send", "binary_swap", "p2p", "cycle"):
             raise UsageError(f"unknown composite mode {mode!r}")
-        return mode
+        return mode  # "cycle": the renderer moves rays, this object only gathers the tiles
 
     def _buf(self, name: str, numel: int, dtype=torch.float32) -> torch.Tensor:
         t = self._scratch.get(name)

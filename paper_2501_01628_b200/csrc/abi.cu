@@ -357,8 +357,14 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.band_clear = (p->flags & DPRT_MARCH_BAND_CLEAR) ? 1 : 0;
+    a.accum = (p->flags & DPRT_MARCH_ACCUM) ? 1 : 0;
+    const bool window = p->row1 > p->row0;
+    if (window && (p->row0 < 0 || p->row1 > H)) return fail(DPRT_E_USAGE, "row window [%d, %d) outside [0, %d)", p->row0, p->row1, H);
+    if ((a.accum || window) && rgb8) return fail(DPRT_E_USAGE, "row windows and accumulation need an RGBA partial");
+    a.pix0 = window ? (long long)p->row0 * W : 0;
+    a.npix_buf = window ? (long long)(p->row1 - p->row0) * W : (long long)W * H;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
-    if (rgb8) a.beam = 1;  // the fused RGB8 output exists in the beam marcher only
+    if (rgb8 || a.accum || window) a.beam = 1;  // RGB8 output, accumulation and row windows: beam marcher only
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
     a.n_tf = p->n_tf;
     a.vmin = (float)p->vmin;
@@ -384,6 +390,11 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     } else {
         rc = dprt_brick_footprint(b, cam, W, H, a.rect);
         if (rc) return rc;
+    }
+    if (window) {  // rays only in rows [row0, row1)
+        if (a.rect[1] < p->row0) a.rect[1] = p->row0;
+        if (a.rect[3] > p->row1) a.rect[3] = p->row1;
+        if (a.rect[3] < a.rect[1]) a.rect[3] = a.rect[1];
     }
     DprtBrick* mb = const_cast<DprtBrick*>(b);  // ray queue + skip-distance cache are mutable scratch
     if (!a.beam && (long long)W * H > mb->ray_cap) {  // the queue marcher needs 32 B per pixel

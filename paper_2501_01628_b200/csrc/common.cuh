@@ -70,6 +70,9 @@ struct MarchArgs {
     int mcd[3];
     int skip;
     int band_clear;  // clear only the footprint's row band of the partial (DPRT_MARCH_BAND_CLEAR)
+    int accum;       // continue from / write back each ray's accumulated state (DPRT_MARCH_ACCUM)
+    long long pix0;      // out[] and samples[] hold pixels from index pix0 = row0 * W on (row window)
+    long long npix_buf;  // pixels out[] / samples[] hold (W * H, or the row window's)
     int beam;  // 1: march_beam_kernel (warp beams, per-pixel ray records); 0: ray queue + march_kernel
     // transfer function
     const float4* __restrict__ tf;

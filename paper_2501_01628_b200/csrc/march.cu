@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
             int64_t k0 = 0;
             primary_dir(a, px, py, d);
             const int64_t n = lattice_range(a, d, &k0);
-            if (a.samples) a.samples[pix] = (uint32_t)n;
+            if (a.samples) a.samples[pix - a.pix0] = (uint32_t)n;
             if (n > 0) {
                 const double t0 = __dmul_rn((double)k0, a.dt);
 #pragma unroll
@@ -447,6 +447,15 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
 #endif
         int j = 0;
         float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+        if (a.accum && nn > 0) {
+            // ray cycling: continue this ray's front-to-back state from the bricks it has crossed
+            const float4 s0 = a.out[pix - a.pix0];
+            C0 = s0.x;
+            C1 = s0.y;
+            C2 = s0.z;
+            A = s0.w;
+            if (A >= ert) nn = 0;  // terminated in front of this brick: nothing to add, nothing to write
+        }
         bool live = nn > 0;
         while (true) {
             const unsigned livem = __ballot_sync(FULL, live);
@@ -653,7 +662,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                 dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
                 dst[2] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[2], C2), 0.f), 1.f) * 255.f + 0.5f);
             } else {
-                a.out[pix] = make_float4(C0, C1, C2, A);
+                a.out[pix - a.pix0] = make_float4(C0, C1, C2, A);
             }
         }
     }
@@ -793,14 +802,16 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
             fill_rgb8_kernel<<<(unsigned)((quads + 255) / 256), 256, 0, stream>>>(a.rgb8, (long long)a.W * a.H,
                                                                               a.bg[0], a.bg[1], a.bg[2]);
             e = cudaGetLastError();
+        } else if (a.accum) {
+            e = cudaSuccess;  // the buffer holds the rays' accumulated state
         } else if (a.band_clear) {
             // the caller reads only the footprint's row band (band-clipped compositing)
-            e = cudaMemsetAsync(a.out + (size_t)a.rect[1] * a.W, 0,
+            e = cudaMemsetAsync(a.out + ((size_t)a.rect[1] * a.W - a.pix0), 0,
                                 (size_t)(a.rect[3] - a.rect[1]) * a.W * sizeof(float4), stream);
         } else {
-            e = cudaMemsetAsync(a.out, 0, (size_t)a.W * a.H * sizeof(float4), stream);
+            e = cudaMemsetAsync(a.out, 0, (size_t)a.npix_buf * sizeof(float4), stream);
         }
-        if (e == cudaSuccess && a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.W * a.H * sizeof(uint32_t), stream);
+        if (e == cudaSuccess && a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kBeamBlock, smem);
         if (per_sm < 1) per_sm = 1;

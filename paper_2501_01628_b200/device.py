@@ -219,27 +219,38 @@ class DeviceTF:
 
 def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, partial: torch.Tensor,
           width: int, height: int, samples: Optional[torch.Tensor] = None, skip: bool = True,
-          footprint: bool = True, band_clear: bool = False) -> None:
+          footprint: bool = True, band_clear: bool = False, accum: bool = False,
+          rows: Optional[Tuple[int, int]] = None) -> None:
     """dprt_march: the brick's full-frame premultiplied RGBA partial into ``partial`` (H*W*4 f32).
-    ``band_clear``: only the footprint's row band is defined afterwards (band-clipped compositing)."""
+    ``band_clear``: only the footprint's row band is defined afterwards (band-clipped compositing).
+    ``rows`` = (r0, r1): march only those pixel rows; ``partial`` (and ``samples``) hold just them.
+    ``accum``: ``partial`` holds each ray's accumulated front-to-back state, which the march continues
+    (ray cycling)."""
     _require_cuda(partial, "partial", torch.float32)
-    if partial.numel() != width * height * 4:
-        raise UsageError(f"partial holds {partial.numel()} floats, need {width * height * 4}")
+    npix = width * height if rows is None else (rows[1] - rows[0]) * width
+    if rows is not None and not (0 <= rows[0] < rows[1] <= height):
+        raise UsageError(f"row window {rows} outside [0, {height})")
+    if partial.numel() != npix * 4:
+        raise UsageError(f"partial holds {partial.numel()} floats, need {npix * 4}")
     sp = ctypes.c_void_p(0)
     if samples is not None:
         _require_cuda(samples, "samples", torch.int32)
-        if samples.numel() != width * height:
+        if samples.numel() != npix:
             raise UsageError("samples buffer must hold one count per pixel")
         sp = ctypes.c_void_p(samples.data_ptr())
     flags = (0 if skip else _lib.MARCH_NO_SKIP) | (0 if footprint else _lib.MARCH_FULL_FRAME)
     if band_clear:
         flags |= _lib.MARCH_BAND_CLEAR
+    if accum:
+        flags |= _lib.MARCH_ACCUM
     variant = os.environ.get("DPRT_MARCHER", "")
     if variant == "beam":
         flags |= _lib.MARCH_BEAM
     elif variant == "queue":
         flags |= _lib.MARCH_QUEUE
     p = tf.params(dt, ert, flags)
+    if rows is not None:
+        p.row0, p.row1 = int(rows[0]), int(rows[1])
     c = camera_struct(cam)
     rc = _lib.lib().dprt_march(brick.handle, ctypes.byref(c), ctypes.byref(p), ctypes.c_void_p(partial.data_ptr()),
                                sp, width, height, _stream(brick.device))

@@ -21,13 +21,13 @@ import numpy as np
 import torch
 
 from . import device as dev
-from .compositor import Compositor
+from .compositor import Compositor, assign_rows
 from .errors import ContractError, UsageError
 from .geom import CameraSpec, Vec3
 from .transport import RankEndpoint
 from .volume import Decomposition, TransferFunction1D, visibility_order
 
-COMPOSITE_MODES = ("auto", "direct_send", "binary_swap", "p2p")
+COMPOSITE_MODES = ("auto", "direct_send", "binary_swap", "p2p", "cycle")
 FUSED_SLOTS = 3  # device RGB8 frames the fused single-rank path rotates through (read-back pipeline depth)
 
 # Distinct colours for rank-ownership visualisation, one per rank modulo 8 (engine.py:41-44).
@@ -55,7 +55,7 @@ class RenderOptions:
 
     dt: float = 1.0                    # lattice spacing along the ray, world units
     ert: float = 0.99                  # early ray termination threshold (per brick)
-    composite: str = "auto"            # auto | direct_send | binary_swap | p2p
+    composite: str = "auto"            # auto | direct_send | binary_swap | p2p | cycle (ray cycling, §2.9)
     skip_empty: bool = True            # exact empty-space skipping
     disable_compositing: bool = False  # debug: root shows only its own brick (negative test, engine.py:172)
     frame_index: int = 0
@@ -278,6 +278,8 @@ class VolumeRenderer:
                 res.samples = self.samples.view(height, width)
                 stats._samples_dev = res.samples
             return res
+        if options.composite == "cycle" and self.ep.R > 1 and not options.disable_compositing:
+            return self._render_cycle(cam, width, height, options, dtf, stats, order, ev, t0)
         bands = None
         if options.clip_exchange and self.ep.R > 1 and not options.disable_compositing and \
                 self.compositor.clips_bands():
@@ -307,6 +309,68 @@ class VolumeRenderer:
             rgba = out.rgba.view(height, width, 4).double().cpu().numpy()
             bg = np.asarray(self.background, np.float64)
             res.image = rgba[..., :3] + (1.0 - rgba[..., 3:4]) * bg
+        if options.collect_samples:
+            res.samples = self.samples.view(height, width)
+            stats._samples_dev = res.samples
+        return res
+
+    def _render_cycle(self, cam, width, height, options, dtf, stats, order, ev, t0) -> RenderResult:
+        """Ray cycling (the reference's paradigm, engine.py:282-310, for DVR).  Rank b's
+        batch = its row block.  It starts at b's position p0 in the visibility order and hops along that
+        order (ring_exchange, transport.py:457-462): at each hop the holder marches its brick into the
+        batch's back state B (positions >= p0) or front state F (positions < p0), continuing the rays'
+        accumulated state (ERT on accumulated opacity, so rays saturated in front skip later bricks).
+        After R hops the batch is home (engine.py:305-309 asserts the same); F over B + background +
+        tone map gives the RGB8 tile, gathered to rank 0 like the other modes."""
+        ep, R, r, W = self.ep, self.ep.R, self.ep.rank, width
+        blocks = assign_rows(height, R)
+        pos = {s: i for i, s in enumerate(order)}
+        nxt, prv = order[(pos[r] + 1) % R], order[(pos[r] - 1) % R]
+        maxn = max(b1 - b0 for b0, b1 in blocks) * W
+        comp = self.compositor
+        bufs = [comp._buf("cycA", max(maxn, 1) * 8), comp._buf("cycB", max(maxn, 1) * 8)]
+        mine = blocks[r]
+        n_mine = (mine[1] - mine[0]) * W
+        bufs[0][: n_mine * 8].zero_()
+        cur = 0
+        sent = 0
+        for k in range(R):
+            po = (pos[r] - k) % R  # origin position of the batch held at this hop
+            rows = blocks[order[po]]
+            n = (rows[1] - rows[0]) * W
+            if n:
+                state = bufs[cur][: n * 8]
+                seg = state[: n * 4] if pos[r] >= po else state[n * 4:]  # back (B) or front (F) segment
+                smp = self.samples[rows[0] * W: rows[1] * W] if options.collect_samples else None
+                dev.march(self.brick, cam, dtf, options.dt, options.ert, seg, width, height, samples=smp,
+                          skip=options.skip_empty, accum=True, rows=rows)
+            # hand the batch on along the visibility order; receive the one behind it
+            rrows = blocks[order[(pos[r] - k - 1) % R]]
+            rn = (rrows[1] - rrows[0]) * W
+            ep.exchange([(nxt, bufs[cur][: n * 8])] if n else [], [(prv, bufs[1 - cur][: rn * 8])] if rn else [])
+            sent += n * 32
+            stats.record(options.frame_index, n, n * 32, (time.perf_counter() - t0) * 1e3)
+            cur = 1 - cur
+        if ev is not None:
+            ev[1].record(torch.cuda.current_stream(self.device))
+        tile = comp._buf("tile8", max(n_mine, 1) * 3, torch.uint8)[: n_mine * 3]
+        tile_f = comp._buf("tilef", max(n_mine, 1) * 4)[: n_mine * 4] if options.keep_float else None
+        if n_mine:
+            home = bufs[cur][: n_mine * 8]
+            dev.composite([home[n_mine * 4:], home[: n_mine * 4]], self.background, rgb8=tile, rgba=tile_f)
+        if self._pending_copy is not None:
+            torch.cuda.current_stream(self.device).wait_event(self._pending_copy)
+            self._pending_copy = None
+        comp.last_bytes = 0
+        out = comp._gather_tiles(mine, tile, tile_f, blocks, options.keep_float)
+        if ev is not None:
+            ev[2].record(torch.cuda.current_stream(self.device))
+            stats.events = tuple(ev)
+        stats.bytes_exchanged += sent + comp.last_bytes
+        res = RenderResult(rgb8=out.rgb8, stats=stats, order=order)
+        if options.keep_float and out.rgba is not None:
+            rgba = out.rgba.view(height, width, 4).double().cpu().numpy()
+            res.image = rgba[..., :3] + (1.0 - rgba[..., 3:4]) * np.asarray(self.background, np.float64)
         if options.collect_samples:
             res.samples = self.samples.view(height, width)
             stats._samples_dev = res.samples
