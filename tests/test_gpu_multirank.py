@@ -55,11 +55,14 @@ def test_sort_last_frame_matches_oracle(cuda_device, oracle_lib, mode, R):
                 assert image is None and rgb8 is None
 
 
-@pytest.mark.parametrize("mode,R", [("direct_send", 4), ("p2p", 3), ("binary_swap", 2)])
-def test_band_clipped_exchange_is_bit_identical(cuda_device, mode, R):
+@pytest.mark.parametrize("mode,R,W,H", [("direct_send", 4, 176, 130), ("p2p", 3, 176, 130),
+                                        ("binary_swap", 2, 176, 130), ("direct_send", 3, 157, 113),
+                                        ("p2p", 4, 157, 113)])
+def test_band_clipped_exchange_is_bit_identical(cuda_device, mode, R, W, H):
     """clip_exchange (only footprint rows move, partials cleared only inside their bands) changes the
-    bytes exchanged, never the frame: RGB8 and float frames equal the unclipped exchange bit for bit."""
-    s = c1(P=R, W=176, H=130)
+    bytes exchanged, never the frame: RGB8 and float frames equal the unclipped exchange bit for bit
+    (odd widths put fragment range edges inside the composite kernel's 4-pixel groups)."""
+    s = c1(P=R, W=W, H=H)
 
     def body(ep):
         b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda_device).generate(s.field)
