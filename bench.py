@@ -234,7 +234,9 @@ def run_reference(args):
     ca = oracle.camera_array(cam.position, cam.view_dir, cam.up, cam.fov_y, cam.aspect)
     lo, hi = dec.boxes[0]
     ob = oracle.OracleBrick(f.dims, lo, hi, 1, f.origin, f.spacing)
-    stride = 36  # 30 of 1080 rows per step
+    # whole frames per step (~0.5 s on 16 threads) unless K + W is large: then every stride-th row, so the
+    # arm stays around a minute; thin samples would under-state the CPU (few rows per OpenMP thread)
+    stride = max(1, -(-(args.warmup + args.steps) // 120))
     rows = len(range(0, H, stride))
     times = []
     for i in range(args.warmup + args.steps):
