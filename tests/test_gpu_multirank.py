@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("mode,R", [("direct_send", 2), ("direct_send", 3), ("binary_swap", 4), ("p2p", 2),
-                                    ("p2p", 4), ("binary_swap", 8), ("auto", 3)])
+                                    ("p2p", 4), ("binary_swap", 8), ("auto", 3), ("p2p", 8), ("direct_send", 8),
+                                    ("cycle", 8)])
 def test_sort_last_frame_matches_oracle(cuda_device, oracle_lib, mode, R):
     s = c1(P=R, W=160, H=122)
     vox = oracle.generate_field(s.field.dims, s.field.blobs)
