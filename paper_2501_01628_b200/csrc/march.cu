@@ -351,9 +351,6 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #define DPRT_SLAB_SHIFT DPRT_MACRO_SHIFT  // slab thickness (cells, log2) of the probe-mode beam step
 #endif
 constexpr int kSlabShift = DPRT_SLAB_SHIFT;
-#ifndef DPRT_BRANCHFREE
-#define DPRT_BRANCHFREE 1  // 0: per-slot branches (the v5 loop), kept for comparison
-#endif
 
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
@@ -554,7 +551,6 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
 #endif
             // Shade this lane's samples in the slab, kBeamUnroll at a time: all their corner loads are
             // issued before the first is shaded, so each lane keeps several loads in flight.
-#if DPRT_BRANCHFREE
             // branch-free batches: slots past the lane's last sample in the slab re-load that sample (same
             // address, an L1 hit) and contribute w = 0; ERT masks the rest of the batch the same way
             const float fend = (float)(jend - 1);
@@ -604,53 +600,6 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                     break;
                 }
             }
-#else
-            while (j < jend) {
-                const int cnt = min(kBeamUnroll, jend - j);
-                float4 qa[kBeamUnroll], qb[kBeamUnroll];
-                float wx[kBeamUnroll], wy[kBeamUnroll], wz[kBeamUnroll];
-                const float fj = (float)j;  // exact: j < 2^24
-#pragma unroll
-                for (int u = 0; u < kBeamUnroll; ++u) {
-                    if (u < cnt) {
-                        const float fs = fj + (float)u;
-                        const float ux = fmaf(fs, st[0], p0[0]);
-                        const float uy = fmaf(fs, st[1], p0[1]);
-                        const float uz = fmaf(fs, st[2], p0[2]);
-                        // no clamp: the quad grid's apron covers the cells rounding can reach (field.cu)
-                        const int ix = __float2int_rd(ux), iy = __float2int_rd(uy), iz = __float2int_rd(uz);
-                        const int qi = iz * qsz + iy * qsy + ix;
-                        quad_bounds_check(a, qi);
-                        qa[u] = __ldg(qorg + qi);
-                        qb[u] = __ldg(qorg1 + qi);
-                        wx[u] = __saturatef(ux - (float)ix);
-                        wy[u] = __saturatef(uy - (float)iy);
-                        wz[u] = __saturatef(uz - (float)iz);
-                    }
-                }
-                bool stop = false;
-#pragma unroll
-                for (int u = 0; u < kBeamUnroll; ++u) {
-                    if (u < cnt && !stop) {
-                        const float v = trilerp(qa[u], qb[u], wx[u], wy[u], wx[u] * wy[u], wz[u]);
-#if DPRT_COUNTERS
-                        const float a0 = A;
-#endif
-                        tf_blend(s_tf, s_tf + a.n_tf, v, tns, tno, top, C0, C1, C2, A);
-#if DPRT_COUNTERS
-                        ++c_shade;
-                        c_contrib += A > a0;
-#endif
-                        if (A >= ert) stop = true;  // early ray termination
-                    }
-                }
-                j += cnt;
-                if (stop) {
-                    live = false;
-                    break;
-                }
-            }
-#endif
             if (j >= nn) live = false;
         }
         if (nn > 0) {
