@@ -292,7 +292,7 @@ def run_ours(args):
     brick = dev.DeviceBrick(desc, device).generate(f)
     renderer = VolumeRenderer(ep, brick, dec, tf, BACKGROUND)
     skip = not args.no_skip
-    opts = RenderOptions(dt=DT, ert=ERT, composite=args.composite, skip_empty=skip)
+    opts = RenderOptions(dt=DT, ert=ERT, composite=args.composite, skip_empty=skip, fragment_dtype=args.fragments)
     stream = torch.cuda.current_stream(device)
     torch.cuda.synchronize(device)
 
@@ -345,7 +345,7 @@ def run_ours(args):
         moved = torch.tensor([float(comp.last_bytes)], dtype=torch.float64, device=device)
         dist.all_reduce(moved, op=dist.ReduceOp.MAX)
         frag_bytes = int(moved.item())
-        full_bytes = int((1 - 1 / R) * W * H * 16)          # unclipped RGBA f32 fragments per rank
+        full_bytes = int((1 - 1 / R) * W * H * (8 if args.fragments == "f16" else 16))  # unclipped fragments/rank
         gather_bytes = int((R - 1) / R * W * H * 3)          # RGB8 tiles into rank 0
         achieved_nv = frag_bytes / (comp_ms * 1e-3) / 1e9
         nvlink = {"bound": "nvlink", "achieved": achieved_nv, "peak": 770.0, "unit": "GB/s",
@@ -439,6 +439,7 @@ def run_ours(args):
             "config": {"workload": "c2: 512^3 f32 blob field (seed 1, 16 blobs), 1 brick per GPU, 1920x1080, "
                                    "dt=1 voxel, ERT 0.99, SURVEY 8(d) TF, auto camera",
                        "field": list(f.dims), "bricks": R, "image": [W, H], "composite": renderer.compositor.mode,
+                       "fragments": args.fragments,
                        "empty_space_skipping": skip, "l2": "inputs larger than L2 (brick 512 MiB/GPU), no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -465,6 +466,8 @@ def main():
     ap.add_argument("--composite", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-skip", action="store_true", help="disable exact empty-space skipping")
+    ap.add_argument("--fragments", default="f32", choices=["f32", "f16"],
+                    help="exchanged RGBA fragment format at N > 1 (f16: half the bytes, fp16 tolerance)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

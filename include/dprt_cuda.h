@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 5
+#define DPRT_ABI_VERSION 6
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -97,9 +97,12 @@ typedef struct DprtMarchParams {
 #define DPRT_MARCH_ACCUM 32       /* ray cycling: partial_rgba holds each ray's accumulated front-to-back
                                      state; the march continues from it (ERT on the accumulated alpha, rays
                                      already at ERT are skipped) and writes it back; nothing is cleared */
+#define DPRT_MARCH_HALF 64        /* beam marcher: partial_rgba is fp16 RGBA (8 B per pixel) -- half-size
+                                     fragments for the exchange; not with DPRT_MARCH_ACCUM */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
 #define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */
+#define DPRT_COMPOSITE_HALF_IN 4  /* fragments are fp16 RGBA (8 B per pixel, 8-byte aligned) */
 
 typedef struct DprtBrick DprtBrick;
 

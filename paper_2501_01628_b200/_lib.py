@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -32,8 +32,10 @@ MARCH_BEAM = 4
 MARCH_QUEUE = 8
 MARCH_BAND_CLEAR = 16
 MARCH_ACCUM = 32
+MARCH_HALF = 64
 COMPOSITE_TONEMAP = 1
 COMPOSITE_RGBA = 2
+COMPOSITE_HALF_IN = 4
 
 EXPORTS = (
     "dprt_cuda_version", "dprt_last_error", "dprt_device_count", "dprt_device_synchronize",

@@ -110,13 +110,18 @@ class Compositor:
     """Per-rank compositing state for one frame size (scratch buffers persist across frames)."""
 
     def __init__(self, ep: RankEndpoint, width: int, height: int, mode: str, device: torch.device,
-                 blender=None):
+                 blender=None, fragment_dtype: torch.dtype = torch.float32):
         self.ep = ep
         self.W = width
         self.H = height
         self.device = device
         self.mode_requested = mode
         self.mode = self.resolve_mode(mode, ep.R)
+        if fragment_dtype not in (torch.float32, torch.float16):
+            raise UsageError(f"fragments are float32 or float16, not {fragment_dtype}")
+        if fragment_dtype == torch.float16 and self.mode in ("binary_swap", "cycle"):
+            raise UsageError("fp16 fragments are exchanged by direct_send / p2p / auto only")
+        self.fdt = fragment_dtype
         self.blender = blender if blender is not None else CudaBlender()
         self.last_bytes = 0
         self._frame = None
@@ -231,11 +236,11 @@ class Compositor:
             if c:
                 sends.append((j, self._rows(partial, c, 4)))
         clips = {s: clip_rows(rows, band[s]) for s in range(P)}
-        inbox = {s: self._buf(f"in{s}", (clips[s][1] - clips[s][0]) * self.W * 4)[: (clips[s][1] - clips[s][0]) * self.W * 4]
-                 for s in plan.recvs if clips[s]}
+        inbox = {s: self._buf(f"in{s}", (clips[s][1] - clips[s][0]) * self.W * 4, self.fdt)[
+                    : (clips[s][1] - clips[s][0]) * self.W * 4] for s in plan.recvs if clips[s]}
         recvs = [(s, inbox[s]) for s in plan.recvs if clips[s]]
         ep.exchange(sends, recvs)
-        self.last_bytes += sum(t.numel() * 4 for _, t in sends)
+        self.last_bytes += sum(t.numel() * t.element_size() for _, t in sends)
         frags, ranges = [], []
         for s in order:
             c = clips[s]
@@ -247,7 +252,7 @@ class Compositor:
         tile_f = self._buf("tilef", n_own * 4) if keep_float else None
         if n_own:
             if not frags:  # every fragment clear: the background alone
-                frags, ranges = [self._buf("tilef0", 4)], [(0, 0)]
+                frags, ranges = [self._buf("tilef0", 4, self.fdt)], [(0, 0)]
             if bands is None:
                 self.blender.over_tonemap(frags, background, tile, tile_f)
             else:
@@ -302,7 +307,7 @@ class Compositor:
             impl = None
             if self.device.type == "cuda":
                 from .p2p import P2PCompositor
-                impl = P2PCompositor.try_create(self.ep, self.W, self.H, self.device)
+                impl = P2PCompositor.try_create(self.ep, self.W, self.H, self.device, self.fdt)
             self._p2p_impl = impl
             self.mode = "p2p" if impl is not None else "direct_send"
         if self.mode != "p2p":
@@ -312,7 +317,7 @@ class Compositor:
     def _p2p(self):
         if getattr(self, "_p2p_impl", None) is None:
             from .p2p import P2PCompositor
-            impl = P2PCompositor.try_create(self.ep, self.W, self.H, self.device)
+            impl = P2PCompositor.try_create(self.ep, self.W, self.H, self.device, self.fdt)
             if impl is None:
                 raise TransportError("p2p compositing needs every rank to map its peers' buffers "
                                      "(CUDA IPC over NVLink); use composite='direct_send'")

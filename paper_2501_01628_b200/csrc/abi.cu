@@ -358,13 +358,15 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.band_clear = (p->flags & DPRT_MARCH_BAND_CLEAR) ? 1 : 0;
     a.accum = (p->flags & DPRT_MARCH_ACCUM) ? 1 : 0;
+    a.half_out = (p->flags & DPRT_MARCH_HALF) ? 1 : 0;
+    if (a.half_out && (a.accum || rgb8)) return fail(DPRT_E_USAGE, "fp16 partials exclude accumulation and RGB8 output");
     const bool window = p->row1 > p->row0;
     if (window && (p->row0 < 0 || p->row1 > H)) return fail(DPRT_E_USAGE, "row window [%d, %d) outside [0, %d)", p->row0, p->row1, H);
     if ((a.accum || window) && rgb8) return fail(DPRT_E_USAGE, "row windows and accumulation need an RGBA partial");
     a.pix0 = window ? (long long)p->row0 * W : 0;
     a.npix_buf = window ? (long long)(p->row1 - p->row0) * W : (long long)W * H;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
-    if (rgb8 || a.accum || window) a.beam = 1;  // RGB8 output, accumulation and row windows: beam marcher only
+    if (rgb8 || a.accum || window || a.half_out) a.beam = 1;  // these outputs exist in the beam marcher only
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
     a.n_tf = p->n_tf;
     a.vmin = (float)p->vmin;
@@ -372,7 +374,8 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.tf_ns = (float)(1.0 / (p->vmax - p->vmin));
     a.tf_no = (float)(-p->vmin / (p->vmax - p->vmin));
     a.ert = (float)p->ert;
-    a.out = reinterpret_cast<float4*>(partial_rgba);
+    a.out = a.half_out ? nullptr : reinterpret_cast<float4*>(partial_rgba);
+    a.out16 = a.half_out ? reinterpret_cast<uint2*>(partial_rgba) : nullptr;
     a.rgb8 = rgb8;
     if (bg) {
         a.bg[0] = bg[0];
@@ -431,7 +434,8 @@ int dprt_composite_ranged(int device, const float* const* inputs, const int64_t*
         if (lo < 0 || hi > npix || lo > hi) return fail(DPRT_E_USAGE, "fragment %d range [%lld, %lld) outside [0, %lld)",
                                                         i, (long long)lo, (long long)hi, (long long)npix);
         if (hi > lo && !inputs[i]) return fail(DPRT_E_USAGE, "fragment %d is null", i);
-        if (reinterpret_cast<uintptr_t>(inputs[i]) & 15) return fail(DPRT_E_USAGE, "fragment %d not 16-byte aligned", i);
+        if (reinterpret_cast<uintptr_t>(inputs[i]) & ((flags & DPRT_COMPOSITE_HALF_IN) ? 7 : 15))
+            return fail(DPRT_E_USAGE, "fragment %d not %d-byte aligned", i, (flags & DPRT_COMPOSITE_HALF_IN) ? 8 : 16);
         a.in[i] = reinterpret_cast<const float4*>(inputs[i]);
         a.lo[i] = lo;
         a.hi[i] = hi;

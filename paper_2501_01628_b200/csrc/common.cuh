@@ -1,6 +1,7 @@
 // Shared definitions for the sm_100a kernels of libdprt_cuda.so (see include/dprt_cuda.h).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -71,6 +72,7 @@ struct MarchArgs {
     int skip;
     int band_clear;  // clear only the footprint's row band of the partial (DPRT_MARCH_BAND_CLEAR)
     int accum;       // continue from / write back each ray's accumulated state (DPRT_MARCH_ACCUM)
+    int half_out;    // the partial is fp16 RGBA (DPRT_MARCH_HALF): out16 instead of out
     long long pix0;      // out[] and samples[] hold pixels from index pix0 = row0 * W on (row window)
     long long npix_buf;  // pixels out[] / samples[] hold (W * H, or the row window's)
     int beam;  // 1: march_beam_kernel (warp beams, per-pixel ray records); 0: ray queue + march_kernel
@@ -81,6 +83,7 @@ struct MarchArgs {
     float tf_ns, tf_no;  // normalised TF coordinate = sat(v * tf_ns + tf_no), tf_ns = 1 / (vmax - vmin)
     // output
     float4* __restrict__ out;
+    uint2* __restrict__ out16;  // fp16 RGBA partial (4 halves per pixel)
     uint8_t* rgb8;  // non-null: write the tone-mapped frame over bg[] instead of the RGBA partial (R == 1)
     float bg[3];
     uint32_t* __restrict__ samples;
@@ -92,6 +95,7 @@ struct MarchArgs {
 
 struct CompositeArgs {
     const float4* in[DPRT_MAX_PARTS];  // fragment i's element for tile pixel p is in[i][p - lo[i]]
+                                       // (fp16 fragments with DPRT_COMPOSITE_HALF_IN: a uint2 per pixel)
     long long lo[DPRT_MAX_PARTS], hi[DPRT_MAX_PARTS];  // tile pixels [lo, hi) fragment i covers (else clear)
     int P;
     long long npix;

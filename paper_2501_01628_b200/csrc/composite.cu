@@ -31,10 +31,44 @@ __device__ __forceinline__ uint32_t pack_rgb8(const float4 c, const float bg[3],
     return tone8(v);
 }
 
+// fp16 RGBA fragment pixel (uint2 = two __half2) -> float4
+__device__ __forceinline__ float4 h2f(const uint2 v) {
+    const float2 rg = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+    const float2 ba = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+    return make_float4(rg.x, rg.y, ba.x, ba.y);
+}
+
+// one fragment pixel / four consecutive fragment pixels, f32 or fp16 storage
+template <bool kHalf>
+__device__ __forceinline__ float4 load1(const float4* frag, long long i) {
+    if (kHalf) return h2f(__ldg(reinterpret_cast<const uint2*>(frag) + i));
+    return __ldg(frag + i);
+}
+template <bool kHalf>
+__device__ __forceinline__ void load4(const float4* frag, long long i, float4 f[4]) {
+    if (kHalf) {
+        const uint2* p = reinterpret_cast<const uint2*>(frag) + i;
+        if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {  // two 16-byte loads carry the 4 pixels
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(p)), b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+            f[0] = h2f(make_uint2(a.x, a.y));
+            f[1] = h2f(make_uint2(a.z, a.w));
+            f[2] = h2f(make_uint2(b.x, b.y));
+            f[3] = h2f(make_uint2(b.z, b.w));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) f[k] = h2f(__ldg(p + k));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[k] = __ldg(frag + i + k);
+    }
+}
+
 // Each thread composites 4 consecutive pixels: per fragment it issues the four 16-byte loads together
 // (and the next fragment's before blending, via unrolling), so P fragments keep 4-8 loads in flight;
 // the 12 RGB8 bytes leave as three aligned 32-bit stores.  A fragment covers only the tile pixels
 // [lo, hi) (a rank's footprint rows): outside them it is clear and is not read at all.
+template <bool kHalf>
 __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long i0 = q * 4;
@@ -46,17 +80,16 @@ __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
 #pragma unroll 2
         for (int p = 0; p < a.P; ++p) {
             const long long lo = a.lo[p], hi = a.hi[p];
-            const float4* fp = a.in[p] + (i0 - lo);
+            const long long off = i0 - lo;
             float4 f[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) f[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // clear: over adds exact 0
             if (i0 >= lo && i0 + 4 <= hi) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) f[k] = __ldg(fp + k);
+                load4<kHalf>(a.in[p], off, f);
             } else if (i0 + 4 > lo && i0 < hi) {  // a range edge inside this group (width not a multiple of 4)
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (i0 + k >= lo && i0 + k < hi) f[k] = __ldg(fp + k);
+                    if (i0 + k >= lo && i0 + k < hi) f[k] = load1<kHalf>(a.in[p], off + k);
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) over(acc[k], f[k]);
@@ -88,7 +121,7 @@ __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
     for (long long i = i0; i < a.npix; ++i) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int p = 0; p < a.P; ++p)
-            if (i >= a.lo[p] && i < a.hi[p]) over(acc, __ldg(a.in[p] + (i - a.lo[p])));
+            if (i >= a.lo[p] && i < a.hi[p]) over(acc, load1<kHalf>(a.in[p], i - a.lo[p]));
         if (a.flags & DPRT_COMPOSITE_RGBA) a.rgba[i] = acc;
         if (a.flags & DPRT_COMPOSITE_TONEMAP)
             for (int ch = 0; ch < 3; ++ch) a.rgb8[3 * i + ch] = (uint8_t)pack_rgb8(acc, a.bg, ch);
@@ -100,7 +133,10 @@ cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream) {
     const int block = 256;
     const long long grid = (threads + block - 1) / block;
     if (grid == 0) return cudaSuccess;
-    composite_kernel<<<(unsigned)grid, block, 0, stream>>>(a);
+    if (a.flags & DPRT_COMPOSITE_HALF_IN)
+        composite_kernel<true><<<(unsigned)grid, block, 0, stream>>>(a);
+    else
+        composite_kernel<false><<<(unsigned)grid, block, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -610,6 +610,10 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                 dst[0] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[0], C0), 0.f), 1.f) * 255.f + 0.5f);
                 dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
                 dst[2] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[2], C2), 0.f), 1.f) * 255.f + 0.5f);
+            } else if (a.half_out) {
+                const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
+                a.out16[pix - a.pix0] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
+                                                   *reinterpret_cast<const unsigned*>(&ba));
             } else {
                 a.out[pix - a.pix0] = make_float4(C0, C1, C2, A);
             }
@@ -755,10 +759,13 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
             e = cudaSuccess;  // the buffer holds the rays' accumulated state
         } else if (a.band_clear) {
             // the caller reads only the footprint's row band (band-clipped compositing)
-            e = cudaMemsetAsync(a.out + ((size_t)a.rect[1] * a.W - a.pix0), 0,
-                                (size_t)(a.rect[3] - a.rect[1]) * a.W * sizeof(float4), stream);
+            const size_t px = a.half_out ? sizeof(uint2) : sizeof(float4);
+            char* base = a.half_out ? reinterpret_cast<char*>(a.out16) : reinterpret_cast<char*>(a.out);
+            e = cudaMemsetAsync(base + ((size_t)a.rect[1] * a.W - a.pix0) * px, 0,
+                                (size_t)(a.rect[3] - a.rect[1]) * a.W * px, stream);
         } else {
-            e = cudaMemsetAsync(a.out, 0, (size_t)a.npix_buf * sizeof(float4), stream);
+            e = a.half_out ? cudaMemsetAsync(a.out16, 0, (size_t)a.npix_buf * sizeof(uint2), stream)
+                           : cudaMemsetAsync(a.out, 0, (size_t)a.npix_buf * sizeof(float4), stream);
         }
         if (e == cudaSuccess && a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;

@@ -225,8 +225,9 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
     ``band_clear``: only the footprint's row band is defined afterwards (band-clipped compositing).
     ``rows`` = (r0, r1): march only those pixel rows; ``partial`` (and ``samples``) hold just them.
     ``accum``: ``partial`` holds each ray's accumulated front-to-back state, which the march continues
-    (ray cycling)."""
-    _require_cuda(partial, "partial", torch.float32)
+    (ray cycling).  A float16 ``partial`` gets fp16 fragments (DPRT_MARCH_HALF)."""
+    half = partial.dtype == torch.float16
+    _require_cuda(partial, "partial", torch.float16 if half else torch.float32)
     npix = width * height if rows is None else (rows[1] - rows[0]) * width
     if rows is not None and not (0 <= rows[0] < rows[1] <= height):
         raise UsageError(f"row window {rows} outside [0, {height})")
@@ -243,6 +244,8 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
         flags |= _lib.MARCH_BAND_CLEAR
     if accum:
         flags |= _lib.MARCH_ACCUM
+    if half:
+        flags |= _lib.MARCH_HALF
     variant = os.environ.get("DPRT_MARCHER", "")
     if variant == "beam":
         flags |= _lib.MARCH_BEAM
@@ -285,12 +288,13 @@ def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[tor
     [lo_i, hi_i) (clear elsewhere) and ``npix`` is the tile size (dprt_composite_ranged)."""
     if not frags:
         raise UsageError("nothing to composite")
+    fdt = frags[0].dtype if frags[0].dtype in (torch.float16, torch.float32) else torch.float32
     if ranges is None:
         n = frags[0].numel()
         if n % 4:
             raise UsageError("fragments must hold whole RGBA pixels")
         for i, f in enumerate(frags):
-            _require_cuda(f, f"fragment {i}", torch.float32)
+            _require_cuda(f, f"fragment {i}", fdt)
             if f.numel() != n:
                 raise UsageError("fragments differ in size")
         npix = n // 4
@@ -298,7 +302,7 @@ def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[tor
         if npix is None or len(ranges) != len(frags):
             raise UsageError("ranged composite needs npix and one (lo, hi) range per fragment")
         for i, (f, (lo, hi)) in enumerate(zip(frags, ranges)):
-            _require_cuda(f, f"fragment {i}", torch.float32)
+            _require_cuda(f, f"fragment {i}", fdt)
             if f.numel() < 4 * (hi - lo):
                 raise UsageError(f"fragment {i} holds {f.numel() // 4} pixels, range needs {hi - lo}")
         n = npix * 4
@@ -322,6 +326,8 @@ def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[tor
             raise UsageError("rgba output must match the fragments")
         flags |= _lib.COMPOSITE_RGBA
         rgba_ptr = ctypes.c_void_p(rgba.data_ptr())
+    if fdt == torch.float16:
+        flags |= _lib.COMPOSITE_HALF_IN
     ptrs = (ctypes.c_void_p * len(frags))(*[f.data_ptr() for f in frags])
     rng = None if ranges is None else (ctypes.c_int64 * (2 * len(ranges)))(*[int(v) for r in ranges for v in r])
     dev = frags[0].device
@@ -332,9 +338,11 @@ def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[tor
 
 def composite_ptrs(device_index: int, ptrs: Sequence[int], npix: int, background, rgb8_ptr: int = 0,
                    rgba_ptr: int = 0, stream: Optional[int] = None,
-                   ranges: Optional[Sequence[Tuple[int, int]]] = None) -> None:
+                   ranges: Optional[Sequence[Tuple[int, int]]] = None, half: bool = False) -> None:
     """Raw-pointer form for peer (IPC-mapped) fragments and outputs: the fused NVLink compositor."""
     flags = (_lib.COMPOSITE_TONEMAP if rgb8_ptr else 0) | (_lib.COMPOSITE_RGBA if rgba_ptr else 0)
+    if half:
+        flags |= _lib.COMPOSITE_HALF_IN
     bg_arr = (ctypes.c_float * 3)(*[float(c) for c in background]) if background is not None else None
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
     rng = None if ranges is None else (ctypes.c_int64 * (2 * len(ranges)))(*[int(v) for r in ranges for v in r])
@@ -375,7 +383,7 @@ class DeviceBuffer:
         p = ctypes.c_void_p()
         _lib.check(_lib.lib().dprt_device_alloc(self.index, self.nbytes, ctypes.byref(p)), "dprt_device_alloc")
         self.ptr = int(p.value)
-        typestr = {torch.float32: "<f4", torch.uint8: "|u1", torch.int32: "<i4"}[dtype]
+        typestr = {torch.float32: "<f4", torch.float16: "<f2", torch.uint8: "|u1", torch.int32: "<i4"}[dtype]
         self.__cuda_array_interface__ = {"shape": (self.numel,), "typestr": typestr, "data": (self.ptr, False),
                                          "version": 3, "strides": None}
         self.tensor = torch.as_tensor(self, device=self.device)

@@ -28,6 +28,7 @@ from .transport import RankEndpoint
 from .volume import Decomposition, TransferFunction1D, visibility_order
 
 COMPOSITE_MODES = ("auto", "direct_send", "binary_swap", "p2p", "cycle")
+FRAGMENT_DTYPES = {"f32": torch.float32, "f16": torch.float16}
 FUSED_SLOTS = 3  # device RGB8 frames the fused single-rank path rotates through (read-back pipeline depth)
 
 # Distinct colours for rank-ownership visualisation, one per rank modulo 8 (engine.py:41-44).
@@ -65,6 +66,8 @@ class RenderOptions:
     clip_exchange: bool = True         # direct-send / p2p move only each rank's footprint rows;
                                        # RenderResult.partial is then defined only inside this rank's band
     timing: bool = False               # CUDA events around march and composite (RankStats.device_times())
+    fragment_dtype: str = "f32"        # "f16": half-size RGBA fragments (march output, exchange, blend input;
+                                       # direct_send / p2p / auto), DESIGN.md §6
 
 
 @dataclass
@@ -150,7 +153,7 @@ def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptio
         "size": [width, height],
         "dt": options.dt, "ert": options.ert, "composite": options.composite,
         "skip": options.skip_empty, "disableCompositing": options.disable_compositing, "mode": options.mode,
-        "clipExchange": options.clip_exchange,
+        "clipExchange": options.clip_exchange, "fragments": options.fragment_dtype,
         "tf": [_tf_hash(tf), tf.vmin, tf.vmax],
         "field": [list(f.dims), list(f.origin), list(f.spacing)],
         "bricks": [[list(lo), list(hi)] for lo, hi in decomposition.boxes],
@@ -204,15 +207,18 @@ class VolumeRenderer:
         self.tf = tf
         self.dtf = dev.DeviceTF(tf, self.brick.device)
 
-    def _ensure(self, width: int, height: int, mode: str) -> None:
+    def _ensure(self, width: int, height: int, mode: str, fragment_dtype: str = "f32") -> None:
+        if fragment_dtype not in FRAGMENT_DTYPES:
+            raise UsageError(f"fragment_dtype must be one of {tuple(FRAGMENT_DTYPES)}, got {fragment_dtype!r}")
+        fdt = FRAGMENT_DTYPES[fragment_dtype]
         if self._size != (width, height):
             self.samples = torch.empty(height * width, dtype=torch.int32, device=self.device)
             self.compositor = None
             self._size = (width, height)
-        if self.compositor is None or self.compositor.mode_requested != mode:
-            self.compositor = Compositor(self.ep, width, height, mode, self.device)
+        if self.compositor is None or self.compositor.mode_requested != mode or self.compositor.fdt != fdt:
+            self.compositor = Compositor(self.ep, width, height, mode, self.device, fragment_dtype=fdt)
             shared = self.compositor.shared_partial()
-            self.partial = shared if shared is not None else torch.empty(height * width * 4, dtype=torch.float32,
+            self.partial = shared if shared is not None else torch.empty(height * width * 4, dtype=fdt,
                                                                           device=self.device)
 
     def _bands(self, cam: CameraSpec, width: int, height: int):
@@ -243,7 +249,7 @@ class VolumeRenderer:
         if verify and self.ep.R > 1:  # one rank cannot diverge from itself
             verify_collective_digest(self.ep, render_digest(cam, width, height, options, self.tf,
                                                             self.background, self.decomposition))
-        self._ensure(width, height, options.composite)
+        self._ensure(width, height, options.composite, options.fragment_dtype)
         order = visibility_order(self.decomposition, cam.position)
         t0 = time.perf_counter()
         ev = None

@@ -23,9 +23,12 @@ from .transport import RankEndpoint
 
 
 class P2PCompositor:
-    def __init__(self, ep: RankEndpoint, width: int, height: int, device: torch.device):
+    def __init__(self, ep: RankEndpoint, width: int, height: int, device: torch.device,
+                 fragment_dtype: torch.dtype = torch.float32):
         """Collective.  Local failures never skip a collective call: they leave ``self.ok`` False."""
         self.ep = ep
+        self.fdt = fragment_dtype
+        self.px = 8 if fragment_dtype == torch.float16 else 16  # fragment bytes per pixel
         self.W = width
         self.H = height
         self.device = device
@@ -34,7 +37,7 @@ class P2PCompositor:
         self.ok = True
         self.partial = self.frame = self.frame_rgba = None
         try:
-            self.partial = dev.DeviceBuffer(device, n * 4)
+            self.partial = dev.DeviceBuffer(device, n * 4, fragment_dtype)
             if ep.rank == 0:
                 self.frame = dev.DeviceBuffer(device, n * 3, torch.uint8)
         except Exception:  # noqa: BLE001 - reported through self.ok
@@ -46,10 +49,11 @@ class P2PCompositor:
         self.last_bytes = 0
 
     @classmethod
-    def try_create(cls, ep: RankEndpoint, width: int, height: int, device: torch.device) -> Optional["P2PCompositor"]:
+    def try_create(cls, ep: RankEndpoint, width: int, height: int, device: torch.device,
+                   fragment_dtype: torch.dtype = torch.float32) -> Optional["P2PCompositor"]:
         """Collectively set up peer mappings; every rank gets None if any rank cannot (no NVLink P2P,
         IPC refused, ...), so the caller can pick the NCCL exchange instead -- on every rank alike."""
-        impl = cls(ep, width, height, device)
+        impl = cls(ep, width, height, device, fragment_dtype)
         flags = ep.all_gather_bytes(b"1" if impl.ok else b"0")
         if all(f == b"1" for f in flags):
             return impl
@@ -76,26 +80,27 @@ class P2PCompositor:
         if npix:
             off = rows[0] * self.W
             if bands is None:
-                ptrs = [self.peer_partials[s] + 16 * off for s in order]
+                ptrs = [self.peer_partials[s] + self.px * off for s in order]
                 ranges = None
             else:  # read each peer only inside its footprint rows (the rest of its partial is clear)
                 ptrs, ranges = [], []
                 for s in order:
                     c = clip_rows(rows, bands[s])
                     if c:
-                        ptrs.append(self.peer_partials[s] + 16 * c[0] * self.W)
+                        ptrs.append(self.peer_partials[s] + self.px * c[0] * self.W)
                         ranges.append(((c[0] - rows[0]) * self.W, (c[1] - rows[0]) * self.W))
                 if not ptrs:
                     ptrs, ranges = [self.peer_partials[ep.rank]], [(0, 0)]
             dev.composite_ptrs(self.index, ptrs, npix, background, rgb8_ptr=self.root_frame + 3 * off,
-                               rgba_ptr=(self.root_rgba + 16 * off) if keep_float else 0, ranges=ranges)
+                               rgba_ptr=(self.root_rgba + 16 * off) if keep_float else 0, ranges=ranges,
+                               half=self.fdt == torch.float16)
         ep.device_barrier()  # every tile has landed in rank 0's frame
         if bands is None:
-            self.last_bytes = 16 * npix * (ep.R - 1) + (3 * npix if ep.rank else 0)
+            self.last_bytes = self.px * npix * (ep.R - 1) + (3 * npix if ep.rank else 0)
         else:
             read = sum((c[1] - c[0]) * self.W for s in range(ep.R) if s != ep.rank
                        for c in [clip_rows(rows, bands[s])] if c)
-            self.last_bytes = 16 * read + (3 * npix if ep.rank else 0)
+            self.last_bytes = self.px * read + (3 * npix if ep.rank else 0)
         if ep.rank != 0:
             return CompositeOutput(None, None)
         frame = self.frame.tensor.view(self.H, self.W, 3)

@@ -19,6 +19,7 @@ from paper_2501_01628_b200.volume import (Decomposition, FieldSpec, TransferFunc
 RGBA_ATOL = 2e-3
 RGBA_MEAN_ATOL = 5e-5
 RGB8_MAX_LSB = 1
+RGBA_ATOL_F16 = 4e-3  # fp16 fragments: <= P * 2^-11 per channel before blending (P <= 8)
 
 
 def cam_array(cam: CameraSpec) -> np.ndarray:

@@ -22,9 +22,9 @@ class TorchBlender:
 
     @staticmethod
     def _over(frags):
-        acc = frags[0].view(-1, 4).clone()
+        acc = frags[0].view(-1, 4).float().clone()
         for f in frags[1:]:
-            acc = acc + (1.0 - acc[:, 3:4]) * f.view(-1, 4)
+            acc = acc + (1.0 - acc[:, 3:4]) * f.view(-1, 4).float()
         return acc
 
     def over(self, frags, out_rgba):
@@ -35,7 +35,7 @@ class TorchBlender:
             full = []
             for f, (lo, hi) in zip(frags, ranges):
                 t = torch.zeros(npix * 4, dtype=torch.float32)
-                t[lo * 4: hi * 4] = f.view(-1)[: (hi - lo) * 4]
+                t[lo * 4: hi * 4] = f.view(-1)[: (hi - lo) * 4].float()
                 full.append(t)
             frags = full
         acc = self._over(frags)
@@ -124,6 +124,31 @@ def test_band_clipped_direct_send_equals_full_exchange(P):
     img = rgba.reshape(H, W, 4).astype(np.float64)
     assert np.abs(img[..., :3] + (1 - img[..., 3:4]) * np.asarray(bg) - ref).max() < 1e-5
     assert sum(r[3] for r in res) < sum(r[4] for r in res)
+
+
+def _half_body(ep, W, H, order, bg):
+    parts = _partials(ep.R, W, H)
+    mine = torch.from_numpy(parts[ep.rank].reshape(-1).copy()).half()
+    comp = Compositor(ep, W, H, "direct_send", torch.device("cpu"), blender=TorchBlender(),
+                      fragment_dtype=torch.float16)
+    out = comp.composite(mine, order, bg, keep_float=True)
+    return (out.rgba.numpy().copy() if ep.rank == 0 else None), comp.last_bytes
+
+
+def test_fp16_fragments_direct_send():
+    """fp16 fragments move half the bytes; the blend of the rounded fragments matches the oracle composite
+    of the same rounded data."""
+    P, W, H = 3, 16, 11
+    order = [2, 0, 1]
+    bg = (0.1, 0.2, 0.3)
+    res = run_ranks(P, _half_body, W, H, order, bg)
+    parts = _partials(P, W, H).astype(np.float16).astype(np.float64)
+    ref = oracle.composite(list(parts), order, bg)
+    rgba = res[0][0].reshape(H, W, 4).astype(np.float64)
+    assert np.abs(rgba[..., :3] + (1 - rgba[..., 3:4]) * np.asarray(bg) - ref).max() < 1e-5
+    with pytest.raises(Exception, match="fp16"):
+        fake_ep = type("Ep", (), {"R": 2, "rank": 0})()
+        Compositor(fake_ep, W, H, "binary_swap", torch.device("cpu"), fragment_dtype=torch.float16)
 
 
 def test_direct_send_plan_covers_every_block_once():

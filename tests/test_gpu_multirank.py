@@ -250,3 +250,32 @@ def test_ray_cycling_matches_oracle(cuda_device, oracle_lib, R):
         q = rgb8.astype(np.int16) - oracle.tone_map_rgb8(want).astype(np.int16)
         assert np.abs(q).max() <= RGB8_MAX_LSB
     assert np.abs(res[0][2][0] - res[0][3][0]).max() < 1e-5  # no ERT: cycling == sort-last
+
+
+@pytest.mark.parametrize("mode,R", [("direct_send", 2), ("p2p", 4), ("auto", 3)])
+def test_fp16_fragment_frames(cuda_device, oracle_lib, mode, R):
+    """fragment_dtype='f16' halves the exchanged bytes; the frame stays within the fp16 tolerance of the
+    oracle (RGBA_ATOL_F16: each fragment channel carries <= 2^-12 relative rounding; RGB8 within 2 LSB)."""
+    from scenes import RGBA_ATOL_F16
+
+    s = c1(P=R, W=144, H=104)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, _ = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, s.W, s.H)
+    want = oracle.composite(ref, s.dec.visibility_order(s.cam.position), s.background)
+
+    def body(ep):
+        b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda_device).generate(s.field)
+        vr = VolumeRenderer(ep, b, s.dec, s.tf, s.background)
+        out = []
+        for fdt in ("f16", "f32"):
+            res = vr.render(s.cam, s.W, s.H, RenderOptions(composite=mode, keep_float=True, fragment_dtype=fdt))
+            torch.cuda.synchronize()
+            out.append((res.image, None if res.rgb8 is None else res.rgb8.cpu().numpy(), res.stats.bytes_exchanged))
+        return out
+
+    res = run_collective(R, body, device=cuda_device)
+    (img16, rgb16, _), (img32, _, _) = res[0]
+    assert np.abs(img16 - want).max() <= RGBA_ATOL_F16
+    assert np.abs(rgb16.astype(np.int16) - oracle.tone_map_rgb8(want).astype(np.int16)).max() <= 2
+    assert np.abs(img16 - img32).max() <= RGBA_ATOL_F16
+    assert sum(r[0][2] for r in res) < sum(r[1][2] for r in res)

@@ -345,3 +345,41 @@ def test_render_stats_device_times_and_samples(cuda_device, oracle_lib):
     with pytest.raises(UsageError, match="timing"):
         vr.render(s.cam, s.W, s.H, RenderOptions()).stats.device_times()
     b.close()
+
+
+def test_fp16_fragments_march_and_composite(cuda_device, oracle_lib):
+    """fp16 fragments: the march's fp16 partial is its f32 partial rounded to nearest (bit for bit), and
+    the composite of fp16 fragments equals the f32 composite of the same rounded values (bit for bit)."""
+    s = c1(P=2, W=101, H=77)
+    dtf = dev.DeviceTF(s.tf, cuda_device)
+    n = s.W * s.H
+    f32, f16 = [], []
+    for r in range(2):
+        b = dev.DeviceBrick(s.dec.brick(r), cuda_device).generate(s.field)
+        p32 = torch.empty(n * 4, dtype=torch.float32, device=cuda_device)
+        p16 = torch.empty(n * 4, dtype=torch.float16, device=cuda_device)
+        dev.march(b, s.cam, dtf, s.dt, s.ert, p32, s.W, s.H)
+        dev.march(b, s.cam, dtf, s.dt, s.ert, p16, s.W, s.H)
+        torch.cuda.synchronize()
+        assert torch.equal(p16, p32.half())
+        f32.append(p32)
+        f16.append(p16)
+        b.close()
+    bg = (0.2, 0.1, 0.3)
+    outs = []
+    for frags in ([f.half().float() for f in f32], f16):
+        rgb8 = torch.empty(n * 3, dtype=torch.uint8, device=cuda_device)
+        rgba = torch.empty(n * 4, dtype=torch.float32, device=cuda_device)
+        dev.composite(frags, bg, rgb8=rgb8, rgba=rgba)
+        outs.append((rgb8, rgba))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    # ranged fp16 (odd offsets: 8-byte loads) == ranged f32 of the same values
+    ranges = [(3, n - 5), (0, n)]
+    r32 = [f32[0].half().float()[12: (n - 5) * 4], f32[1].half().float()]
+    r16 = [f16[0][12: (n - 5) * 4], f16[1]]
+    res = []
+    for frags in (r32, r16):
+        rgba = torch.empty(n * 4, dtype=torch.float32, device=cuda_device)
+        dev.composite(frags, None, rgba=rgba, ranges=ranges, npix=n)
+        res.append(rgba)
+    assert torch.equal(res[0], res[1])
