@@ -16,7 +16,7 @@ from scenes import RGB8_MAX_LSB, RGBA_ATOL, c1, oracle_partials
 pytestmark = pytest.mark.gpu
 
 
-def _rank_body(ep, mode, W, H):
+def _rank_body(ep, mode, W, H, fdt="f32"):
     import torch
 
     from paper_2501_01628_b200 import device as dev
@@ -30,7 +30,8 @@ def _rank_body(ep, mode, W, H):
     vr = VolumeRenderer(ep, b, s.dec, s.tf, s.background)
     out = []
     for frame in range(2):
-        res = vr.render(s.cam, W, H, RenderOptions(composite=mode, keep_float=True, frame_index=frame))
+        res = vr.render(s.cam, W, H, RenderOptions(composite=mode, keep_float=True, frame_index=frame,
+                                                   fragment_dtype=fdt))
         torch.cuda.synchronize()
         out.append((None if res.image is None else np.asarray(res.image),
                     None if res.rgb8 is None else res.rgb8.cpu().numpy()))
@@ -40,10 +41,13 @@ def _rank_body(ep, mode, W, H):
     return used, out
 
 
-@pytest.mark.parametrize("mode,R", [("p2p", 2), ("auto", 3)])
-def test_ipc_p2p_frame_across_processes(cuda_device, oracle_lib, mode, R):
+@pytest.mark.parametrize("mode,R,fdt", [("p2p", 2, "f32"), ("auto", 3, "f32"), ("p2p", 2, "f16")])
+def test_ipc_p2p_frame_across_processes(cuda_device, oracle_lib, mode, R, fdt):
+    from scenes import RGBA_ATOL_F16
+
     W, H = 160, 122
-    results = run_ranks(R, _rank_body, mode, W, H, timeout=240.0)
+    tol, lsb = (RGBA_ATOL, RGB8_MAX_LSB) if fdt == "f32" else (RGBA_ATOL_F16, 2)
+    results = run_ranks(R, _rank_body, mode, W, H, fdt, timeout=240.0)
     s = c1(P=R, W=W, H=H)
     vox = oracle.generate_field(s.field.dims, s.field.blobs)
     ref, _ = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, W, H)
@@ -52,14 +56,15 @@ def test_ipc_p2p_frame_across_processes(cuda_device, oracle_lib, mode, R):
         assert used == "p2p", f"rank {r} fell back to {used}: the IPC mapping failed"
         for image, rgb8 in frames:
             if r == 0:
-                assert np.abs(image - want).max() <= RGBA_ATOL
+                assert np.abs(image - want).max() <= tol
                 q = rgb8.astype(np.int16) - oracle.tone_map_rgb8(want).astype(np.int16)
-                assert np.abs(q).max() <= RGB8_MAX_LSB
+                assert np.abs(q).max() <= lsb
             else:
                 assert image is None and rgb8 is None
 
 
-def test_bench_multi_rank_code_path(tmp_path):
+@pytest.mark.parametrize("fragments", ["f32", "f16"])
+def test_bench_multi_rank_code_path(tmp_path, fragments):
     """bench.py's N > 1 leg (weak-scaled bricks, compositor roofline, e2e, max over ranks) run as two
     torchrun processes on this box's one GPU with the gloo control plane (DPRT_BENCH_BACKEND=gloo): a
     functional check of the code the 8-GPU scaling run executes, not a measurement."""
@@ -73,7 +78,7 @@ def test_bench_multi_rank_code_path(tmp_path):
     env = dict(os.environ, DPRT_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", str(root / "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "3"]
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--fragments", fragments]
     p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
@@ -81,4 +86,4 @@ def test_bench_multi_rank_code_path(tmp_path):
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["compositor_roofline"]["mode"] in ("p2p", "direct_send")
-    assert line["config"]["bricks"] == 2
+    assert line["config"]["bricks"] == 2 and line["config"]["fragments"] == fragments
