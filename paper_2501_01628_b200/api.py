@@ -56,7 +56,8 @@ _PARAMS: Dict[str, Dict[str, object]] = {
     "camera": {"position": (0.0, 0.0, 3.0), "direction": (0.0, 0.0, -1.0),
                "up": (0.0, 1.0, 0.0), "fovY": 60.0, "aspect": 1.0},
     "renderer": {"background": (0.0, 0.0, 0.0), "dt": 1.0, "ert": 0.99, "composite": "auto",
-                 "skipEmpty": True, "disableCompositing": False, "mode": "dvr"},
+                 "skipEmpty": True, "disableCompositing": False, "mode": "dvr", "clipExchange": True,
+                 "fragments": "f32"},
     "frame": {"world": None, "camera": None, "renderer": None, "size": (256, 256)},
 }
 
@@ -364,7 +365,8 @@ def render_frame_collective(frame: Frame) -> RenderResult:
     r = renderer.committed
     options = RenderOptions(dt=float(r["dt"]), ert=float(r["ert"]), composite=str(r["composite"]),
                             skip_empty=bool(r["skipEmpty"]), disable_compositing=bool(r["disableCompositing"]),
-                            frame_index=frame.sequence, mode=str(r["mode"]))
+                            frame_index=frame.sequence, mode=str(r["mode"]), clip_exchange=bool(r["clipExchange"]),
+                            fragment_dtype=str(r["fragments"]))
     background = tuple(float(v) for v in r["background"])
     tf = world.volume.committed["transferFunction"].tf()
     vr = frame._renderer
