@@ -354,6 +354,44 @@ constexpr int kSlabShift = DPRT_SLAB_SHIFT;
 
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
+// Background RGB8 for every pixel outside the footprint rectangle (grid-stride over 4-pixel groups; a
+// group straddling the rectangle's edge writes only its outside pixels -- the beams own the inside).
+__device__ void fill_outside_rect(const MarchArgs& a) {
+    const uint32_t cr = (uint32_t)floorf(fminf(fmaxf(a.bg[0], 0.f), 1.f) * 255.f + 0.5f);
+    const uint32_t cg = (uint32_t)floorf(fminf(fmaxf(a.bg[1], 0.f), 1.f) * 255.f + 0.5f);
+    const uint32_t cb = (uint32_t)floorf(fminf(fmaxf(a.bg[2], 0.f), 1.f) * 255.f + 0.5f);
+    const int W = a.W, npix = a.W * a.H;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; 4 * q < npix; q += gridDim.x * blockDim.x) {
+        const int i0 = 4 * q, y0 = i0 / W, x0 = i0 - y0 * W;
+        bool out[4], all = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int x = x0 + k, y = y0;
+            if (x >= W) {  // the group wraps into the next row
+                x -= W;
+                ++y;
+            }
+            out[k] = i0 + k < npix && (y < a.rect[1] || y >= a.rect[3] || x < a.rect[0] || x >= a.rect[2]);
+            all = all && out[k];
+        }
+        uint8_t* dst = a.rgb8 + 3 * (size_t)i0;
+        if (all && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+            uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+            d32[0] = cr | (cg << 8) | (cb << 16) | (cr << 24);
+            d32[1] = cg | (cb << 8) | (cr << 16) | (cg << 24);
+            d32[2] = cb | (cr << 8) | (cg << 16) | (cb << 24);
+            continue;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!out[k]) continue;
+            dst[3 * k] = (uint8_t)cr;
+            dst[3 * k + 1] = (uint8_t)cg;
+            dst[3 * k + 2] = (uint8_t)cb;
+        }
+    }
+}
+
 #ifndef DPRT_BEAM_MINBLOCKS
 #define DPRT_BEAM_MINBLOCKS 3
 #endif
@@ -387,6 +425,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
+    if (a.rgb8) fill_outside_rect(a);  // fused background fill of the pixels no beam covers
     while (true) {
         int tile = 0;
         if (lane == 0) tile = atomicAdd(a.counters + 1, 1);
@@ -396,7 +435,8 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
         const int py = a.rect[1] + (tile / tiles_x) * kBeamH + (lane / kBeamW);
         int nn = 0, pix = 0;
         float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
-        if (px < a.rect[2] && py < a.rect[3]) {
+        const bool inside = px < a.rect[2] && py < a.rect[3];
+        if (inside) {
             // exact f64 ray setup for this lane's pixel, fused
             pix = py * a.W + px;
             double d[3];
@@ -416,7 +456,14 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
             }
         }
         const unsigned hitm = __ballot_sync(FULL, nn > 0);
-        if (!hitm) continue;
+        if (!hitm) {
+            if (a.rgb8 && inside) {  // no ray of this beam meets the brick: background (tone-mapped)
+                uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) dst[c] = (uint8_t)floorf(fminf(fmaxf(a.bg[c], 0.f), 1.f) * 255.f + 0.5f);
+            }
+            continue;
+        }
 #if DPRT_COUNTERS
         c_rays += nn > 0;
 #endif
@@ -602,15 +649,18 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
             }
             if (j >= nn) live = false;
         }
-        if (nn > 0) {
-            if (a.rgb8) {
-                // single-rank frame: the over-background + tone map of the compositor, fused (engine.py:500-502)
+        if (a.rgb8) {
+            if (inside) {
+                // single-rank frame: the over-background + tone map of the compositor, fused
+                // (engine.py:500-502); a miss inside the footprint is the background itself
                 const float one = 1.f - A;
                 uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
                 dst[0] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[0], C0), 0.f), 1.f) * 255.f + 0.5f);
                 dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
                 dst[2] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[2], C2), 0.f), 1.f) * 255.f + 0.5f);
-            } else if (a.half_out) {
+            }
+        } else if (nn > 0) {
+            if (a.half_out) {
                 const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
                 a.out16[pix - a.pix0] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
                                                    *reinterpret_cast<const unsigned*>(&ba));
@@ -691,32 +741,6 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
     return cudaMemcpyAsync(b.skipd, tmp, (size_t)nmc, cudaMemcpyDeviceToDevice, stream);
 }
 
-// Background frame for the fused single-rank path: tone_map(bg) in every pixel, 4 pixels per thread.
-__global__ void fill_rgb8_kernel(uint8_t* __restrict__ rgb8, long long npix, float r, float g, float b) {
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long i0 = 4 * q;
-    if (i0 >= npix) return;
-    const uint32_t cr = (uint32_t)floorf(fminf(fmaxf(r, 0.f), 1.f) * 255.f + 0.5f);
-    const uint32_t cg = (uint32_t)floorf(fminf(fmaxf(g, 0.f), 1.f) * 255.f + 0.5f);
-    const uint32_t cb = (uint32_t)floorf(fminf(fmaxf(b, 0.f), 1.f) * 255.f + 0.5f);
-    uint8_t* dst = rgb8 + 3 * i0;
-    if (i0 + 4 <= npix && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
-        const uint32_t w0 = cr | (cg << 8) | (cb << 16) | (cr << 24);
-        const uint32_t w1 = cg | (cb << 8) | (cr << 16) | (cg << 24);
-        const uint32_t w2 = cb | (cr << 8) | (cg << 16) | (cb << 24);
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-        d32[0] = w0;
-        d32[1] = w1;
-        d32[2] = w2;
-        return;
-    }
-    for (long long i = i0; i < npix && i < i0 + 4; ++i) {
-        rgb8[3 * i] = (uint8_t)cr;
-        rgb8[3 * i + 1] = (uint8_t)cg;
-        rgb8[3 * i + 2] = (uint8_t)cb;
-    }
-}
-
 cudaError_t read_counters(unsigned long long out[4], int reset) {
 #if DPRT_COUNTERS
     cudaError_t e = cudaMemcpyFromSymbol(out, g_counters, 4 * sizeof(unsigned long long));
@@ -751,10 +775,7 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
         // pixels the beams do not write (misses, outside the footprint) must read as zero -- or as the
         // tone-mapped background when the beams write the RGB8 frame directly
         if (a.rgb8) {
-            const long long quads = ((long long)a.W * a.H + 3) / 4;
-            fill_rgb8_kernel<<<(unsigned)((quads + 255) / 256), 256, 0, stream>>>(a.rgb8, (long long)a.W * a.H,
-                                                                              a.bg[0], a.bg[1], a.bg[2]);
-            e = cudaGetLastError();
+            e = cudaSuccess;  // the beam kernel fills the background itself (fill_outside_rect)
         } else if (a.accum) {
             e = cudaSuccess;  // the buffer holds the rays' accumulated state
         } else if (a.band_clear) {

@@ -383,3 +383,22 @@ def test_fp16_fragments_march_and_composite(cuda_device, oracle_lib):
         dev.composite(frags, None, rgba=rgba, ranges=ranges, npix=n)
         res.append(rgba)
     assert torch.equal(res[0], res[1])
+
+
+def test_fused_frame_writes_every_pixel(cuda_device, oracle_lib):
+    """dprt_march_rgb8 owns the whole frame: pixels outside the footprint, beams that miss the brick and
+    misses inside it all get the tone-mapped background (the buffer starts as garbage)."""
+    s = c1(P=1, W=203, H=151)
+    b = dev.DeviceBrick(s.dec.brick(0), cuda_device).generate(s.field)
+    dtf = dev.DeviceTF(s.tf, cuda_device)
+    n = s.W * s.H
+    for cam in (s.cam, orbit_camera(s.field.bounds().center(), 300.0, 0.4, 0.2, 20.0, s.W / s.H)):
+        frame = torch.full((n * 3,), 0xAB, dtype=torch.uint8, device=cuda_device)
+        dev.march_rgb8(b, cam, dtf, s.dt, s.ert, s.background, frame, s.W, s.H)
+        p = torch.empty(n * 4, dtype=torch.float32, device=cuda_device)
+        dev.march(b, cam, dtf, s.dt, s.ert, p, s.W, s.H)
+        ref = torch.empty(n * 3, dtype=torch.uint8, device=cuda_device)
+        dev.composite([p], s.background, rgb8=ref)
+        torch.cuda.synchronize()
+        assert torch.equal(frame, ref)
+    b.close()
