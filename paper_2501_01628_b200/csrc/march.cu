@@ -354,41 +354,68 @@ constexpr int kSlabShift = DPRT_SLAB_SHIFT;
 
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
-// Background RGB8 for every pixel outside the footprint rectangle (grid-stride over 4-pixel groups; a
-// group straddling the rectangle's edge writes only its outside pixels -- the beams own the inside).
-__device__ void fill_outside_rect(const MarchArgs& a) {
+// The pixels no beam covers -- rows [y0, y1) outside the footprint rectangle -- get their "nothing here"
+// value inside the march kernel itself (no separate fill or memset pass): the tone-mapped background for
+// the fused RGB8 frame, a clear fragment (0) for an RGBA partial.  Grid-stride over 4-pixel groups; a
+// group straddling the rectangle's edge writes only its outside pixels (the beams own the inside).
+__device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1) {
     const uint32_t cr = (uint32_t)floorf(fminf(fmaxf(a.bg[0], 0.f), 1.f) * 255.f + 0.5f);
     const uint32_t cg = (uint32_t)floorf(fminf(fmaxf(a.bg[1], 0.f), 1.f) * 255.f + 0.5f);
     const uint32_t cb = (uint32_t)floorf(fminf(fmaxf(a.bg[2], 0.f), 1.f) * 255.f + 0.5f);
-    const int W = a.W, npix = a.W * a.H;
+    const int W = a.W, first = y0 * W, npix = (y1 - y0) * W;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; 4 * q < npix; q += gridDim.x * blockDim.x) {
-        const int i0 = 4 * q, y0 = i0 / W, x0 = i0 - y0 * W;
+        const int i0 = first + 4 * q, yy = i0 / W, x0 = i0 - yy * W;
         bool out[4], all = true;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            int x = x0 + k, y = y0;
+            int x = x0 + k, y = yy;
             if (x >= W) {  // the group wraps into the next row
                 x -= W;
                 ++y;
             }
-            out[k] = i0 + k < npix && (y < a.rect[1] || y >= a.rect[3] || x < a.rect[0] || x >= a.rect[2]);
+            out[k] = 4 * q + k < npix && (y < a.rect[1] || y >= a.rect[3] || x < a.rect[0] || x >= a.rect[2]);
             all = all && out[k];
         }
-        uint8_t* dst = a.rgb8 + 3 * (size_t)i0;
-        if (all && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
-            uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-            d32[0] = cr | (cg << 8) | (cb << 16) | (cr << 24);
-            d32[1] = cg | (cb << 8) | (cr << 16) | (cg << 24);
-            d32[2] = cb | (cr << 8) | (cg << 16) | (cb << 24);
-            continue;
-        }
+        if (a.rgb8) {
+            uint8_t* dst = a.rgb8 + 3 * (size_t)i0;
+            if (all && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+                d32[0] = cr | (cg << 8) | (cb << 16) | (cr << 24);
+                d32[1] = cg | (cb << 8) | (cr << 16) | (cg << 24);
+                d32[2] = cb | (cr << 8) | (cg << 16) | (cb << 24);
+                continue;
+            }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (!out[k]) continue;
-            dst[3 * k] = (uint8_t)cr;
-            dst[3 * k + 1] = (uint8_t)cg;
-            dst[3 * k + 2] = (uint8_t)cb;
+            for (int k = 0; k < 4; ++k) {
+                if (!out[k]) continue;
+                dst[3 * k] = (uint8_t)cr;
+                dst[3 * k + 1] = (uint8_t)cg;
+                dst[3 * k + 2] = (uint8_t)cb;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!out[k]) continue;
+                const long long i = (long long)i0 + k - a.pix0;
+                if (a.half_out)
+                    a.out16[i] = make_uint2(0u, 0u);
+                else
+                    a.out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
+    }
+}
+
+// A pixel inside the footprint whose ray adds nothing (no owned sample, or a beam that misses the brick).
+__device__ __forceinline__ void write_clear(const MarchArgs& a, int pix) {
+    if (a.rgb8) {
+        uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dst[c] = (uint8_t)floorf(fminf(fmaxf(a.bg[c], 0.f), 1.f) * 255.f + 0.5f);
+    } else if (a.half_out) {
+        a.out16[pix - a.pix0] = make_uint2(0u, 0u);
+    } else {
+        a.out[pix - a.pix0] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -425,7 +452,11 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
-    if (a.rgb8) fill_outside_rect(a);  // fused background fill of the pixels no beam covers
+    if (!a.accum) {  // fused clear / background of the pixels no beam covers (no memset pass)
+        const int y0 = a.band_clear ? a.rect[1] : (int)(a.pix0 / a.W);
+        const int y1 = a.band_clear ? a.rect[3] : (int)((a.pix0 + a.npix_buf) / a.W);
+        fill_outside_rect(a, y0, y1);
+    }
     while (true) {
         int tile = 0;
         if (lane == 0) tile = atomicAdd(a.counters + 1, 1);
@@ -457,11 +488,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
         }
         const unsigned hitm = __ballot_sync(FULL, nn > 0);
         if (!hitm) {
-            if (a.rgb8 && inside) {  // no ray of this beam meets the brick: background (tone-mapped)
-                uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) dst[c] = (uint8_t)floorf(fminf(fmaxf(a.bg[c], 0.f), 1.f) * 255.f + 0.5f);
-            }
+            if (inside && !a.accum) write_clear(a, pix);  // no ray of this beam meets the brick
             continue;
         }
 #if DPRT_COUNTERS
@@ -649,8 +676,8 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
             }
             if (j >= nn) live = false;
         }
-        if (a.rgb8) {
-            if (inside) {
+        if (inside && (nn > 0 || !a.accum)) {  // accumulated state of a skipped ray stays as it was
+            if (a.rgb8) {
                 // single-rank frame: the over-background + tone map of the compositor, fused
                 // (engine.py:500-502); a miss inside the footprint is the background itself
                 const float one = 1.f - A;
@@ -658,9 +685,7 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                 dst[0] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[0], C0), 0.f), 1.f) * 255.f + 0.5f);
                 dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
                 dst[2] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[2], C2), 0.f), 1.f) * 255.f + 0.5f);
-            }
-        } else if (nn > 0) {
-            if (a.half_out) {
+            } else if (a.half_out) {
                 const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
                 a.out16[pix - a.pix0] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
                                                    *reinterpret_cast<const unsigned*>(&ba));
@@ -772,23 +797,10 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = 2 * a.n_tf * sizeof(float4);
     if (a.beam) {
-        // pixels the beams do not write (misses, outside the footprint) must read as zero -- or as the
-        // tone-mapped background when the beams write the RGB8 frame directly
-        if (a.rgb8) {
-            e = cudaSuccess;  // the beam kernel fills the background itself (fill_outside_rect)
-        } else if (a.accum) {
-            e = cudaSuccess;  // the buffer holds the rays' accumulated state
-        } else if (a.band_clear) {
-            // the caller reads only the footprint's row band (band-clipped compositing)
-            const size_t px = a.half_out ? sizeof(uint2) : sizeof(float4);
-            char* base = a.half_out ? reinterpret_cast<char*>(a.out16) : reinterpret_cast<char*>(a.out);
-            e = cudaMemsetAsync(base + ((size_t)a.rect[1] * a.W - a.pix0) * px, 0,
-                                (size_t)(a.rect[3] - a.rect[1]) * a.W * px, stream);
-        } else {
-            e = a.half_out ? cudaMemsetAsync(a.out16, 0, (size_t)a.npix_buf * sizeof(uint2), stream)
-                           : cudaMemsetAsync(a.out, 0, (size_t)a.npix_buf * sizeof(float4), stream);
-        }
-        if (e == cudaSuccess && a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
+        // no clear pass: the beam kernel itself writes every pixel it is responsible for -- zero (RGBA
+        // partial) or the tone-mapped background (RGB8 frame) outside the footprint and for misses
+        // (fill_outside_rect, write_clear); accumulation leaves the rays' state alone
+        if (a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kBeamBlock, smem);
         if (per_sm < 1) per_sm = 1;
