@@ -18,6 +18,7 @@ ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--no-skip", action="store_true")
 ap.add_argument("--threshold", type=float, default=0.1)
 ap.add_argument("--field", choices=["blobs", "ml"], default="blobs")
+ap.add_argument("--rgb8", action="store_true", help="time dprt_march_rgb8 (the single-rank bench step)")
 args = ap.parse_args()
 d = torch.device("cuda", 0)
 if args.field == "ml":
@@ -37,13 +38,23 @@ dev.march(b, cam, dtf, 1.0, 0.99, p, args.W, args.H, samples=s, skip=not args.no
 torch.cuda.synchronize()
 owned = int(s.sum().item())
 hit = int((s > 0).sum().item())
+frame = torch.empty(args.W * args.H * 3, dtype=torch.uint8, device=d)
+
+
+def step():
+    if args.rgb8:
+        dev.march_rgb8(b, cam, dtf, 1.0, 0.99, (0.05, 0.06, 0.08), frame, args.W, args.H, skip=not args.no_skip)
+    else:
+        dev.march(b, cam, dtf, 1.0, 0.99, p, args.W, args.H, skip=not args.no_skip)
+
+
 for _ in range(3):
-    dev.march(b, cam, dtf, 1.0, 0.99, p, args.W, args.H, skip=not args.no_skip)
+    step()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize()
 e0.record()
 for _ in range(args.iters):
-    dev.march(b, cam, dtf, 1.0, 0.99, p, args.W, args.H, skip=not args.no_skip)
+    step()
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / args.iters
