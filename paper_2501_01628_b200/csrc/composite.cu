@@ -128,11 +128,47 @@ __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
     }
 }
 
+// Small tiles (a rank's row block after the exchange): one pixel per thread, so the grid still fills the
+// 148 SMs, with up to 8 fragments' loads issued before the first is blended.
+template <bool kHalf>
+__global__ void __launch_bounds__(256) composite_px_kernel(const CompositeArgs a) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.npix) return;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p0 = 0; p0 < a.P; p0 += 8) {
+        float4 f[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int p = p0 + k;
+            f[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p < a.P && i >= a.lo[p] && i < a.hi[p]) f[k] = load1<kHalf>(a.in[p], i - a.lo[p]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) over(acc, f[k]);
+    }
+    if (a.flags & DPRT_COMPOSITE_RGBA) a.rgba[i] = acc;
+    if (a.flags & DPRT_COMPOSITE_TONEMAP)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) a.rgb8[3 * i + ch] = (uint8_t)pack_rgb8(acc, a.bg, ch);
+}
+
+#ifndef DPRT_COMPOSITE_PX_BELOW
+#define DPRT_COMPOSITE_PX_BELOW (1 << 22)  // tiles below this many pixels blending >= 3 fragments use one
+#endif                                     // pixel per thread (graph-timed sweep, profiles/r01_composite_sweep.md)
+
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream) {
-    const long long threads = (a.npix + 3) / 4;
     const int block = 256;
+    if (a.npix == 0) return cudaSuccess;
+    if (a.npix < DPRT_COMPOSITE_PX_BELOW && a.P >= 3) {
+        const long long grid = (a.npix + block - 1) / block;
+        if (a.flags & DPRT_COMPOSITE_HALF_IN)
+            composite_px_kernel<true><<<(unsigned)grid, block, 0, stream>>>(a);
+        else
+            composite_px_kernel<false><<<(unsigned)grid, block, 0, stream>>>(a);
+        return cudaGetLastError();
+    }
+    const long long threads = (a.npix + 3) / 4;
     const long long grid = (threads + block - 1) / block;
-    if (grid == 0) return cudaSuccess;
     if (a.flags & DPRT_COMPOSITE_HALF_IN)
         composite_kernel<true><<<(unsigned)grid, block, 0, stream>>>(a);
     else
