@@ -356,51 +356,47 @@ __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int
 
 // The pixels no beam covers -- rows [y0, y1) outside the footprint rectangle -- get their "nothing here"
 // value inside the march kernel itself (no separate fill or memset pass): the tone-mapped background for
-// the fused RGB8 frame, a clear fragment (0) for an RGBA partial.  Grid-stride over 4-pixel groups; a
-// group straddling the rectangle's edge writes only its outside pixels (the beams own the inside).
-__device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1) {
+// the fused RGB8 frame, a clear fragment (0) for an RGBA partial.  Blocks take whole rows, threads 4-pixel
+// groups; a group straddling the rectangle's edge writes only its outside pixels (the beams own the inside).
+__device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1, int unit, int nunits, int t, int nt) {
     const uint32_t cr = (uint32_t)floorf(fminf(fmaxf(a.bg[0], 0.f), 1.f) * 255.f + 0.5f);
     const uint32_t cg = (uint32_t)floorf(fminf(fmaxf(a.bg[1], 0.f), 1.f) * 255.f + 0.5f);
     const uint32_t cb = (uint32_t)floorf(fminf(fmaxf(a.bg[2], 0.f), 1.f) * 255.f + 0.5f);
-    const int W = a.W, first = y0 * W, npix = (y1 - y0) * W;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; 4 * q < npix; q += gridDim.x * blockDim.x) {
-        const int i0 = first + 4 * q, yy = i0 / W, x0 = i0 - yy * W;
-        bool out[4], all = true;
+    const int W = a.W, qpr = (W + 3) / 4;  // 4-pixel groups per row (no index division: rows per block)
+    for (int y = y0 + unit; y < y1; y += nunits) {
+        const bool row_out = y < a.rect[1] || y >= a.rect[3];
+        for (int q = t; q < qpr; q += nt) {
+            const int x0 = 4 * q;
+            if (!row_out && x0 >= a.rect[0] && x0 + 4 <= a.rect[2]) continue;  // inside: the beams' pixels
+            const long long i0 = (long long)y * W + x0;
+            if (a.rgb8) {
+                uint8_t* dst = a.rgb8 + 3 * i0;
+                const bool all = x0 + 4 <= W && (row_out || x0 + 4 <= a.rect[0] || x0 >= a.rect[2]);
+                if (all && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+                    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+                    d32[0] = cr | (cg << 8) | (cb << 16) | (cr << 24);
+                    d32[1] = cg | (cb << 8) | (cr << 16) | (cg << 24);
+                    d32[2] = cb | (cr << 8) | (cg << 16) | (cb << 24);
+                    continue;
+                }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            int x = x0 + k, y = yy;
-            if (x >= W) {  // the group wraps into the next row
-                x -= W;
-                ++y;
-            }
-            out[k] = 4 * q + k < npix && (y < a.rect[1] || y >= a.rect[3] || x < a.rect[0] || x >= a.rect[2]);
-            all = all && out[k];
-        }
-        if (a.rgb8) {
-            uint8_t* dst = a.rgb8 + 3 * (size_t)i0;
-            if (all && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
-                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-                d32[0] = cr | (cg << 8) | (cb << 16) | (cr << 24);
-                d32[1] = cg | (cb << 8) | (cr << 16) | (cg << 24);
-                d32[2] = cb | (cr << 8) | (cg << 16) | (cb << 24);
-                continue;
-            }
+                for (int k = 0; k < 4; ++k) {
+                    const int x = x0 + k;
+                    if (x >= W || (!row_out && x >= a.rect[0] && x < a.rect[2])) continue;
+                    dst[3 * k] = (uint8_t)cr;
+                    dst[3 * k + 1] = (uint8_t)cg;
+                    dst[3 * k + 2] = (uint8_t)cb;
+                }
+            } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (!out[k]) continue;
-                dst[3 * k] = (uint8_t)cr;
-                dst[3 * k + 1] = (uint8_t)cg;
-                dst[3 * k + 2] = (uint8_t)cb;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (!out[k]) continue;
-                const long long i = (long long)i0 + k - a.pix0;
-                if (a.half_out)
-                    a.out16[i] = make_uint2(0u, 0u);
-                else
-                    a.out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int k = 0; k < 4; ++k) {
+                    const int x = x0 + k;
+                    if (x >= W || (!row_out && x >= a.rect[0] && x < a.rect[2])) continue;
+                    if (a.half_out)
+                        a.out16[i0 + k - a.pix0] = make_uint2(0u, 0u);
+                    else
+                        a.out[i0 + k - a.pix0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
         }
     }
@@ -452,11 +448,6 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
-    if (!a.accum) {  // fused clear / background of the pixels no beam covers (no memset pass)
-        const int y0 = a.band_clear ? a.rect[1] : (int)(a.pix0 / a.W);
-        const int y1 = a.band_clear ? a.rect[3] : (int)((a.pix0 + a.npix_buf) / a.W);
-        fill_outside_rect(a, y0, y1);
-    }
     while (true) {
         int tile = 0;
         if (lane == 0) tile = atomicAdd(a.counters + 1, 1);
@@ -693,6 +684,14 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                 a.out[pix - a.pix0] = make_float4(C0, C1, C2, A);
             }
         }
+    }
+    if (!a.accum) {
+        // fused clear / background of the pixels no beam covers (no memset pass), done by each warp once
+        // the tile queue is empty, so it overlaps the slowest beams instead of delaying the first ones
+        const int y0 = a.band_clear ? a.rect[1] : (int)(a.pix0 / a.W);
+        const int y1 = a.band_clear ? a.rect[3] : (int)((a.pix0 + a.npix_buf) / a.W);
+        const int wpb = blockDim.x >> 5;
+        fill_outside_rect(a, y0, y1, (int)blockIdx.x * wpb + (tid >> 5), (int)gridDim.x * wpb, lane, 32);
     }
 #if DPRT_COUNTERS
     DPRT_COUNT(0, c_shade);

@@ -59,11 +59,18 @@ frags = [part[: rows * W * 4].clone() for _ in range(8)]
 rgb = torch.empty(rows * W * 3, dtype=torch.uint8, device=d)
 for _ in range(3):
     dev.composite(frags, (0.05, 0.06, 0.08), rgb8=rgb)
+# graph-timed: 20 launches per replay (no Python launch overhead in the kernel time)
+st = torch.cuda.Stream()
+st.wait_stream(torch.cuda.current_stream())
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    for _ in range(20):
+        dev.composite(frags, (0.05, 0.06, 0.08), rgb8=rgb)
+g.replay()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize()
 e0.record()
-for _ in range(20):
-    dev.composite(frags, (0.05, 0.06, 0.08), rgb8=rgb)
+g.replay()
 e1.record()
 torch.cuda.synchronize()
 out["composite_rank_ms"] = e0.elapsed_time(e1) / 20
