@@ -244,7 +244,7 @@ def render_brick(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.nd
 def render_brick_accum(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.ndarray, vmin: float,
                        vmax: float, dt: float, ert: float, width: int, height: int, state: np.ndarray,
                        rows: Tuple[int, int], nthreads: int = 0) -> None:
-    """Ray cycling (DESIGN.md §2.9): continue the accumulated state (H, W, 4) f64 of rows [r0, r1) through
+    """Ray cycling (DESIGN.md §2.10): continue the accumulated state (H, W, 4) f64 of rows [r0, r1) through
     one brick, in place (ERT on the accumulated alpha)."""
     vox = np.ascontiguousarray(vox, np.float32)
     if tuple(vox.shape) != tuple(reversed(brick.stored_dims)):
@@ -266,7 +266,7 @@ def render_brick_accum(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf:
 def cycle_frame(bricks_vox: Sequence[np.ndarray], bricks: Sequence[OracleBrick], order: Sequence[int],
                 row_blocks: Sequence[Tuple[int, int]], cam: np.ndarray, tf: np.ndarray, vmin: float, vmax: float,
                 dt: float, ert: float, width: int, height: int, background) -> np.ndarray:
-    """The ray-cycling frame (DESIGN.md §2.9), restated serially: the batch of rank b's rows starts at b's
+    """The ray-cycling frame (DESIGN.md §2.10), restated serially: the batch of rank b's rows starts at b's
     position p0 in the visibility order and visits positions p0, p0+1, ..., R-1 (back segment, state B)
     then 0, ..., p0-1 (front segment, state F); the frame is F over B over the background."""
     R = len(bricks)

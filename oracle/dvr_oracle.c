@@ -251,7 +251,7 @@ static void tf_lookup(const Brick* b, double v, double out[4]) {
 
 /* One pixel of one brick: returns the owned lattice sample count; rgba = premultiplied partial. */
 /* accum = 0: the brick's own partial from a clear ray (sort-last).  accum = 1: continue the ray's
- * accumulated state in rgba (ray cycling, DESIGN.md §2.9): ERT on the accumulated alpha, a ray already at
+ * accumulated state in rgba (ray cycling, DESIGN.md §2.10): ERT on the accumulated alpha, a ray already at
  * ERT adds nothing. */
 static int64_t march_pixel(const Brick* b, const double* cam, int px, int py, int W, int H, double rgba[4],
                            int accum) {
@@ -353,7 +353,7 @@ int dvr_oracle_render_brick(const float* vox, const int64_t* geo, const double* 
     return 0;
 }
 
-/* Ray cycling (DESIGN.md §2.9): continue the accumulated front-to-back state of rows row0 <= y < row1
+/* Ray cycling (DESIGN.md §2.10): continue the accumulated front-to-back state of rows row0 <= y < row1
  * through this brick.  state: H*W*4 doubles (full-frame indexing), read and written in place. */
 int dvr_oracle_render_brick_accum(const float* vox, const int64_t* geo, const double* wgeo, const double* cam,
                                   const float* tf, int n_tf, double vmin, double tf_scale, double dt, double ert,

@@ -225,7 +225,7 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
     ``band_clear``: only the footprint's row band is defined afterwards (band-clipped compositing).
     ``rows`` = (r0, r1): march only those pixel rows; ``partial`` (and ``samples``) hold just them.
     ``accum``: ``partial`` holds each ray's accumulated front-to-back state, which the march continues
-    (ray cycling, DESIGN.md §2.9).  A float16 ``partial`` gets fp16 fragments (DPRT_MARCH_HALF)."""
+    (ray cycling, DESIGN.md §2.10).  A float16 ``partial`` gets fp16 fragments (DPRT_MARCH_HALF)."""
     half = partial.dtype == torch.float16
     _require_cuda(partial, "partial", torch.float16 if half else torch.float32)
     npix = width * height if rows is None else (rows[1] - rows[0]) * width

@@ -56,7 +56,7 @@ class RenderOptions:
 
     dt: float = 1.0                    # lattice spacing along the ray, world units
     ert: float = 0.99                  # early ray termination threshold (per brick)
-    composite: str = "auto"            # auto | direct_send | binary_swap | p2p | cycle (ray cycling, §2.9)
+    composite: str = "auto"            # auto | direct_send | binary_swap | p2p | cycle (ray cycling, §2.10)
     skip_empty: bool = True            # exact empty-space skipping
     disable_compositing: bool = False  # debug: root shows only its own brick (negative test, engine.py:172)
     frame_index: int = 0
@@ -321,7 +321,7 @@ class VolumeRenderer:
         return res
 
     def _render_cycle(self, cam, width, height, options, dtf, stats, order, ev, t0) -> RenderResult:
-        """Ray cycling (the reference's paradigm, engine.py:282-310, for DVR; DESIGN.md §2.9).  Rank b's
+        """Ray cycling (the reference's paradigm, engine.py:282-310, for DVR; DESIGN.md §2.10).  Rank b's
         batch = its row block.  It starts at b's position p0 in the visibility order and hops along that
         order (ring_exchange, transport.py:457-462): at each hop the holder marches its brick into the
         batch's back state B (positions >= p0) or front state F (positions < p0), continuing the rays'
