@@ -393,7 +393,8 @@ def test_fused_frame_writes_every_pixel(cuda_device, oracle_lib):
     dtf = dev.DeviceTF(s.tf, cuda_device)
     n = s.W * s.H
     for cam in (s.cam, orbit_camera(s.field.bounds().center(), 300.0, 0.4, 0.2, 20.0, s.W / s.H)):
-        frame = torch.full((n * 3,), 0xAB, dtype=torch.uint8, device=cuda_device)
+        guarded = torch.full((n * 3 + 256,), 0xAB, dtype=torch.uint8, device=cuda_device)
+        frame = guarded[:n * 3]
         dev.march_rgb8(b, cam, dtf, s.dt, s.ert, s.background, frame, s.W, s.H)
         p = torch.empty(n * 4, dtype=torch.float32, device=cuda_device)
         dev.march(b, cam, dtf, s.dt, s.ert, p, s.W, s.H)
@@ -401,4 +402,34 @@ def test_fused_frame_writes_every_pixel(cuda_device, oracle_lib):
         dev.composite([p], s.background, rgb8=ref)
         torch.cuda.synchronize()
         assert torch.equal(frame, ref)
+        assert bool((guarded[n * 3:] == 0xAB).all()), "write past the frame"
+    b.close()
+
+
+def test_partial_writes_stay_in_bounds(cuda_device, oracle_lib):
+    """Band-cleared, windowed and fp16 partial marches write only their buffers (sentinel guard after the
+    end) and define every pixel they promise: the band rows (band clear) / the window rows."""
+    s = c1(P=2, W=131, H=97)
+    dtf = dev.DeviceTF(s.tf, cuda_device)
+    n = s.W * s.H
+    b = dev.DeviceBrick(s.dec.brick(1), cuda_device).generate(s.field)
+    full = torch.empty(n * 4, dtype=torch.float32, device=cuda_device)
+    dev.march(b, s.cam, dtf, s.dt, s.ert, full, s.W, s.H)
+    rect = b.footprint(s.cam, s.W, s.H)
+    cases = [("band", torch.float32, None), ("window", torch.float32, (20, 71)), ("half", torch.float16, None)]
+    for name, dt, rows in cases:
+        npx = n if rows is None else (rows[1] - rows[0]) * s.W
+        guarded = torch.full((npx * 4 + 64,), 7.0, dtype=dt, device=cuda_device)
+        buf = guarded[:npx * 4]
+        dev.march(b, s.cam, dtf, s.dt, s.ert, buf, s.W, s.H, band_clear=name == "band", rows=rows)
+        torch.cuda.synchronize()
+        assert bool((guarded[npx * 4:] == 7.0).all()), f"{name}: write past the buffer"
+        ref = full.view(s.H, s.W, 4)
+        got = buf.view(-1, s.W, 4).float()
+        if name == "band":
+            assert torch.equal(got[rect[1]:rect[3]], ref[rect[1]:rect[3]])
+        elif name == "window":
+            assert torch.equal(got, ref[rows[0]:rows[1]])
+        else:
+            assert torch.equal(got, ref.half().float())
     b.close()
