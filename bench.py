@@ -354,21 +354,23 @@ def run_ours(args):
                   "unclipped_fragment_bytes_per_rank": full_bytes, "rgb8_into_root": gather_bytes,
                   "mode": comp.mode, "clipped_to_footprint_rows": bands is not None}
 
-    # ---- marcher alone, CUDA events on its launch stream (roofline)
-    # (the same call the step makes: the fused RGB8 march at one rank, the RGBA-partial march otherwise)
+    # ---- marcher alone, CUDA events on its launch stream (roofline): K back-to-back launches of the same
+    # call the step makes (the fused RGB8 march at one rank; the band-cleared RGBA-partial march otherwise)
+    # between one event pair, so the average is the kernel's launch duration without per-event gaps
     partial = renderer.partial
     frame8 = torch.empty(W * H * 3, dtype=torch.uint8, device=device)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clip = R > 1 and renderer.compositor.clips_bands()
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    for a, b in ev:
-        a.record(stream)
+    m0.record(stream)
+    for _ in range(args.steps):
         if R == 1:
             dev.march_rgb8(brick, cam, renderer.dtf, DT, ERT, BACKGROUND, frame8, W, H, skip=skip)
         else:
-            dev.march(brick, cam, renderer.dtf, DT, ERT, partial, W, H, skip=skip)
-        b.record(stream)
+            dev.march(brick, cam, renderer.dtf, DT, ERT, partial, W, H, skip=skip, band_clear=clip)
+    m1.record(stream)
     barrier()
-    march_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+    march_ms = m0.elapsed_time(m1) / args.steps
     rect = brick.footprint(cam, W, H)
     fp_px = max(0, rect[2] - rect[0]) * max(0, rect[3] - rect[1])
     alg_bytes = desc.stored_bytes + 16 * fp_px + 16 * tf.n
