@@ -86,7 +86,13 @@ typedef struct DprtMarchParams {
     uint64_t tf_version;
     int32_t row0, row1; /* row1 > row0: march only pixel rows [row0, row1); partial_rgba and samples then
                            hold just those rows (pixel (x, y) at index (y - row0) * W + x).  0, 0: all rows */
+    int32_t counter_slot; /* 0..DPRT_MARCH_COUNTER_SLOTS-1: the brick's tile-queue counter this launch uses.
+                             Marches of one brick that may run concurrently (frames in flight on different
+                             streams) must use different slots; 0 for stream-ordered use */
+    int32_t reserved;
 } DprtMarchParams;
+
+#define DPRT_MARCH_COUNTER_SLOTS 4
 
 #define DPRT_MARCH_NO_SKIP 1      /* disable exact empty-space skipping (macrocell skip distances) */
 #define DPRT_MARCH_FULL_FRAME 2   /* march every pixel instead of the brick's screen footprint */

@@ -68,7 +68,10 @@ class MarchParams(ctypes.Structure):
     _fields_ = [("tf_rgba", ctypes.c_void_p), ("n_tf", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("vmin", ctypes.c_double), ("vmax", ctypes.c_double), ("dt", ctypes.c_double),
                 ("ert", ctypes.c_double), ("tf_version", ctypes.c_uint64), ("row0", ctypes.c_int32),
-                ("row1", ctypes.c_int32)]
+                ("row1", ctypes.c_int32), ("counter_slot", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+MARCH_COUNTER_SLOTS = 4  # DPRT_MARCH_COUNTER_SLOTS
 
 
 _lib: Optional[ctypes.CDLL] = None

@@ -145,7 +145,7 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     b->quad = nullptr;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&b->quad, (size_t)nq * sizeof(float4));  // 16 B per apron-grid voxel
-    if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * DPRT_MARCH_COUNTER_SLOTS * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc);
     if (e == cudaSuccess) e = cudaMalloc(&b->skip_tmp, (size_t)nmc);
@@ -321,6 +321,8 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     if (!(p->vmax > p->vmin)) return fail(DPRT_E_USAGE, "transfer function range needs vmax > vmin");
     if (!(p->dt > 0.0) || !isfinite(p->dt)) return fail(DPRT_E_USAGE, "dt must be finite and > 0");
     if (!(cam->half_w > 0.0) || !(cam->half_h > 0.0)) return fail(DPRT_E_USAGE, "camera half extents must be > 0");
+    if (p->counter_slot < 0 || p->counter_slot >= DPRT_MARCH_COUNTER_SLOTS)
+        return fail(DPRT_E_USAGE, "counter slot %d outside [0, %d)", p->counter_slot, DPRT_MARCH_COUNTER_SLOTS);
     int rc = bind(b->device);
     if (rc) return rc;
     dprt::MarchArgs a;
@@ -409,7 +411,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
         mb->ray_cap = (long long)W * H;
     }
     a.rays = mb->rays;
-    a.counters = mb->counters;
+    a.counters = mb->counters + 2 * p->counter_slot;  // one tile queue per concurrently running frame
     if (a.skip && (p->tf_version == 0 || b->skip_version != p->tf_version)) {
         CK(dprt::launch_skip_build(*mb, a, mb->skip_tmp, (cudaStream_t)stream), "skip-distance build");
         mb->skip_version = p->tf_version;

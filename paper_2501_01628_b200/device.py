@@ -21,6 +21,9 @@ from .geom import CameraSpec
 from .volume import BrickDesc, FieldSpec, TransferFunction1D
 
 
+MARCH_COUNTER_SLOTS = _lib.MARCH_COUNTER_SLOTS  # tile queues per brick: slot 0 stream-ordered, 1.. frame lanes
+
+
 def _stream(device: torch.device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -85,6 +88,22 @@ class DeviceBrick:
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().dprt_brick_create(self.index, ctypes.byref(d), ctypes.byref(h)), "dprt_brick_create")
         self._h = h
+        # frames in flight (march_rgb8 with a lane stream): the last march event per lane stream, the TF
+        # version of the last lane march and whether that march rebuilt the TF-dependent skip distances
+        self._lane_reads = {}
+        self._lane_version = None
+        self._lane_rebuilt = False
+
+    def join_lanes(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Make ``stream`` (default: the current stream) wait for every march still in flight on a lane
+        stream.  Called before anything stream-ordered touches what those marches read: the voxels, the
+        skip distances, the tile counters."""
+        if not self._lane_reads:
+            return
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        for ev in self._lane_reads.values():
+            st.wait_event(ev)
+        self._lane_reads.clear()
 
     @property
     def handle(self) -> ctypes.c_void_p:
@@ -101,6 +120,7 @@ class DeviceBrick:
         else:
             blobs = np.ascontiguousarray(f.blobs, np.float64)
             spec = _lib.FieldSpec(0, blobs.shape[0], ctypes.c_void_p(blobs.ctypes.data))
+        self.join_lanes()
         _lib.check(_lib.lib().dprt_brick_generate(self.handle, ctypes.byref(spec), _stream(self.device)),
                    "dprt_brick_generate")
         return self
@@ -108,6 +128,7 @@ class DeviceBrick:
     def upload(self, voxels) -> "DeviceBrick":
         """Stored voxels (z, y, x) from a host numpy array or a device tensor."""
         shape = tuple(reversed(self.desc.stored_dims))
+        self.join_lanes()
         if isinstance(voxels, torch.Tensor):
             if tuple(voxels.shape) != shape:
                 raise UsageError(f"voxel tensor {tuple(voxels.shape)} != stored {shape}")
@@ -170,6 +191,16 @@ class DeviceTF:
         self._slot = 0
         self._side = None          # side stream for the staging copies
         self._marker = None        # main-stream event recorded at the previous staged update
+        self._lane_reads = {}      # id(table) -> events of lane-stream marches that read it (frames in flight)
+
+    def note_lane_read(self, lane: torch.cuda.Stream, event: torch.cuda.Event) -> None:
+        """A march on ``lane`` (not the current stream) reads the current table until ``event`` (lanes run
+        their marches in order, so the latest event per lane covers the earlier ones)."""
+        self._lane_reads.setdefault(id(self.table), {})[lane.cuda_stream] = event
+
+    def _wait_lane_reads(self, stream: torch.cuda.Stream, table: torch.Tensor) -> None:
+        for ev in self._lane_reads.pop(id(table), {}).values():
+            stream.wait_event(ev)
 
     def update(self, tf: TransferFunction1D, staging: Optional[torch.Tensor] = None) -> None:
         """New table contents (optionally copied from a pinned host staging tensor)."""
@@ -179,6 +210,10 @@ class DeviceTF:
             self.version = next(_TF_VERSIONS)
             self._host = host.copy()
             if host.shape[0] != self.table.numel():
+                # lane marches may still read the old table: the current stream (its allocator's reuse
+                # order) waits for them before the tensor is released
+                for t in self._tables or [self.table]:
+                    self._wait_lane_reads(torch.cuda.current_stream(t.device), t)
                 self.table = torch.empty(host.shape[0], dtype=torch.float32, device=self.table.device)
                 self._tables = None
         self.tf = tf
@@ -187,6 +222,7 @@ class DeviceTF:
             self._stage(staging)
             return
         src = staging if staging is not None else torch.from_numpy(self._host)
+        self._wait_lane_reads(torch.cuda.current_stream(self.table.device), self.table)
         self.table.copy_(src, non_blocking=staging is not None)
 
     def _stage(self, staging: torch.Tensor) -> None:
@@ -202,6 +238,7 @@ class DeviceTF:
         # exactly that work (the marker), not for the march still running out of the other slot
         if self._marker is not None:
             self._side.wait_event(self._marker)
+        self._wait_lane_reads(self._side, dst)  # ... and for lane-stream marches out of that slot
         self._marker = torch.cuda.Event()
         self._marker.record(main)
         _lib.check(_lib.lib().dprt_stage_input(d.index, ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(staging.data_ptr()),
@@ -254,6 +291,7 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
     p = tf.params(dt, ert, flags)
     if rows is not None:
         p.row0, p.row1 = int(rows[0]), int(rows[1])
+    brick.join_lanes()  # counter slot 0, skip distances: ordered after frames still in flight
     c = camera_struct(cam)
     rc = _lib.lib().dprt_march(brick.handle, ctypes.byref(c), ctypes.byref(p), ctypes.c_void_p(partial.data_ptr()),
                                sp, width, height, _stream(brick.device))
@@ -262,8 +300,17 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
 
 def march_rgb8(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, background,
                rgb8: torch.Tensor, width: int, height: int, samples: Optional[torch.Tensor] = None,
-               skip: bool = True) -> None:
-    """dprt_march_rgb8: single-rank frame, over-background and tone map fused into the march."""
+               skip: bool = True, lane: Optional[torch.cuda.Stream] = None,
+               slot: int = 0) -> Optional[torch.cuda.Event]:
+    """dprt_march_rgb8: single-rank frame, over-background and tone map fused into the march.
+
+    ``lane`` (frames in flight): run the march on that stream with tile-counter ``slot`` (1..3, one per
+    lane) instead of the current stream.  The lane first waits for the current stream's work so far (the
+    frame's inputs are ordered as usual); the current stream does NOT wait for the march -- the returned
+    event marks the frame complete.  Frames on different lanes overlap: the next frame's CTAs take the
+    SMs the previous frame's last beams leave idle.  Hazards between lanes are resolved here: a march that
+    (re)builds the TF-dependent skip distances, or follows one that did, first waits for the other lanes,
+    and every stream-ordered march / brick write joins the lanes (``DeviceBrick.join_lanes``)."""
     _require_cuda(rgb8, "rgb8", torch.uint8)
     if rgb8.numel() != width * height * 3:
         raise UsageError("rgb8 frame must hold 3 bytes per pixel")
@@ -274,9 +321,37 @@ def march_rgb8(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert
     p = tf.params(dt, ert, 0 if skip else _lib.MARCH_NO_SKIP)
     c = camera_struct(cam)
     bg = (ctypes.c_float * 3)(*[float(v) for v in background])
+    if lane is None:
+        if slot != 0:
+            raise UsageError("counter slots other than 0 need a lane stream")
+        brick.join_lanes()
+        rc = _lib.lib().dprt_march_rgb8(brick.handle, ctypes.byref(c), ctypes.byref(p), bg,
+                                        ctypes.c_void_p(rgb8.data_ptr()), sp, width, height, _stream(brick.device))
+        _lib.check(rc, "dprt_march_rgb8")
+        return None
+    if not 1 <= slot < _lib.MARCH_COUNTER_SLOTS:
+        raise UsageError(f"lane counter slot must be in [1, {_lib.MARCH_COUNTER_SLOTS}), got {slot}")
+    main = torch.cuda.current_stream(brick.device)
+    ready = torch.cuda.Event()
+    ready.record(main)
+    lane.wait_event(ready)
+    rebuild = brick._lane_version != tf.version
+    if rebuild or brick._lane_rebuilt:
+        for key, ev in list(brick._lane_reads.items()):
+            if key != lane.cuda_stream:
+                lane.wait_event(ev)
+    p.counter_slot = slot
     rc = _lib.lib().dprt_march_rgb8(brick.handle, ctypes.byref(c), ctypes.byref(p), bg,
-                                    ctypes.c_void_p(rgb8.data_ptr()), sp, width, height, _stream(brick.device))
+                                    ctypes.c_void_p(rgb8.data_ptr()), sp, width, height,
+                                    ctypes.c_void_p(lane.cuda_stream))
     _lib.check(rc, "dprt_march_rgb8")
+    done = torch.cuda.Event()
+    done.record(lane)
+    brick._lane_reads[lane.cuda_stream] = done
+    brick._lane_rebuilt = rebuild
+    brick._lane_version = tf.version
+    tf.note_lane_read(lane, done)
+    return done
 
 
 def composite(frags: Sequence[torch.Tensor], background=None, rgb8: Optional[torch.Tensor] = None,

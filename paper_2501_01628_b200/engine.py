@@ -68,6 +68,10 @@ class RenderOptions:
     timing: bool = False               # CUDA events around march and composite (RankStats.device_times())
     fragment_dtype: str = "f32"        # "f16": half-size RGBA fragments (march output, exchange, blend input;
                                        # direct_send / p2p / auto), DESIGN.md §6
+    frames_in_flight: int = 1          # single rank: > 1 marches frames on that many lane streams, so frame
+                                       # k+1 starts while frame k's last beams finish; the
+                                       # current stream then does not wait for the frame: use
+                                       # RenderResult.ready / VolumeRenderer.join() before reading rgb8
 
 
 @dataclass
@@ -115,6 +119,13 @@ class RenderResult:
     samples: Optional[torch.Tensor] = None  # with collect_samples: (H, W) int32, this rank's brick
     partial: Optional[torch.Tensor] = None  # this rank's RGBA partial (H, W, 4) f32 (device)
     order: Optional[List[int]] = None
+    ready: Optional[torch.cuda.Event] = None  # frames_in_flight > 1: rgb8 is complete once this fires
+
+    def wait_ready(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Order ``stream`` (default: current) after this frame's device work (a no-op unless the frame
+        was rendered with frames_in_flight > 1, where the current stream does not wait by itself)."""
+        if self.ready is not None:
+            (stream if stream is not None else torch.cuda.current_stream()).wait_event(self.ready)
 
 
 _TF_HASHES: "dict[int, tuple]" = {}
@@ -198,8 +209,11 @@ class VolumeRenderer:
         self._rank_dtf = None
         self._rank_tf_src = None
         self._fused_events = [None] * FUSED_SLOTS
+        self._fused_writers = [None] * FUSED_SLOTS  # lane march that last wrote each device frame
         self._fused_next = 0
         self._fused_slot = 0
+        self._lanes = []  # frames in flight: lane streams (counter slots 1..), next lane
+        self._lane_next = 0
         self._band_key = None
         self._band_cache = None
 
@@ -260,26 +274,51 @@ class VolumeRenderer:
         if self.ep.R == 1 and not options.keep_float and os.environ.get("DPRT_FUSED_SINGLE", "1") != "0":
             # one rank: the composite is just over-background + tone map -> fused into the march
             # a ring of device frames so the read-backs of frames k-1, k-2 overlap the march of frame k
-            if self._fused_frames is None or tuple(self._fused_frames[0].shape) != (height, width, 3):
+            lanes = self._frame_lanes(options)
+            nslots = max(FUSED_SLOTS, len(lanes) + 2)
+            if self._fused_frames is None or tuple(self._fused_frames[0].shape) != (height, width, 3) or \
+                    len(self._fused_frames) != nslots:
+                self.join()  # old frames may still be written / read back: their memory is reused
                 self._fused_frames = [torch.empty((height, width, 3), dtype=torch.uint8, device=self.device)
-                                      for _ in range(FUSED_SLOTS)]
-                self._fused_events = [None] * FUSED_SLOTS
+                                      for _ in range(nslots)]
+                self._fused_events = [None] * nslots
+                self._fused_writers = [None] * nslots
+                self._fused_next = 0
             slot = self._fused_next
-            self._fused_next = (slot + 1) % FUSED_SLOTS
-            if self._fused_events[slot] is not None:
-                torch.cuda.current_stream(self.device).wait_event(self._fused_events[slot])
-                self._fused_events[slot] = None
-            self._fused_slot = slot
+            self._fused_next = (slot + 1) % nslots
             frame = self._fused_frames[slot]
-            dev.march_rgb8(self.brick, cam, dtf, options.dt, options.ert, self.background, frame.view(-1),
-                           width, height, samples=self.samples if options.collect_samples else None,
-                           skip=options.skip_empty)
+            self._fused_slot = slot
+            samples = self.samples if options.collect_samples else None
+            if not lanes:
+                if self._fused_events[slot] is not None:
+                    torch.cuda.current_stream(self.device).wait_event(self._fused_events[slot])
+                    self._fused_events[slot] = None
+                dev.march_rgb8(self.brick, cam, dtf, options.dt, options.ert, self.background, frame.view(-1),
+                               width, height, samples=samples, skip=options.skip_empty)
+                ready = None
+            else:
+                li = self._lane_next
+                self._lane_next = (li + 1) % len(lanes)
+                lane = lanes[li]
+                # this device frame's previous read-back and previous writer (possibly another lane)
+                for key in ("_fused_events", "_fused_writers"):
+                    evs = getattr(self, key)
+                    if evs[slot] is not None:
+                        lane.wait_event(evs[slot])
+                        evs[slot] = None
+                if ev is not None:
+                    ev[0].record(lane)
+                ready = dev.march_rgb8(self.brick, cam, dtf, options.dt, options.ert, self.background,
+                                       frame.view(-1), width, height, samples=samples, skip=options.skip_empty,
+                                       lane=lane, slot=li + 1)
+                self._fused_writers[slot] = ready
             if ev is not None:
-                ev[1].record(torch.cuda.current_stream(self.device))
-                ev[2].record(torch.cuda.current_stream(self.device))
+                st = torch.cuda.current_stream(self.device) if not lanes else lane
+                ev[1].record(st)
+                ev[2].record(st)
                 stats.events = tuple(ev)
             stats.record(options.frame_index, width * height, 0, (time.perf_counter() - t0) * 1e3)
-            res = RenderResult(rgb8=frame, stats=stats, order=order)
+            res = RenderResult(rgb8=frame, stats=stats, order=order, ready=ready)
             if options.collect_samples:
                 res.samples = self.samples.view(height, width)
                 stats._samples_dev = res.samples
@@ -382,6 +421,31 @@ class VolumeRenderer:
             stats._samples_dev = res.samples
         return res
 
+    def _frame_lanes(self, options: RenderOptions) -> list:
+        """Lane streams for frames in flight (single rank, fused frame, no sample counts); [] = ordered on
+        the current stream as usual."""
+        n = int(options.frames_in_flight)
+        if n < 1 or n >= dev.MARCH_COUNTER_SLOTS:
+            raise UsageError(f"frames_in_flight must be in [1, {dev.MARCH_COUNTER_SLOTS - 1}], got {n}")
+        if n == 1 or options.collect_samples:
+            if self._lanes:
+                self.join()
+                self._lanes = []
+            return []
+        if len(self._lanes) != n:
+            self.join()
+            self._lanes = [torch.cuda.Stream(self.device) for _ in range(n)]
+            self._lane_next = 0
+        return self._lanes
+
+    def join(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Order ``stream`` (default: current) after every frame still in flight on a lane stream."""
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        for i, w in enumerate(self._fused_writers):
+            if w is not None:
+                st.wait_event(w)
+        self.brick.join_lanes(st)
+
     def render_to_host(self, cam: CameraSpec, width: int, height: int, host: Optional[torch.Tensor],
                        options: RenderOptions = RenderOptions(), verify: bool = True) -> "HostFrame":
         """Collective render whose RGB8 frame is copied into ``host`` (pinned, (H, W, 3) uint8, rank 0) on a
@@ -395,8 +459,11 @@ class VolumeRenderer:
         main = torch.cuda.current_stream(self.device)
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(self.device)
-        ready = torch.cuda.Event()
-        ready.record(main)
+        if res.ready is not None:  # frames in flight: the frame's own lane event, not the current stream
+            ready = res.ready
+        else:
+            ready = torch.cuda.Event()
+            ready.record(main)
         self._copy_stream.wait_event(ready)
         with torch.cuda.stream(self._copy_stream):
             host.copy_(res.rgb8, non_blocking=True)

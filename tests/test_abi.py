@@ -51,7 +51,7 @@ int main(void) {
   printf("DprtBrickDesc %zu\\n", sizeof(DprtBrickDesc)); F(DprtBrickDesc, ghost); F(DprtBrickDesc, origin); F(DprtBrickDesc, spacing);
   printf("DprtCamera %zu\\n", sizeof(DprtCamera)); F(DprtCamera, half_w); F(DprtCamera, half_h);
   printf("DprtFieldSpec %zu\\n", sizeof(DprtFieldSpec)); F(DprtFieldSpec, blobs);
-  printf("DprtMarchParams %zu\\n", sizeof(DprtMarchParams)); F(DprtMarchParams, vmin); F(DprtMarchParams, ert); F(DprtMarchParams, tf_version);
+  printf("DprtMarchParams %zu\\n", sizeof(DprtMarchParams)); F(DprtMarchParams, vmin); F(DprtMarchParams, ert); F(DprtMarchParams, tf_version); F(DprtMarchParams, row1); F(DprtMarchParams, counter_slot);
   return 0;
 }
 """)
