@@ -352,6 +352,18 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #endif
 constexpr int kSlabShift = DPRT_SLAB_SHIFT;
 
+// Tile-queue order: 1 = rows of tiles centre-out (default), 2 = rows and the tiles within a
+// row centre-out, 0 = row-major.  The queue then ends with the short rays at the footprint's top and bottom
+// edges instead of whatever rows come last, which shortens the launch's tail (c2 0.243 -> 0.227 ms).
+#ifndef DPRT_TILE_ORDER
+#define DPRT_TILE_ORDER 1
+#endif
+// k-th index of 0..n-1 in centre-out order: m, m-1, m+1, m-2, m+2, ... (m = n / 2)
+__device__ __forceinline__ int center_out(int k, int n) {
+    const int m = n >> 1, d = (k + 1) >> 1;
+    return (k & 1) ? m - d : m + d;
+}
+
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
 // The pixels no beam covers -- rows [y0, y1) outside the footprint rectangle -- get their "nothing here"
@@ -453,8 +465,16 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
         if (lane == 0) tile = atomicAdd(a.counters + 1, 1);
         tile = __shfl_sync(FULL, tile, 0);
         if (tile >= ntiles) break;
-        const int px = a.rect[0] + (tile % tiles_x) * kBeamW + (lane % kBeamW);
-        const int py = a.rect[1] + (tile / tiles_x) * kBeamH + (lane / kBeamW);
+#if DPRT_TILE_ORDER
+        // centre-out queue order: rows of tiles from the footprint's middle row outwards (and, with 2, the
+        // tiles of a row from its middle outwards), so the queue ends with the short rays at the edges
+        const int trow = center_out(tile / tiles_x, tiles_y);
+        const int tcol = DPRT_TILE_ORDER >= 2 ? center_out(tile % tiles_x, tiles_x) : tile % tiles_x;
+#else
+        const int trow = tile / tiles_x, tcol = tile % tiles_x;
+#endif
+        const int px = a.rect[0] + tcol * kBeamW + (lane % kBeamW);
+        const int py = a.rect[1] + trow * kBeamH + (lane / kBeamW);
         int nn = 0, pix = 0;
         float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
         const bool inside = px < a.rect[2] && py < a.rect[3];
