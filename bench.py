@@ -4,7 +4,9 @@
 
 N=1 workload = BASELINE config 2: a 512^3 f32 blob field as one brick, 1920x1080, dt = 1 voxel, ERT 0.99,
 the SURVEY §8(d) transfer function, auto-framing camera.  N>1 (torchrun, one process per GPU, NCCL):
-weak scaling, one 512^3-cell brick per rank of a kd-split field, composited at 1920x1080.  A step is
+weak scaling: the field grows with N (512^3 cells per rank), kd-split into N bricks balanced by non-empty
+voxel count (``--decomposition mass``, the default; ``even`` gives every rank 512^3 cells), composited
+at 1920x1080.  A step is
 one frame: march this rank's brick -> sort-last composite -> RGB8 frame on rank 0.  The brick (512 MiB)
 is larger than L2 (126 MB), so no flush is needed between steps.  At one rank, frames are marched two in
 flight on lane streams (``--frames-in-flight``); the timed region ends after every frame
@@ -38,6 +40,7 @@ FIELD_EDGE = 512
 W, H = 1920, 1080
 DT, ERT = 1.0, 0.99
 BACKGROUND = (0.05, 0.06, 0.08)
+MASS_THRESHOLD = 0.1  # default_tf(): alpha is 0 below this value
 
 
 def log(*a):
@@ -64,12 +67,19 @@ def field_dims(n_ranks: int):
     return tuple(c + 1 for c in cells)
 
 
-def workload(n_ranks: int):
+def workload(n_ranks: int, strategy: str = "even", device=None):
+    """The field, its kd decomposition over n_ranks, camera and TF.  ``strategy`` "mass" balances the
+    bricks by non-empty voxel count (voxels >= the TF's alpha threshold, counted on ``device``)."""
     from paper_2501_01628_b200.geom import auto_camera
     from paper_2501_01628_b200.volume import blob_field, decompose, default_tf
 
     f = blob_field(field_dims(n_ranks), seed=1, n_blobs=16)
-    dec = decompose(f, n_ranks)
+    if strategy == "mass" and n_ranks > 1:
+        from paper_2501_01628_b200 import device as dev
+
+        dec = decompose(f, n_ranks, "mass", dev.field_mass_function(f, device, MASS_THRESHOLD))
+    else:
+        dec = decompose(f, n_ranks)
     cam = auto_camera(f.bounds(), W, H)
     return f, dec, cam, default_tf()
 
@@ -289,7 +299,7 @@ def run_ours(args):
         torch.cuda.set_device(device)
         ep = SoloEndpoint(device)
     rank, R = ep.rank, ep.R
-    f, dec, cam, tf = workload(R)
+    f, dec, cam, tf = workload(R, args.decomposition, device)
     desc = dec.brick(rank)
     brick = dev.DeviceBrick(desc, device).generate(f)
     renderer = VolumeRenderer(ep, brick, dec, tf, BACKGROUND)
@@ -447,9 +457,13 @@ def run_ours(args):
             "metric": METRIC, "value": fps * 1.0, "unit": UNIT, "n_gpus": R, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "c2: 512^3 f32 blob field (seed 1, 16 blobs), 1 brick per GPU, 1920x1080, "
-                                   "dt=1 voxel, ERT 0.99, SURVEY 8(d) TF, auto camera",
-                       "field": list(f.dims), "bricks": R, "image": [W, H], "composite": renderer.compositor.mode,
+            "config": {"workload": ("c2: 512^3 f32 blob field (seed 1, 16 blobs), 1 brick per GPU, 1920x1080, "
+                                    "dt=1 voxel, ERT 0.99, SURVEY 8(d) TF, auto camera") if R == 1 else
+                                   (f"weak scaling of c2: {'x'.join(str(c - 1) for c in f.dims)}-cell f32 blob field "
+                                    f"(seed 1, 16 blobs), {R} kd bricks ({args.decomposition}), 1920x1080, dt=1 voxel, "
+                                    "ERT 0.99, SURVEY 8(d) TF, auto camera"),
+                       "field": list(f.dims), "bricks": R, "decomposition": args.decomposition if R > 1 else "whole",
+                       "image": [W, H], "composite": renderer.compositor.mode,
                        "fragments": args.fragments, "frames_in_flight": fif,
                        "empty_space_skipping": skip, "l2": "inputs larger than L2 (brick 512 MiB/GPU), no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -477,6 +491,8 @@ def main():
     ap.add_argument("--composite", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-skip", action="store_true", help="disable exact empty-space skipping")
+    ap.add_argument("--decomposition", default="mass", choices=["even", "mass"],
+                    help="N > 1: kd split of the field, even cells or balanced by non-empty voxel count")
     ap.add_argument("--frames-in-flight", type=int, default=2,
                     help="single rank: frames marched concurrently on lane streams (1 = stream-ordered)")
     ap.add_argument("--fragments", default="f32", choices=["f32", "f16"],

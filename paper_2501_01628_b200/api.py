@@ -233,14 +233,9 @@ class World(ApiObject):
 
 def _mass_function(spec: FieldSpec, data: Optional[np.ndarray], tau: float, cuda: torch.device):
     """Integer slab masses (voxels >= tau) for the mass-weighted kd split, computed locally."""
-    if data is None:
-        from .volume import BrickDesc
-
-        whole = dev.DeviceBrick(BrickDesc.whole(spec, 0), cuda).generate(spec)
-        vox = torch.from_numpy(whole.download())
-        whole.close()
-    else:
-        vox = torch.from_numpy(np.asarray(data, np.float32))
+    if data is None:  # generated field: masked on the GPU in z-chunks, never moved to the host
+        return dev.field_mass_function(spec, cuda, tau)
+    vox = torch.from_numpy(np.asarray(data, np.float32))
     mask = (vox >= tau).to(torch.int64)
 
     def mass(axis, lo, hi):

@@ -146,6 +146,13 @@ class DeviceBrick:
         torch.cuda.current_stream(self.device).synchronize()  # host array must outlive the copy
         return self
 
+    def download_device(self) -> torch.Tensor:
+        """Stored voxels (z, y, x) as a new f32 tensor on the brick's device (stream-ordered copy)."""
+        out = torch.empty(tuple(reversed(self.desc.stored_dims)), dtype=torch.float32, device=self.device)
+        rc = _lib.lib().dprt_brick_download(self.handle, ctypes.c_void_p(out.data_ptr()), 1, _stream(self.device))
+        _lib.check(rc, "dprt_brick_download")
+        return out
+
     def download(self) -> np.ndarray:
         out = np.empty(tuple(reversed(self.desc.stored_dims)), np.float32)
         rc = _lib.lib().dprt_brick_download(self.handle, ctypes.c_void_p(out.ctypes.data), 0, _stream(self.device))
@@ -169,6 +176,38 @@ class DeviceBrick:
             self.close()
         except Exception:  # noqa: BLE001 - interpreter shutdown
             pass
+
+
+def field_mass_function(f: FieldSpec, device: torch.device, tau: float, chunk: int = 64):
+    """The mass function of the mass-weighted kd split (volume.decompose) for a synthetic field, computed
+    on the GPU: the field is generated in z-chunks of ``chunk`` cell planes (bit-identical to the whole
+    field), thresholded at ``tau`` into a 1-byte mask kept on the device, and
+    ``mass(axis, lo, hi)`` sums the voxel box [lo, hi) of the mask over the two other axes -- the same
+    counts as api._mass_function's host path, without moving the field to the host."""
+    from .volume import BrickDesc
+
+    nx, ny, nz = f.dims
+    mask = torch.empty((nz, ny, nx), dtype=torch.uint8, device=device)
+    z = 0
+    while z < nz - 1:
+        z1 = min(z + chunk, nz - 1)
+        b = DeviceBrick(BrickDesc(f.dims, (0, 0, z), (nx - 1, ny - 1, z1), 0, f.origin, f.spacing), device)
+        try:
+            vox = b.generate(f).download_device()  # voxel planes z .. z1
+        finally:
+            torch.cuda.current_stream(device).synchronize()
+            b.close()
+        last = z1 == nz - 1
+        mask[z: z1 + 1 if last else z1] = (vox if last else vox[:-1]) >= tau
+        del vox
+        z = z1
+
+    def mass(axis, lo, hi):
+        sub = mask[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        dims = tuple(a for a in range(3) if a != 2 - axis)
+        return sub.sum(dim=dims, dtype=torch.int64).cpu().numpy()
+
+    return mass
 
 
 _TF_VERSIONS = itertools.count(1)

@@ -57,9 +57,11 @@ def graph_timed(fn, reps=20):
     return e0.elapsed_time(e1) / reps
 
 
-out = {"W": W, "H": H, "assumptions": {"barrier_us": BARRIER_US, "peer_GBps": PEER_GBS}, "runs": []}
+STRATEGY = sys.argv[1] if len(sys.argv) > 1 else "even"  # kd split of bench.py's field: even | mass
+out = {"W": W, "H": H, "assumptions": {"barrier_us": BARRIER_US, "peer_GBps": PEER_GBS}, "strategy": STRATEGY,
+       "runs": []}
 for N in (1, 2, 4, 8):
-    f, dec, cam, tf = bench.workload(N)
+    f, dec, cam, tf = bench.workload(N, STRATEGY, d)
     dtf = dev.DeviceTF(tf, d)
     bands = [tuple(dev.desc_footprint(dec.brick(s), cam, W, H)[1::2]) for s in range(N)]
     parts, march_ms = [], []
@@ -109,4 +111,4 @@ for N in (1, 2, 4, 8):
     del parts
     torch.cuda.empty_cache()
 Path("gpurun_out").mkdir(exist_ok=True)
-Path("gpurun_out/scaling_projection.json").write_text(json.dumps(out, indent=1))
+Path(f"gpurun_out/scaling_projection{'' if STRATEGY == 'even' else '_' + STRATEGY}.json").write_text(json.dumps(out, indent=1))
