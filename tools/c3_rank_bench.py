@@ -14,18 +14,23 @@ from paper_2501_01628_b200 import device as dev
 from paper_2501_01628_b200.geom import auto_camera
 from paper_2501_01628_b200.volume import blob_field, decompose, default_tf
 
-ranks = [int(r) for r in sys.argv[1].split(",")] if len(sys.argv) > 1 else list(range(8))
+ranks = [int(r) for r in sys.argv[1].split(",")] if len(sys.argv) > 1 and sys.argv[1] != "all" else list(range(8))
+STRATEGY = sys.argv[2] if len(sys.argv) > 2 else "even"  # even: 2x2x2 bricks of 1024^3 cells; mass: balanced
 W, H = 3840, 2160
 d = torch.device("cuda", 0)
 f = blob_field((2049, 2049, 2049), seed=1)
-dec = decompose(f, 8)
+if STRATEGY == "mass":  # kd split balanced by voxels >= the TF's alpha threshold (counted on the GPU)
+    dec = decompose(f, 8, "mass", dev.field_mass_function(f, d, 0.1))
+    torch.cuda.empty_cache()
+else:
+    dec = decompose(f, 8)
 cam = auto_camera(f.bounds(), W, H)
 tf = default_tf()
 dtf = dev.DeviceTF(tf, d)
 part = torch.empty(W * H * 4, dtype=torch.float32, device=d)
 peak = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
 order = dec.visibility_order(cam.position)
-out = {"W": W, "H": H, "field": list(f.dims), "order": order, "ranks": []}
+out = {"W": W, "H": H, "field": list(f.dims), "order": order, "strategy": STRATEGY, "ranks": []}
 for r in ranks:
     desc = dec.brick(r)
     t0 = time.time()
@@ -80,4 +85,4 @@ mx = max(x["march_ms"] for x in out["ranks"])
 out["max_rank_march_ms"] = mx
 print(json.dumps({k: v for k, v in out.items() if k != "ranks"}))
 Path("gpurun_out").mkdir(exist_ok=True)
-Path("gpurun_out/c3_ranks.json").write_text(json.dumps(out, indent=1))
+Path(f"gpurun_out/c3_ranks{'' if STRATEGY == 'even' else '_' + STRATEGY}.json").write_text(json.dumps(out, indent=1))
