@@ -108,3 +108,48 @@ def test_random_scene_matches_oracle(cuda_device, oracle_lib, seed):
         torch.cuda.synchronize()
         b.close()
         assert torch.equal(fused, rgb8), f"case {seed}: fused single-rank frame differs from march + composite"
+
+
+MODES = ["direct_send", "binary_swap", "p2p", "cycle"]
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_multirank_frame_matches_oracle(cuda_device, oracle_lib, seed):
+    """R rank threads on one GPU through the real exchange schedules (transport.run_collective): the RGB8
+    frame at rank 0 within 1 LSB of the oracle's sort-last composite (ray cycling: of its own oracle
+    restatement, oracle.cycle_frame), and every rank's sample ownership exact."""
+    from paper_2501_01628_b200.compositor import assign_rows
+    from paper_2501_01628_b200.engine import RenderOptions, VolumeRenderer
+    from paper_2501_01628_b200.transport import run_collective
+    from scenes import cam_array, oracle_brick
+
+    rng = np.random.default_rng(5000 + seed)
+    mode = MODES[seed % len(MODES)]
+    R = int(rng.choice([2, 4, 8])) if mode == "binary_swap" else int(rng.integers(2, 9))
+    f, _, cam, tf, dt, ert, W, H, bg = _random_case(seed + 100)
+    dec = decompose(f, R)
+    vox = oracle.generate_field(f.dims, f.blobs)
+    ref, ref_s = oracle_partials(vox, dec, cam, tf, dt, ert, W, H)
+    order = dec.visibility_order(cam.position)
+    if mode == "cycle":
+        obs = [oracle_brick(dec, r) for r in range(R)]
+        img = oracle.cycle_frame([ob.extract(vox) for ob in obs], obs, order, assign_rows(H, R), cam_array(cam),
+                                 tf.as_f32(), tf.vmin, tf.vmax, dt, ert, W, H, bg)
+    else:
+        img = oracle.composite(ref, order, bg)
+    want = oracle.tone_map_rgb8(img).astype(np.int16)
+
+    def body(ep):
+        b = dev.DeviceBrick(dec.brick(ep.rank), cuda_device).generate(f)
+        vr = VolumeRenderer(ep, b, dec, tf, bg)
+        res = vr.render(cam, W, H, RenderOptions(composite=mode, dt=dt, ert=ert, collect_samples=True))
+        torch.cuda.synchronize()
+        out = (res.samples.cpu().numpy().astype(np.uint32), None if res.rgb8 is None else res.rgb8.cpu().numpy())
+        b.close()
+        return out
+
+    results = run_collective(R, body, device=cuda_device)
+    for r in range(R):
+        assert np.array_equal(results[r][0], ref_s[r]), f"case {seed} ({mode}, R={R}): rank {r} ownership"
+    diff = np.abs(results[0][1].astype(np.int16) - want)
+    assert diff.max() <= RGB8_MAX_LSB, f"case {seed} ({mode}, R={R}): RGB8 differs by {diff.max()} LSB"
