@@ -105,6 +105,8 @@ typedef struct DprtMarchParams {
                                      already at ERT are skipped) and writes it back; nothing is cleared */
 #define DPRT_MARCH_HALF 64        /* beam marcher: partial_rgba is fp16 RGBA (8 B per pixel) -- half-size
                                      fragments for the exchange; not with DPRT_MARCH_ACCUM */
+#define DPRT_MARCH_WIDE 128       /* beam marcher: 64-bit quad offsets even for a brick of < 2^31 quads (bricks
+                                     of >= 2^31 quads always use them); for testing the wide path */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
 #define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */

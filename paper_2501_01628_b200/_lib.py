@@ -33,6 +33,7 @@ MARCH_QUEUE = 8
 MARCH_BAND_CLEAR = 16
 MARCH_ACCUM = 32
 MARCH_HALF = 64
+MARCH_WIDE = 128
 COMPOSITE_TONEMAP = 1
 COMPOSITE_RGBA = 2
 COMPOSITE_HALF_IN = 4

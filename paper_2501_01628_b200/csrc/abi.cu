@@ -109,11 +109,12 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
             nv *= hi - lo + 1;
             nq *= hi - lo + 3;
         }
-        // the marcher addresses voxels and (apron) quads with signed 32-bit offsets: split larger fields
-        // into more bricks
-        if (nq >= (1LL << 31))
-            return fail(DPRT_E_USAGE, "brick stores %lld voxels (%lld with the quad apron); the limit is 2^31 - 1",
-                        nv, nq);
+        // the beam marcher addresses quads with a 64-bit z-plane term once a brick holds >= 2^31 of them
+        // (march_beam_kernel<true>); in-plane offsets and the queue marcher stay 32-bit
+        const long long plane = (desc->hi[0] - desc->lo[0] + 2 * desc->ghost + 3) * (desc->hi[1] - desc->lo[1] + 2 * desc->ghost + 3);
+        if (nq >= (1LL << 40) || plane >= (1LL << 31))
+            return fail(DPRT_E_USAGE, "brick stores %lld voxels (%lld with the quad apron); the limit is 2^40 quads "
+                        "and 2^31 per z-plane", nv, nq);
     }
     int rc = bind(device);
     if (rc) return rc;
@@ -356,6 +357,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.qsy = (int)b->qd[0];
     a.qsz = (int)(b->qd[0] * b->qd[1]);
     a.qorg = b->quad + a.qsz + a.qsy + 1;
+    a.wide = ((long long)b->qd[0] * b->qd[1] * b->qd[2] >= (1LL << 31) || (p->flags & DPRT_MARCH_WIDE)) ? 1 : 0;
     a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.band_clear = (p->flags & DPRT_MARCH_BAND_CLEAR) ? 1 : 0;
@@ -369,6 +371,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.npix_buf = window ? (long long)(p->row1 - p->row0) * W : (long long)W * H;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
     if (rgb8 || a.accum || window || a.half_out) a.beam = 1;  // these outputs exist in the beam marcher only
+    if (!a.beam && a.wide) return fail(DPRT_E_USAGE, "the queue marcher takes bricks of < 2^31 quads; use the beam marcher");
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
     a.n_tf = p->n_tf;
     a.vmin = (float)p->vmin;

@@ -20,6 +20,8 @@
 
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 #ifndef DPRT_BOUNDS_CHECK
@@ -189,7 +191,7 @@ __device__ __forceinline__ float trilerp(const float4 q0, const float4 q1, float
 }
 
 // DPRT_BOUNDS_CHECK builds trap on a quad index (relative to qorg, both loads) outside the apron grid.
-__device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, int qi) {
+__device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, long long qi) {
 #if DPRT_BOUNDS_CHECK
     const long long org = (long long)a.qsz + a.qsy + 1, total = (long long)a.qsz * (a.sd[2] + 2);
     if (qi + org < 0 || qi + org + a.qsz >= total) __trap();
@@ -434,6 +436,9 @@ __device__ __forceinline__ void write_clear(const MarchArgs& a, int pix) {
 #define DPRT_BEAM_BLOCK 256
 #endif
 constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are independent beams)
+// kWide: the brick holds >= 2^31 apron quads (a mass-balanced brick of a 2048^3 field can), so the z-plane
+// term of the quad offset is 64-bit; other bricks keep 32-bit offsets (the wide form costs ~6-12 %).
+template <bool kWide>
 __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
@@ -650,7 +655,8 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                     const float uy = fmaf(fs, st[1], p0[1]);
                     const float uz = fmaf(fs, st[2], p0[2]);
                     const int ix = __float2int_rd(ux), iy = __float2int_rd(uy), iz = __float2int_rd(uz);
-                    const int qi = iz * qsz + iy * qsy + ix;
+                    using Off = typename std::conditional<kWide, long long, int>::type;
+                    const Off qi = (Off)iz * qsz + (iy * qsy + ix);
                     quad_bounds_check(a, qi);
                     qa[u] = __ldg(qorg + qi);
                     qb[u] = __ldg(qorg1 + qi);
@@ -821,9 +827,10 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
         // (fill_outside_rect, write_clear); accumulation leaves the rays' state alone
         if (a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_beam_kernel, kBeamBlock, smem);
+        auto* kern = a.wide ? march_beam_kernel<true> : march_beam_kernel<false>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBeamBlock, smem);
         if (per_sm < 1) per_sm = 1;
-        march_beam_kernel<<<sms * per_sm, kBeamBlock, smem, stream>>>(a);
+        kern<<<sms * per_sm, kBeamBlock, smem, stream>>>(a);
         return cudaGetLastError();
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, kTileX * kTileY, smem);

@@ -69,3 +69,24 @@ def test_config3_brick_full_frame(cuda_device, oracle_lib, rank):
     b.close()
     del b
     torch.cuda.empty_cache()
+
+
+def test_config3_mass_balanced_wide_brick(cuda_device, oracle_lib):
+    """Config 3's field split by non-empty voxel count (the GPU mass function): its largest brick holds
+    more than 2^31 apron quads, so it marches with 64-bit quad offsets.  Full-frame ownership exact,
+    strided rows within tolerance."""
+    W, H = 3840, 2160
+    f = blob_field((2049, 2049, 2049), seed=1)
+    dec = decompose(f, 8, "mass", dev.field_mass_function(f, cuda_device, 0.1))
+    torch.cuda.empty_cache()
+    sizes = [np.prod([d + 2 for d in dec.brick(r).stored_dims]) for r in range(8)]
+    r = int(np.argmax(sizes))
+    assert sizes[r] >= 2 ** 31, "expected one brick beyond the 32-bit quad range"
+    cam = auto_camera(f.bounds(), W, H)
+    tf = default_tf()
+    b, rgba, samples = _march(dec, r, cam, tf, W, H, cuda_device)
+    assert np.array_equal(samples, oracle.sample_counts(oracle_brick(dec, r), cam_array(cam), 1.0, W, H))
+    _strided_rows_check(b, dec, r, cam, tf, W, H, rgba, 96)
+    b.close()
+    del b
+    torch.cuda.empty_cache()

@@ -433,3 +433,24 @@ def test_partial_writes_stay_in_bounds(cuda_device, oracle_lib):
         else:
             assert torch.equal(got, ref.half().float())
     b.close()
+
+
+def test_wide_quad_offsets_are_bit_identical(cuda_device, oracle_lib):
+    """Bricks of >= 2^31 apron quads march with 64-bit z-plane offsets (march_beam_kernel<true>); forced
+    onto a small brick, that kernel writes exactly the bytes of the 32-bit one."""
+    f = blob_field((70, 61, 53), seed=12)
+    dec = decompose(f, 2)
+    W, H = 150, 110
+    cam = auto_camera(f.bounds(), W, H)
+    dtf = dev.DeviceTF(dense_tf(), cuda_device)
+    for r in range(2):
+        b = dev.DeviceBrick(dec.brick(r), cuda_device).generate(f)
+        out = []
+        for wide in (False, True):
+            p = torch.empty(H * W * 4, dtype=torch.float32, device=cuda_device)
+            s = torch.empty(H * W, dtype=torch.int32, device=cuda_device)
+            dev.march(b, cam, dtf, 0.8, 0.97, p, W, H, samples=s, force_wide=wide)
+            out.append((p, s))
+        torch.cuda.synchronize()
+        assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+        b.close()
