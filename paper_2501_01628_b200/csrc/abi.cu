@@ -109,12 +109,12 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
             nv *= hi - lo + 1;
             nq *= hi - lo + 3;
         }
-        // the beam marcher addresses quads with a 64-bit z-plane term once a brick holds >= 2^31 of them
-        // (march_beam_kernel<true>); in-plane offsets and the queue marcher stay 32-bit
-        const long long plane = (desc->hi[0] - desc->lo[0] + 2 * desc->ghost + 3) * (desc->hi[1] - desc->lo[1] + 2 * desc->ghost + 3);
-        if (nq >= (1LL << 40) || plane >= (1LL << 31))
-            return fail(DPRT_E_USAGE, "brick stores %lld voxels (%lld with the quad apron); the limit is 2^40 quads "
-                        "and 2^31 per z-plane", nv, nq);
+        // the beam marcher addresses quads with signed 32-bit offsets, or unsigned ones from the apron
+        // grid's start once a brick holds >= 2^31 of them (march_beam_kernel<true>); the queue marcher
+        // takes < 2^31 only
+        if (nq >= (1LL << 32))
+            return fail(DPRT_E_USAGE, "brick stores %lld voxels (%lld with the quad apron); the limit is 2^32 - 1",
+                        nv, nq);
     }
     int rc = bind(device);
     if (rc) return rc;

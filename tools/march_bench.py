@@ -19,6 +19,7 @@ ap.add_argument("--no-skip", action="store_true")
 ap.add_argument("--threshold", type=float, default=0.1)
 ap.add_argument("--field", choices=["blobs", "ml"], default="blobs")
 ap.add_argument("--rgb8", action="store_true", help="time dprt_march_rgb8 (the single-rank bench step)")
+ap.add_argument("--wide", action="store_true", help="RGBA march forced onto the 64-bit-offset kernel")
 args = ap.parse_args()
 d = torch.device("cuda", 0)
 if args.field == "ml":
@@ -45,7 +46,7 @@ def step():
     if args.rgb8:
         dev.march_rgb8(b, cam, dtf, 1.0, 0.99, (0.05, 0.06, 0.08), frame, args.W, args.H, skip=not args.no_skip)
     else:
-        dev.march(b, cam, dtf, 1.0, 0.99, p, args.W, args.H, skip=not args.no_skip)
+        dev.march(b, cam, dtf, 1.0, 0.99, p, args.W, args.H, skip=not args.no_skip, force_wide=args.wide)
 
 
 for _ in range(3):
