@@ -105,8 +105,9 @@ typedef struct DprtMarchParams {
                                      already at ERT are skipped) and writes it back; nothing is cleared */
 #define DPRT_MARCH_HALF 64        /* beam marcher: partial_rgba is fp16 RGBA (8 B per pixel) -- half-size
                                      fragments for the exchange; not with DPRT_MARCH_ACCUM */
-#define DPRT_MARCH_WIDE 128       /* beam marcher: 64-bit quad offsets even for a brick of < 2^31 quads (bricks
-                                     of >= 2^31 quads always use them); for testing the wide path */
+#define DPRT_MARCH_WIDE 128       /* beam marcher: the wide-brick addressing (unsigned 32-bit quad offsets from the
+                                     apron grid's start) even for a brick of < 2^31 quads -- bricks of 2^31 to
+                                     2^32 - 1 quads always use it; for testing that path */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
 #define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */
@@ -119,7 +120,9 @@ const char* dprt_last_error(void); /* thread-local message of the last failing c
 int dprt_device_count(int* n);
 
 /* Brick lifecycle.  Replaces World._on_commit's accel build (pkg/src/dprt/api.py:146-171) and
- * build_bvh (bvh.py:105-157): the brick's device storage is the per-rank acceleration state. */
+ * build_bvh (bvh.py:105-157): the brick's device storage is the per-rank acceleration state (f32 voxels,
+ * 16-byte coefficient quads over a one-voxel apron, macrocell min/max).  A brick holds < 2^32 apron quads
+ * ((stored dims + 2) per axis, multiplied); DPRT_E_USAGE beyond that. */
 int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out);
 int dprt_brick_stored(const DprtBrick* b, int64_t stored_lo[3], int64_t stored_dims[3]);
 int dprt_brick_upload(DprtBrick* b, const float* src, int src_is_device, void* stream);
