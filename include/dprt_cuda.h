@@ -108,6 +108,8 @@ typedef struct DprtMarchParams {
 #define DPRT_MARCH_WIDE 128       /* beam marcher: the wide-brick addressing (unsigned 32-bit quad offsets from the
                                      apron grid's start) even for a brick of < 2^31 quads -- bricks of 2^31 to
                                      2^32 - 1 quads always use it; for testing that path */
+#define DPRT_MARCH_DEEP 256       /* beam marcher: the large-brick configuration (6-sample batches, 2 CTAs/SM)
+                                     even for a brick of < 2^28 stored voxels; for testing / tuning */
 
 #define DPRT_COMPOSITE_TONEMAP 1  /* write rgb8 = tone_map(C + (1 - A) * bg) (engine.py:500-502) */
 #define DPRT_COMPOSITE_RGBA 2     /* write the blended premultiplied RGBA (no background) */

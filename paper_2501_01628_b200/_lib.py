@@ -34,6 +34,7 @@ MARCH_BAND_CLEAR = 16
 MARCH_ACCUM = 32
 MARCH_HALF = 64
 MARCH_WIDE = 128
+MARCH_DEEP = 256
 COMPOSITE_TONEMAP = 1
 COMPOSITE_RGBA = 2
 COMPOSITE_HALF_IN = 4

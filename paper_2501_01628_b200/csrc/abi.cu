@@ -358,6 +358,9 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.qsz = (int)(b->qd[0] * b->qd[1]);
     a.qorg = b->quad + a.qsz + a.qsy + 1;
     a.wide = ((long long)b->qd[0] * b->qd[1] * b->qd[2] >= (1LL << 31) || (p->flags & DPRT_MARCH_WIDE)) ? 1 : 0;
+    // bricks of >= 2^28 stored voxels (4.3 GB of quads; c3's 1026^3 bricks, not c2's 513^3) touch far more
+    // quads than L2 holds per frame: run the deeper-batch, fewer-warp configuration
+    a.deep = ((long long)b->sd[0] * b->sd[1] * b->sd[2] >= (1LL << 28) || (p->flags & DPRT_MARCH_DEEP)) ? 1 : 0;
     a.skipd = b->skipd;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.band_clear = (p->flags & DPRT_MARCH_BAND_CLEAR) ? 1 : 0;

@@ -67,7 +67,8 @@ struct MarchArgs {
     const float* __restrict__ vox;
     const float4* __restrict__ qorg;  // coefficient quad of stored voxel (0,0,0); apron at index -1 and sd
     int qsy, qsz;                     // quad strides (apron grid)
-    int wide;                         // >= 2^31 apron quads: 64-bit z-plane offsets (march_beam_kernel<true>)
+    int wide;                         // >= 2^31 apron quads: unsigned offsets from the apron base (kWide)
+    int deep;                         // large brick: the memory-latency-bound configuration (kDeepUnroll)
     const uint8_t* __restrict__ skipd;
     int mcd[3];
     int skip;

@@ -427,6 +427,13 @@ __device__ __forceinline__ void write_clear(const MarchArgs& a, int pix) {
     }
 }
 
+#ifndef DPRT_DEEP_UNROLL
+#define DPRT_DEEP_UNROLL 6
+#endif
+#ifndef DPRT_DEEP_MINBLOCKS
+#define DPRT_DEEP_MINBLOCKS 2
+#endif
+constexpr int kDeepUnroll = DPRT_DEEP_UNROLL, kDeepBlocks = DPRT_DEEP_MINBLOCKS;
 #ifndef DPRT_BEAM_MINBLOCKS
 #define DPRT_BEAM_MINBLOCKS 3
 #endif
@@ -437,8 +444,14 @@ constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are indep
 // kWide: the brick holds >= 2^31 apron quads (a mass-balanced brick of a 2048^3 field can): quad offsets are
 // unsigned 32-bit from the apron grid's first quad (+1 instruction per sample, ~2 %); other bricks keep the
 // signed offsets from stored voxel (0, 0, 0).  (A 64-bit z-plane term measured 6-12 % slower.)
-template <bool kWide>
-__global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_kernel(const MarchArgs a) {
+//
+// kUnroll / kMinBlocks: samples per branch-free batch and CTAs per SM.  Small bricks (c2: ~0.3 GB of touched
+// quads, L2 hit ~48 %) are issue / L1 bound and run 4 @ 3 CTAs (24 warps); large ones (c3: 2.5-4.4 GB of
+// touched quads, L2 hit ~25 %) are memory-latency bound and run 6 @ 2 CTAs -- fewer warps, more loads in
+// flight per warp (c3 slowest ranks -6 to -12 %, c2 +15 %).  Chosen per launch from the
+// brick size (launch_march).
+template <bool kWide, int kUnroll, int kMinBlocks>
+__global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
     for (int i = tid; i < a.n_tf; i += blockDim.x) {
@@ -641,17 +654,17 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                 continue;
             }
 #endif
-            // Shade this lane's samples in the slab, kBeamUnroll at a time: all their corner loads are
+            // Shade this lane's samples in the slab, kUnroll at a time: all their corner loads are
             // issued before the first is shaded, so each lane keeps several loads in flight.
             // branch-free batches: slots past the lane's last sample in the slab re-load that sample (same
             // address, an L1 hit) and contribute w = 0; ERT masks the rest of the batch the same way
             const float fend = (float)(jend - 1);
             while (j < jend) {
-                float4 qa[kBeamUnroll], qb[kBeamUnroll];
-                float wx[kBeamUnroll], wy[kBeamUnroll], wz[kBeamUnroll];
+                float4 qa[kUnroll], qb[kUnroll];
+                float wx[kUnroll], wy[kUnroll], wz[kUnroll];
                 const float fj = (float)j;  // exact: j < 2^24
 #pragma unroll
-                for (int u = 0; u < kBeamUnroll; ++u) {
+                for (int u = 0; u < kUnroll; ++u) {
                     const float fs = fminf(fj + (float)u, fend);
                     const float ux = fmaf(fs, st[0], p0[0]);
                     const float uy = fmaf(fs, st[1], p0[1]);
@@ -675,10 +688,10 @@ __global__ void __launch_bounds__(kBeamBlock, DPRT_BEAM_MINBLOCKS) march_beam_ke
                     wy[u] = __saturatef(uy - (float)iy);
                     wz[u] = __saturatef(uz - (float)iz);
                 }
-                const int cnt = min(kBeamUnroll, jend - j);
+                const int cnt = min(kUnroll, jend - j);
                 float m = 1.f;  // 1 while the slot is a real sample of a live ray, then 0
 #pragma unroll
-                for (int u = 0; u < kBeamUnroll; ++u) {
+                for (int u = 0; u < kUnroll; ++u) {
                     if (u >= cnt) m = 0.f;
                     const float v = trilerp(qa[u], qb[u], wx[u], wy[u], wx[u] * wy[u], wz[u]);
                     const float x = __saturatef(fmaf(v, tns, tno)) * top;
@@ -838,7 +851,10 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
         // (fill_outside_rect, write_clear); accumulation leaves the rays' state alone
         if (a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
-        auto* kern = a.wide ? march_beam_kernel<true> : march_beam_kernel<false>;
+        auto* kern = a.deep ? (a.wide ? march_beam_kernel<true, kDeepUnroll, kDeepBlocks>
+                                      : march_beam_kernel<false, kDeepUnroll, kDeepBlocks>)
+                            : (a.wide ? march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS>
+                                      : march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS>);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBeamBlock, smem);
         if (per_sm < 1) per_sm = 1;
         kern<<<sms * per_sm, kBeamBlock, smem, stream>>>(a);

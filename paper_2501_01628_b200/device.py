@@ -296,7 +296,7 @@ class DeviceTF:
 def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, partial: torch.Tensor,
           width: int, height: int, samples: Optional[torch.Tensor] = None, skip: bool = True,
           footprint: bool = True, band_clear: bool = False, accum: bool = False,
-          rows: Optional[Tuple[int, int]] = None, force_wide: bool = False) -> None:
+          rows: Optional[Tuple[int, int]] = None, force_wide: bool = False, force_deep: bool = False) -> None:
     """dprt_march: the brick's full-frame premultiplied RGBA partial into ``partial`` (H*W*4 f32).
     ``band_clear``: only the footprint's row band is defined afterwards (band-clipped compositing).
     ``rows`` = (r0, r1): march only those pixel rows; ``partial`` (and ``samples``) hold just them.
@@ -322,8 +322,10 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
         flags |= _lib.MARCH_ACCUM
     if half:
         flags |= _lib.MARCH_HALF
-    if force_wide:  # test hook: the 64-bit-offset kernel of bricks with >= 2^31 quads
+    if force_wide:  # test hook: the addressing of bricks with >= 2^31 quads
         flags |= _lib.MARCH_WIDE
+    if force_deep:  # test hook: the large-brick batch / occupancy configuration
+        flags |= _lib.MARCH_DEEP
     variant = os.environ.get("DPRT_MARCHER", "")
     if variant == "beam":
         flags |= _lib.MARCH_BEAM

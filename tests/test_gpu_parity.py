@@ -436,8 +436,10 @@ def test_partial_writes_stay_in_bounds(cuda_device, oracle_lib):
 
 
 def test_wide_quad_offsets_are_bit_identical(cuda_device, oracle_lib):
-    """Bricks of >= 2^31 apron quads march with 64-bit z-plane offsets (march_beam_kernel<true>); forced
-    onto a small brick, that kernel writes exactly the bytes of the 32-bit one."""
+    """Bricks of >= 2^31 apron quads march with unsigned offsets from the apron base (kWide), bricks of
+    >= 2^28 voxels with 6-sample batches at 2 CTAs/SM (deep); forced onto a small brick, every
+    combination writes exactly the bytes of the default kernel (padded slots and ERT-masked slots add
+    exact zeros whatever the batch length)."""
     f = blob_field((70, 61, 53), seed=12)
     dec = decompose(f, 2)
     W, H = 150, 110
@@ -446,11 +448,12 @@ def test_wide_quad_offsets_are_bit_identical(cuda_device, oracle_lib):
     for r in range(2):
         b = dev.DeviceBrick(dec.brick(r), cuda_device).generate(f)
         out = []
-        for wide in (False, True):
+        for wide, deep in ((False, False), (True, False), (False, True), (True, True)):
             p = torch.empty(H * W * 4, dtype=torch.float32, device=cuda_device)
             s = torch.empty(H * W, dtype=torch.int32, device=cuda_device)
-            dev.march(b, cam, dtf, 0.8, 0.97, p, W, H, samples=s, force_wide=wide)
+            dev.march(b, cam, dtf, 0.8, 0.97, p, W, H, samples=s, force_wide=wide, force_deep=deep)
             out.append((p, s))
         torch.cuda.synchronize()
-        assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+        for p, s in out[1:]:
+            assert torch.equal(out[0][0], p) and torch.equal(out[0][1], s)
         b.close()
