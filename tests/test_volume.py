@@ -111,3 +111,16 @@ def test_default_tf_shape():
     assert np.all(t[x < 0.1, 3] == 0) and abs(t[-1, 3] - 0.05) < 1e-7
     with pytest.raises(UsageError):
         TransferFunction1D(np.zeros((1, 4), np.float32))
+
+
+def test_centre_out_tile_order_is_a_permutation():
+    """The marcher's tile-queue order (march.cu center_out: m, m-1, m+1, m-2, ... with m = n / 2) visits
+    every row index exactly once and ends at the edges -- restated here for the CPU suite."""
+    def center_out(k, n):
+        m, d = n >> 1, (k + 1) >> 1
+        return m - d if k & 1 else m + d
+
+    for n in range(1, 70):
+        seq = [center_out(k, n) for k in range(n)]
+        assert sorted(seq) == list(range(n))
+        assert seq[0] == n // 2 and set(seq[-2:]) <= {0, n - 1} | ({n - 2, 1} if n < 4 else set())

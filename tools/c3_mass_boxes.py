@@ -1,3 +1,5 @@
+"""Config 3's field split into 8 kd bricks balanced by non-empty voxel count (GPU mass function): print each
+brick's cells and apron-quad count (which bricks exceed 2^31 quads and run the wide addressing)."""
 import sys, json
 sys.path.insert(0, "/root/repo")
 import torch
