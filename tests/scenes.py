@@ -22,6 +22,17 @@ RGB8_MAX_LSB = 1
 RGBA_ATOL_F16 = 4e-3  # fp16 fragments: <= P * 2^-11 per channel before blending (P <= 8)
 
 
+def ert_edge_pixels(a_gpu: np.ndarray, a_ref: np.ndarray, ert: float, eps: float = 1e-5) -> np.ndarray:
+    """Pixels where early ray termination can legitimately differ between the f32 GPU path and the f64
+    oracle: one side's accumulated opacity reached ``ert`` (within rounding) at a sample where the other's
+    stayed a hair below it, so the latter takes (at most) one more sample.  Elsewhere both stop -- or run
+    out -- at the same sample and the strict RGBA_ATOL applies."""
+    if ert >= 1.0:
+        return np.zeros(a_gpu.shape, bool)
+    # the side that stopped first ends within rounding of the threshold; the other may hold one more sample
+    return np.abs(np.minimum(a_gpu, a_ref) - ert) <= eps
+
+
 def cam_array(cam: CameraSpec) -> np.ndarray:
     return oracle.camera_array(cam.position, cam.view_dir, cam.up, cam.fov_y, cam.aspect)
 
