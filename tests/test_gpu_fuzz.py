@@ -4,7 +4,8 @@ cameras (outside, grazing, inside the volume), transfer functions, step sizes an
 Per case: every brick's per-pixel owned sample counts are integer-exact, every RGBA partial is within
 RGBA_ATOL of the oracle's, the visibility order equals the oracle's independent kd order, and the
 composited RGB8 frame is within RGB8_MAX_LSB; single-brick cases also check the fused
-single-rank frame byte for byte against march + composite.  Sizes stay small so the oracle finishes
+single-rank frame byte for byte against march + composite, and brick 0 of every case is re-marched with the
+large-brick kernel configurations (wide addressing, deep batches), which must write identical bytes.  Sizes stay small so the oracle finishes
 each case in well under a second.
 """
 
@@ -88,6 +89,12 @@ def test_random_scene_matches_oracle(cuda_device, oracle_lib, seed):
         p = torch.empty(H * W * 4, dtype=torch.float32, device=cuda_device)
         s = torch.empty(H * W, dtype=torch.int32, device=cuda_device)
         dev.march(b, cam, dtf, dt, ert, p, W, H, samples=s)
+        if r == 0:  # the large-brick configurations write the same bytes
+            for wide, deep in ((True, False), (False, True)):
+                p2 = torch.empty_like(p)
+                dev.march(b, cam, dtf, dt, ert, p2, W, H, force_wide=wide, force_deep=deep)
+                torch.cuda.synchronize()
+                assert torch.equal(p, p2), f"case {seed}: wide={wide} deep={deep} kernel differs"
         torch.cuda.synchronize()
         b.close()
         got_s = s.view(H, W).cpu().numpy().astype(np.uint32)
