@@ -46,10 +46,14 @@ typedef struct DprtBrickDesc {
     int64_t lo[3];
     int64_t hi[3];
     int32_t ghost;
-    int32_t reserved;
+    int32_t flags; /* DPRT_BRICK_* (0 = defaults) */
     double origin[3];
     double spacing[3];
 } DprtBrickDesc;
+
+#define DPRT_BRICK_HALF_QUADS 1 /* opt-in: the coefficient quads in fp16 (8 B per voxel instead of 16) -- half
+                                    the quad bytes for memory-bound bricks at a stated precision cost
+                                    (DESIGN.md §5); beam marcher only */
 
 /* Pinhole camera, host-evaluated exactly as CameraSpec.basis() (geom.py:163-168) and
  * camera_primary_ray's half extents (geom.py:250-251). */

@@ -35,6 +35,7 @@ MARCH_ACCUM = 32
 MARCH_HALF = 64
 MARCH_WIDE = 128
 MARCH_DEEP = 256
+BRICK_HALF_QUADS = 1
 COMPOSITE_TONEMAP = 1
 COMPOSITE_RGBA = 2
 COMPOSITE_HALF_IN = 4
@@ -54,7 +55,7 @@ c_int64_3 = ctypes.c_int64 * 3
 
 class BrickDesc(ctypes.Structure):
     _fields_ = [("dims", c_int64_3), ("lo", c_int64_3), ("hi", c_int64_3), ("ghost", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("origin", c_double3), ("spacing", c_double3)]
+                ("flags", ctypes.c_int32), ("origin", c_double3), ("spacing", c_double3)]
 
 
 class Camera(ctypes.Structure):

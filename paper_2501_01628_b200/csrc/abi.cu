@@ -101,6 +101,7 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
             return fail(DPRT_E_USAGE, "spacing/origin on axis %d must be finite, spacing > 0", a);
     }
     if (desc->ghost < 0) return fail(DPRT_E_USAGE, "ghost must be >= 0");
+    if (desc->flags & ~DPRT_BRICK_HALF_QUADS) return fail(DPRT_E_USAGE, "unknown brick flags 0x%x", desc->flags);
     {
         long long nv = 1, nq = 1;
         for (int a = 0; a < 3; ++a) {
@@ -144,8 +145,10 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     b->ray_cap = 0;
     b->counters = nullptr;
     b->quad = nullptr;
+    b->half_quads = (desc->flags & DPRT_BRICK_HALF_QUADS) ? 1 : 0;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&b->quad, (size_t)nq * sizeof(float4));  // 16 B per apron-grid voxel
+    if (e == cudaSuccess)  // 16 B per apron-grid voxel (8 B with fp16 quads)
+        e = cudaMalloc(&b->quad, (size_t)nq * (b->half_quads ? sizeof(uint2) : sizeof(float4)));
     if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * DPRT_MARCH_COUNTER_SLOTS * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc);
@@ -356,7 +359,8 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.vox = b->vox;
     a.qsy = (int)b->qd[0];
     a.qsz = (int)(b->qd[0] * b->qd[1]);
-    a.qorg = b->quad + a.qsz + a.qsy + 1;
+    a.qorg = b->quad + a.qsz + a.qsy + 1;  // fp16 quads: reinterpreted as uint2 at the same element offsets
+    a.half_quads = b->half_quads;
     a.wide = ((long long)b->qd[0] * b->qd[1] * b->qd[2] >= (1LL << 31) || (p->flags & DPRT_MARCH_WIDE)) ? 1 : 0;
     // bricks of >= 2^28 stored voxels (4.3 GB of quads; c3's 1026^3 bricks, not c2's 513^3) touch far more
     // quads than L2 holds per frame: run the deeper-batch, fewer-warp configuration
@@ -375,6 +379,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
     if (rgb8 || a.accum || window || a.half_out) a.beam = 1;  // these outputs exist in the beam marcher only
     if (!a.beam && a.wide) return fail(DPRT_E_USAGE, "the queue marcher takes bricks of < 2^31 quads; use the beam marcher");
+    if (!a.beam && a.half_quads) return fail(DPRT_E_USAGE, "fp16 quads need the beam marcher");
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
     a.n_tf = p->n_tf;
     a.vmin = (float)p->vmin;

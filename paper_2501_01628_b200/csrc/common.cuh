@@ -35,7 +35,9 @@ struct DeviceBrick {
     int64_t s_lo[3];   // first stored voxel (global index)
     int64_t sd[3];     // stored voxel dims
     float* vox;        // sd[0]*sd[1]*sd[2] f32, x fastest
-    float4* quad;      // coefficient quads over the apron grid qd (field.cu quad_kernel)
+    float4* quad;      // coefficient quads over the apron grid qd (field.cu quad_kernel); with
+                       // DPRT_BRICK_HALF_QUADS the same slots hold 4 x fp16 (uint2) instead
+    int half_quads;
     int64_t qd[3];     // quad grid dims = sd + 2 (one apron voxel on every side)
     int64_t mcd[3];    // macrocell grid dims
     float2* macro;     // per macrocell (min, max) over its dilated voxel range
@@ -69,6 +71,7 @@ struct MarchArgs {
     int qsy, qsz;                     // quad strides (apron grid)
     int wide;                         // >= 2^31 apron quads: unsigned offsets from the apron base (kWide)
     int deep;                         // large brick: the memory-latency-bound configuration (kDeepUnroll)
+    int half_quads;                   // quads stored as 4 x fp16 (DPRT_BRICK_HALF_QUADS)
     const uint8_t* __restrict__ skipd;
     int mcd[3];
     int skip;

@@ -188,6 +188,17 @@ __device__ __forceinline__ float trilerp(const float4 q0, const float4 q1, float
     return fmaf(fz, e1 - e0, e0);
 }
 
+// fp16 quads (DPRT_BRICK_HALF_QUADS): the cell's two z-faces as 8-byte loads, widened to f32.
+__device__ __forceinline__ void load_half_quads(const uint2* q, int qsz, float4& qa, float4& qb) {
+    const uint2 ha = __ldg(q), hb = __ldg(q + qsz);
+    const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&ha.x));
+    const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&ha.y));
+    const float2 b0 = __half22float2(*reinterpret_cast<const __half2*>(&hb.x));
+    const float2 b1 = __half22float2(*reinterpret_cast<const __half2*>(&hb.y));
+    qa = make_float4(a0.x, a0.y, a1.x, a1.y);
+    qb = make_float4(b0.x, b0.y, b1.x, b1.y);
+}
+
 // DPRT_BOUNDS_CHECK builds trap on a quad index (relative to qorg, both loads) outside the apron grid.
 __device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, long long qi) {
 #if DPRT_BOUNDS_CHECK
@@ -450,7 +461,8 @@ constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are indep
 // touched quads, L2 hit ~25 %) are memory-latency bound and run 6 @ 2 CTAs -- fewer warps, more loads in
 // flight per warp (c3 slowest ranks -6 to -12 %, c2 +15 %).  Chosen per launch from the
 // brick size (launch_march).
-template <bool kWide, int kUnroll, int kMinBlocks>
+// kHalf: the brick's quads are 4 x fp16 (DPRT_BRICK_HALF_QUADS, opt-in): 8-byte loads, widened to f32 at once.
+template <bool kWide, int kUnroll, int kMinBlocks, bool kHalf>
 __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
@@ -472,6 +484,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
     const unsigned qk = (unsigned)a.qsz + (unsigned)a.qsy + 1u;  // apron offset of stored voxel (0, 0, 0)
     const float4* __restrict__ qbase = a.qorg - qk;            // the apron grid's first quad (kWide)
     const float4* __restrict__ qbase1 = qbase + a.qsz;
+    const uint2* __restrict__ hq_org = reinterpret_cast<const uint2*>(qbase) + qk;  // fp16 quads: 8-byte slots
     const int qsy = a.qsy, qsz = a.qsz;
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1];
@@ -676,13 +689,21 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                         // more than the signed form, no 64-bit registers
                         const unsigned qu = (unsigned)iz * (unsigned)qsz + (unsigned)iy * (unsigned)qsy + (unsigned)ix + qk;
                         quad_bounds_check(a, (long long)qu - qk);
-                        qa[u] = __ldg(qbase + qu);
-                        qb[u] = __ldg(qbase1 + qu);
+                        if constexpr (kHalf) {
+                            load_half_quads(reinterpret_cast<const uint2*>(qbase) + qu, qsz, qa[u], qb[u]);
+                        } else {
+                            qa[u] = __ldg(qbase + qu);
+                            qb[u] = __ldg(qbase1 + qu);
+                        }
                     } else {
                         const int qi = iz * qsz + iy * qsy + ix;
                         quad_bounds_check(a, qi);
-                        qa[u] = __ldg(qorg + qi);
-                        qb[u] = __ldg(qorg1 + qi);
+                        if constexpr (kHalf) {
+                            load_half_quads(hq_org + qi, qsz, qa[u], qb[u]);
+                        } else {
+                            qa[u] = __ldg(qorg + qi);
+                            qb[u] = __ldg(qorg1 + qi);
+                        }
                     }
                     wx[u] = __saturatef(ux - (float)ix);
                     wy[u] = __saturatef(uy - (float)iy);
@@ -851,10 +872,17 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
         // (fill_outside_rect, write_clear); accumulation leaves the rays' state alone
         if (a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
-        auto* kern = a.deep ? (a.wide ? march_beam_kernel<true, kDeepUnroll, kDeepBlocks>
-                                      : march_beam_kernel<false, kDeepUnroll, kDeepBlocks>)
-                            : (a.wide ? march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS>
-                                      : march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS>);
+        using K = void (*)(const MarchArgs);
+        const K kerns[2][2][2] = {  // [half][deep][wide]
+            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false>,
+              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false>},
+             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, false>,
+              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, false>}},
+            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true>,
+              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true>},
+             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, true>,
+              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, true>}}};
+        const K kern = kerns[a.half_quads ? 1 : 0][a.deep ? 1 : 0][a.wide ? 1 : 0];
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBeamBlock, smem);
         if (per_sm < 1) per_sm = 1;
         kern<<<sms * per_sm, kBeamBlock, smem, stream>>>(a);

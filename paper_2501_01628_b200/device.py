@@ -78,13 +78,18 @@ class DeviceBrick:
     Lifetime mirrors the reference's RefCounted objects (refcount.py:10-63): ``close()`` releases the
     native handle; using a closed brick raises UsageError."""
 
-    def __init__(self, desc: BrickDesc, device: torch.device):
+    def __init__(self, desc: BrickDesc, device: torch.device, half_quads: bool = False):
+        """``half_quads`` (opt-in): the coefficient quads in fp16, half the quad bytes for memory-bound bricks
+        at a stated precision cost."""
         if device.type != "cuda":
             raise UsageError("DeviceBrick needs a CUDA device")
         self.desc = desc
         self.device = device
+        self.half_quads = bool(half_quads)
         self.index = device.index if device.index is not None else torch.cuda.current_device()
         d = desc_struct(desc)
+        if half_quads:
+            d.flags |= _lib.BRICK_HALF_QUADS
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().dprt_brick_create(self.index, ctypes.byref(d), ctypes.byref(h)), "dprt_brick_create")
         self._h = h

@@ -171,3 +171,38 @@ def test_random_multirank_frame_matches_oracle(cuda_device, oracle_lib, seed):
         assert np.array_equal(results[r][0], ref_s[r]), f"case {seed} ({mode}, R={R}): rank {r} ownership"
     diff = np.abs(results[0][1].astype(np.int16) - want)
     assert diff.max() <= RGB8_MAX_LSB, f"case {seed} ({mode}, R={R}): RGB8 differs by {diff.max()} LSB"
+
+
+def half_quad_bound(tf) -> float:
+    """Stated per-pixel RGBA bound of the opt-in fp16 quads: each coefficient of the face
+    value a + B fx + C fy + D fx fy rounds once to fp16 (relative 2^-11), so for field values in [0, 1] the
+    sampled value moves by <= 5 * 2^-11; through the TF's steepest channel slope L that moves a sample's
+    colour / opacity by <= 5 * 2^-11 * L, and the front-to-back weights sum to <= 1."""
+    t = tf.as_f32().astype(np.float64)
+    slope = np.abs(np.diff(t, axis=0)).max() * (tf.n - 1) / (tf.vmax - tf.vmin)
+    return RGBA_ATOL + 5 * 2.0 ** -11 * slope
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_half_quads_within_stated_bound(cuda_device, oracle_lib, seed):
+    """Opt-in fp16 coefficient quads (DPRT_BRICK_HALF_QUADS): ownership still exact (the ray setup is f64),
+    RGBA within half_quad_bound of the oracle (ERT-edge pixels as in the f32 sweep)."""
+    f, dec, cam, tf, dt, ert, W, H, bg = _random_case(seed)
+    vox = oracle.generate_field(f.dims, f.blobs)
+    ref, ref_s = oracle_partials(vox, dec, cam, tf, dt, ert, W, H)
+    dtf = dev.DeviceTF(tf, cuda_device)
+    bound = half_quad_bound(tf)
+    amax = float(tf.as_f32()[:, 3].max())
+    for r in range(dec.P):
+        b = dev.DeviceBrick(dec.brick(r), cuda_device, half_quads=True).generate(f)
+        p = torch.empty(H * W * 4, dtype=torch.float32, device=cuda_device)
+        s = torch.empty(H * W, dtype=torch.int32, device=cuda_device)
+        dev.march(b, cam, dtf, dt, ert, p, W, H, samples=s)
+        torch.cuda.synchronize()
+        b.close()
+        assert np.array_equal(s.view(H, W).cpu().numpy().astype(np.uint32), ref_s[r])
+        got = p.view(H, W, 4).cpu().numpy().astype(np.float64)
+        err = np.abs(got - ref[r]).max(axis=2)
+        edge = ert_edge_pixels(got[..., 3], ref[r][..., 3], ert, eps=5 * 2.0 ** -11 * amax * 4)
+        assert err[~edge].max(initial=0) <= bound, f"case {seed}: brick {r} {err.max():.3e} > {bound:.3e}"
+        assert err.max() <= bound + (1.0 - ert) * amax

@@ -16,6 +16,7 @@ from paper_2501_01628_b200.volume import blob_field, decompose, default_tf
 
 ranks = [int(r) for r in sys.argv[1].split(",")] if len(sys.argv) > 1 and sys.argv[1] != "all" else list(range(8))
 STRATEGY = sys.argv[2] if len(sys.argv) > 2 else "even"  # even: 2x2x2 bricks of 1024^3 cells; mass: balanced
+HALF = len(sys.argv) > 3 and sys.argv[3] == "half"      # opt-in fp16 quads
 W, H = 3840, 2160
 d = torch.device("cuda", 0)
 f = blob_field((2049, 2049, 2049), seed=1)
@@ -34,7 +35,7 @@ out = {"W": W, "H": H, "field": list(f.dims), "order": order, "strategy": STRATE
 for r in ranks:
     desc = dec.brick(r)
     t0 = time.time()
-    b = dev.DeviceBrick(desc, d).generate(f)
+    b = dev.DeviceBrick(desc, d, half_quads=HALF).generate(f)
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     for _ in range(3):

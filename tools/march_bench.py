@@ -19,7 +19,8 @@ ap.add_argument("--no-skip", action="store_true")
 ap.add_argument("--threshold", type=float, default=0.1)
 ap.add_argument("--field", choices=["blobs", "ml"], default="blobs")
 ap.add_argument("--rgb8", action="store_true", help="time dprt_march_rgb8 (the single-rank bench step)")
-ap.add_argument("--wide", action="store_true", help="RGBA march forced onto the 64-bit-offset kernel")
+ap.add_argument("--wide", action="store_true", help="RGBA march forced onto the wide-brick addressing")
+ap.add_argument("--half-quads", action="store_true", help="opt-in fp16 coefficient quads")
 args = ap.parse_args()
 d = torch.device("cuda", 0)
 if args.field == "ml":
@@ -31,7 +32,7 @@ else:
 dec = decompose(f, 1)
 cam = auto_camera(f.bounds(), args.W, args.H)
 tf = default_tf(threshold=args.threshold)
-b = dev.DeviceBrick(dec.brick(0), d).generate(f)
+b = dev.DeviceBrick(dec.brick(0), d, half_quads=args.half_quads).generate(f)
 dtf = dev.DeviceTF(tf, d)
 p = torch.empty(args.W * args.H * 4, dtype=torch.float32, device=d)
 s = torch.empty(args.W * args.H, dtype=torch.int32, device=d)
