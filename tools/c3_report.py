@@ -72,5 +72,8 @@ if mass_src.exists():
                  "The kd cuts fall where the integer count of voxels >= 0.1 (the default TF's alpha threshold; "
                  "`device.field_mass_function`, on the GPU) balances; the largest brick then holds more than 2^31 "
                  "apron quads and marches with 64-bit z-plane offsets (`march_beam_kernel<true>`).")
-(ROOT / "profiles" / "r01_c3_per_rank.md").write_text("\n".join(L))
+half_note = ROOT / "profiles" / "r01_c3_half_quads.md"  # the opt-in fp16-quad numbers, kept alongside
+if half_note.exists():
+    L += ["", half_note.read_text().strip()]
+(ROOT / "profiles" / "r01_c3_per_rank.md").write_text("\n".join(L) + "\n")
 print("\n".join(L))
