@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 6
+#define DPRT_ABI_VERSION 7
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -53,7 +53,9 @@ typedef struct DprtBrickDesc {
 
 #define DPRT_BRICK_HALF_QUADS 1 /* opt-in: the coefficient quads in fp16 (8 B per voxel instead of 16) -- half
                                     the quad bytes for memory-bound bricks at a stated precision cost
-                                    (DESIGN.md §5); beam marcher only */
+                                    (DESIGN.md §5); beam marcher only.  The stated bound assumes field values
+                                    in [0, 1] (the rounding error scales with |value|); upload / generate fail
+                                    with DPRT_E_USAGE if any voxel lies outside [-8, 8] */
 
 /* Pinhole camera, host-evaluated exactly as CameraSpec.basis() (geom.py:163-168) and
  * camera_primary_ray's half extents (geom.py:250-251). */
@@ -149,6 +151,14 @@ int dprt_desc_footprint(const DprtBrickDesc* desc, const DprtCamera* cam, int W,
  * footprint) and, if `samples` is non-NULL, the owned lattice sample count per pixel (W*H u32). */
 int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
                uint32_t* samples, int W, int H, void* stream);
+
+/* Roofline instrumentation (diagnostic, synchronous): the same beam march as dprt_march -- ray setup, exact
+ * skipping, slab and batch decisions -- with no image output, counting what it must read and shade:
+ * out[0] = f32 voxels (cells) of the macrocells in which at least one real sample of a live ray is shaded
+ * (x 4 B = the brick bytes a perfect marcher reads once; DESIGN.md §7 "needed bytes"), out[1] = shaded
+ * samples, out[2] = contributing samples (weight > 0), out[3] = those macrocells.  Blocks until done. */
+int dprt_march_stats(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, int W, int H, uint64_t out[4],
+                     void* stream);
 
 /* Single-rank frame (R == 1): the same march with the compositor's over-background and tone map fused
  * into the ray's last step -- writes the (W*H*3) RGB8 frame directly, no RGBA partial, no composite pass.

@@ -29,6 +29,7 @@ from .dvr import (  # noqa: F401
     primary_dirs,
     render_brick,
     render_brick_accum,
+    render_lattice,
     sample_counts,
     slab,
     tone_map_rgb8,

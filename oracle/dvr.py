@@ -19,7 +19,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_build" / "libdvr_oracle.so"
-_ABI = 6
+_ABI = 7
 
 _lib = None
 
@@ -56,6 +56,12 @@ def load_oracle():
     lib.dvr_oracle_lattice.argtypes = [P, P, P, P, ctypes.c_double, P]
     lib.dvr_oracle_lattice.restype = ctypes.c_int64
     lib.dvr_oracle_generate.argtypes = [P, P, P, ctypes.c_int, P, P, ctypes.c_int]
+    lib.dvr_oracle_generate_fast.argtypes = [P, P, P, ctypes.c_int, P, P, ctypes.c_int]
+    lib.dvr_oracle_render_lattice.argtypes = [
+        P, P, P, P, P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+        ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+        ctypes.c_int, P, ctypes.c_int]
+    lib.dvr_oracle_render_lattice.restype = ctypes.c_int
     lib.dvr_oracle_generate_ml.argtypes = [P, P, P, P, P, ctypes.c_int]
     lib.dvr_oracle_det_cos.argtypes = [ctypes.c_double]
     lib.dvr_oracle_det_cos.restype = ctypes.c_double
@@ -140,7 +146,7 @@ def lattice(origin, direction, lo, hi, dt: float) -> Tuple[int, int]:
 # field + bricks
 
 def generate_field(dims, blobs, stored_lo=(0, 0, 0), stored_dims=None,
-                   nthreads: int = 0) -> np.ndarray:
+                   nthreads: int = 0, fast: bool = False) -> np.ndarray:
     """f32 voxels of the blob field over a stored region; array shape (sd_z, sd_y, sd_x).  ``blobs`` may
     also be a FieldSpec-like object with ``kind`` / ``blobs`` / ``ml`` (Marschner-Lobb fields)."""
     if hasattr(blobs, "kind"):
@@ -153,7 +159,8 @@ def generate_field(dims, blobs, stored_lo=(0, 0, 0), stored_dims=None,
     sd = np.asarray(stored_dims if stored_dims is not None else dims, np.int64)
     b = np.ascontiguousarray(blobs, np.float64).reshape(-1, 5)
     out = np.empty((int(sd[2]), int(sd[1]), int(sd[0])), np.float32)
-    load_oracle().dvr_oracle_generate(_ptr(N), _ptr(s_lo), _ptr(sd), len(b), _ptr(b), _ptr(out), nthreads)
+    gen = load_oracle().dvr_oracle_generate_fast if fast else load_oracle().dvr_oracle_generate
+    gen(_ptr(N), _ptr(s_lo), _ptr(sd), len(b), _ptr(b), _ptr(out), nthreads)
     return out
 
 
@@ -239,6 +246,30 @@ def render_brick(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.nd
     if rc != 0:
         raise ValueError(f"oracle render_brick failed with code {rc}")
     return out, samples
+
+
+def render_lattice(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.ndarray, vmin: float,
+                   vmax: float, dt: float, ert: float, width: int, height: int, xs: int, ys: int,
+                   x0: int = 0, y0: int = 0, nthreads: int = 0) -> np.ndarray:
+    """One brick's RGBA partial (f64 premultiplied) on the pixel lattice (x0 + i xs, y0 + j ys): an
+    (ny, nx, 4) array, ny = ceil((H - y0) / ys), nx = ceil((W - x0) / xs)."""
+    vox = np.ascontiguousarray(vox, np.float32)
+    if tuple(vox.shape) != tuple(reversed(brick.stored_dims)):
+        raise ValueError(f"voxel array {vox.shape} does not match stored dims {brick.stored_dims}")
+    geo = np.array([*brick.stored_lo, *brick.stored_dims, *brick.dims, *brick.lo, *brick.hi], np.int64)
+    wgeo = np.array([*brick.origin, *brick.spacing], np.float64)
+    tf = np.ascontiguousarray(tf, np.float32).reshape(-1, 4)
+    tf_scale = (tf.shape[0] - 1) / (float(vmax) - float(vmin))
+    nx = -(-(width - x0) // xs)
+    ny = -(-(height - y0) // ys)
+    out = np.zeros((ny, nx, 4), np.float64)
+    rc = load_oracle().dvr_oracle_render_lattice(
+        _ptr(vox), _ptr(geo), _ptr(wgeo), _ptr(np.ascontiguousarray(cam, np.float64)), _ptr(tf), tf.shape[0],
+        float(vmin), float(tf_scale), float(dt), float(ert), width, height, x0, xs, nx, y0, ys, ny, _ptr(out),
+        nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle render_lattice failed with code {rc}")
+    return out
 
 
 def render_brick_accum(vox: np.ndarray, brick: OracleBrick, cam: np.ndarray, tf: np.ndarray, vmin: float,

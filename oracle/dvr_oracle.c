@@ -26,7 +26,7 @@
 #include <omp.h>
 #endif
 
-#define ORACLE_ABI_VERSION 6
+#define ORACLE_ABI_VERSION 7
 
 int dvr_oracle_version(void) { return ORACLE_ABI_VERSION; }
 
@@ -138,6 +138,47 @@ void dvr_oracle_generate(const int64_t* N, const int64_t* s_lo, const int64_t* s
             float* row = out + (z * sd[1] + y) * sd[0];
             for (int64_t x = 0; x < sd[0]; ++x)
                 row[x] = field_value(N, s_lo[0] + x, s_lo[1] + y, s_lo[2] + z, nb, blobs);
+        }
+}
+
+/* The same voxels as dvr_oracle_generate, faster: per voxel row (y, z) only the blobs whose support can
+ * reach the row are evaluated (the y/z part of r^2 alone already gives q <= 0 for the others, with margin),
+ * in blob order and with the identical per-voxel expression -- a skipped blob is one the scalar loop skips
+ * too (q > 0 false), so every voxel is bit-identical (tests/test_oracle.py).  Used where whole 1024^3
+ * bricks are generated on the host (bench.py's config-3 CPU baseline). */
+void dvr_oracle_generate_fast(const int64_t* N, const int64_t* s_lo, const int64_t* sd, int nb, const double* blobs,
+                              float* out, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < sd[2]; ++z)
+        for (int64_t y = 0; y < sd[1]; ++y) {
+            const int64_t j = s_lo[1] + y, k = s_lo[2] + z;
+            const double uy = N[1] > 1 ? (double)j / (double)(N[1] - 1) : 0.0;
+            const double uz = N[2] > 1 ? (double)k / (double)(N[2] - 1) : 0.0;
+            int live[64];
+            int nl = 0;
+            for (int b = 0; b < nb && b < 64; ++b) {
+                const double* p = blobs + 5 * b;
+                const double dy = uy - p[1], dz = uz - p[2];
+                if ((dy * dy + dz * dz) * p[3] < 1.0 + 1e-9) live[nl++] = b;
+            }
+            float* row = out + (z * sd[1] + y) * sd[0];
+            for (int64_t x = 0; x < sd[0]; ++x) {
+                const int64_t i = s_lo[0] + x;
+                const double ux = N[0] > 1 ? (double)i / (double)(N[0] - 1) : 0.0;
+                double f = 0.0;
+                for (int l = 0; l < nl; ++l) {
+                    const double* p = blobs + 5 * live[l];
+                    double dx = ux - p[0], dy = uy - p[1], dz = uz - p[2];
+                    double r2 = dx * dx + dy * dy + dz * dz;
+                    double q = 1.0 - r2 * p[3];
+                    if (q > 0.0) f = f + p[4] * (q * q * q);
+                }
+                if (f > 1.0) f = 1.0;
+                row[x] = (float)f;
+            }
         }
 }
 
@@ -355,6 +396,31 @@ int dvr_oracle_render_brick(const float* vox, const int64_t* geo, const double* 
 
 /* Ray cycling: continue the accumulated front-to-back state of rows row0 <= y < row1
  * through this brick.  state: H*W*4 doubles (full-frame indexing), read and written in place. */
+/* One brick's RGBA partial on a strided pixel lattice: pixels (x0 + i * xs, y0 + j * ys), i < nx, j < ny,
+ * written compactly to out_rgba[(j * nx + i) * 4] (f64, premultiplied).  The same march_pixel as
+ * dvr_oracle_render_brick, parallel over all sampled pixels (the config-3 CPU baseline's 1/64 subset). */
+int dvr_oracle_render_lattice(const float* vox, const int64_t* geo, const double* wgeo, const double* cam,
+                              const float* tf, int n_tf, double vmin, double tf_scale, double dt, double ert,
+                              int W, int H, int x0, int xs, int nx, int y0, int ys, int ny, double* out_rgba,
+                              int nthreads) {
+    if (n_tf < 2 || !(dt > 0.0) || W <= 0 || H <= 0 || xs <= 0 || ys <= 0 || nx < 0 || ny < 0) return -1;
+    Brick b;
+    int rc = brick_setup(&b, vox, geo, wgeo, tf, n_tf, vmin, tf_scale, dt, ert);
+    if (rc) return rc;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    const int64_t n = (int64_t)nx * ny;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t q = 0; q < n; ++q) {
+        const int px = x0 + (int)(q % nx) * xs, py = y0 + (int)(q / nx) * ys;
+        double rgba[4] = {0.0, 0.0, 0.0, 0.0};
+        if (px < W && py < H) march_pixel(&b, cam, px, py, W, H, rgba, 0);
+        memcpy(out_rgba + 4 * q, rgba, sizeof(rgba));
+    }
+    return 0;
+}
+
 int dvr_oracle_render_brick_accum(const float* vox, const int64_t* geo, const double* wgeo, const double* cam,
                                   const float* tf, int n_tf, double vmin, double tf_scale, double dt, double ert,
                                   int W, int H, int row0, int row1, double* state, int nthreads) {

@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -46,7 +46,7 @@ EXPORTS = (
     "dprt_brick_generate", "dprt_brick_build_macrocells", "dprt_brick_destroy", "dprt_brick_footprint",
     "dprt_march", "dprt_march_rgb8", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
     "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters", "dprt_kat_slab", "dprt_kat_primary_dirs",
-    "dprt_stage_input", "dprt_composite_ranged", "dprt_desc_footprint",
+    "dprt_stage_input", "dprt_composite_ranged", "dprt_desc_footprint", "dprt_march_stats",
 )
 
 c_double3 = ctypes.c_double * 3
@@ -111,6 +111,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_stage_input": ([I, P, P, ctypes.c_uint64, P], I),
         "dprt_composite_ranged": ([I, P, P, I, ctypes.c_int64, P, I, P, P, P], I),
         "dprt_desc_footprint": ([P, P, I, I, P], I),
+        "dprt_march_stats": ([P, P, P, I, I, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

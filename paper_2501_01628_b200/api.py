@@ -255,7 +255,8 @@ class Frame(ApiObject):
         self._result: Optional[FrameResult] = None
         self._complete = False
         self._renderer: Optional[VolumeRenderer] = None
-        self._host_frame: Optional[torch.Tensor] = None
+        self._host_ring: List[torch.Tensor] = []  # pinned RGB8 frames the read-backs alternate between (rank 0)
+        self._host_next = 0
 
     def _on_commit(self) -> None:
         for name in ("world", "camera", "renderer"):
@@ -273,33 +274,61 @@ class Frame(ApiObject):
         return render_frame_collective(self)
 
     def wait(self) -> None:
+        """Blocks until the last render's pixels are in host memory (rank 0; a no-op elsewhere)."""
         self._check_alive()
         if not self._complete:
             raise UsageError("wait_frame before any render")
+        if self._result is not None:
+            self._result._wait()
 
     def map(self) -> Union["FrameResult", _NotRoot]:
         return map_frame(self)
 
 
 class FrameResult:
-    """Mapped RGB8 pixel buffer; valid until the next render completes (api.py:208-229)."""
+    """Mapped RGB8 pixel buffer; valid until the next render completes (api.py:208-229).
 
-    def __init__(self, width: int, height: int, pixels: bytes, sequence: int):
+    The read-back is asynchronous: the frame's bytes are copied into a pinned host buffer on a side stream
+    while the host returns to the application, and ``pixels`` materialises them (waiting for that copy)
+    on first access -- a renderer that never maps a frame, or maps every k-th, pays no host copy for the
+    others.  ``pixels`` returns ``bytes`` like the reference; ``array`` is the same pixels as an (H, W, 3)
+    uint8 view of the pinned buffer without the bytes copy (valid under the same rule)."""
+
+    def __init__(self, width: int, height: int, pixels, sequence: int):
         self.width = width
         self.height = height
         self.sequence = sequence
-        self._pixels = pixels
+        self._pixels = pixels if isinstance(pixels, (bytes, bytearray)) else None
+        self._pending = None if self._pixels is not None else pixels  # engine.HostFrame on its way to the host
         self._valid = True
 
     @property
     def valid(self) -> bool:
         return self._valid
 
-    @property
-    def pixels(self) -> bytes:
+    def _host(self) -> torch.Tensor:
         if not self._valid:
             raise UsageError("frame buffer was invalidated by a newer render")
+        return self._pending.wait()
+
+    @property
+    def array(self) -> np.ndarray:
+        if self._pixels is not None:
+            return np.frombuffer(self._pixels, np.uint8).reshape(self.height, self.width, 3)
+        return self._host().numpy()
+
+    @property
+    def pixels(self) -> bytes:
+        if self._pixels is None:
+            self._pixels = self._host().numpy().tobytes()
+            self._pending = None
+        elif not self._valid:
+            raise UsageError("frame buffer was invalidated by a newer render")
         return self._pixels
+
+    def _wait(self) -> None:
+        if self._pending is not None:
+            self._pending.wait()
 
     def _invalidate(self) -> None:
         self._valid = False
@@ -372,19 +401,27 @@ def render_frame_collective(frame: Frame) -> RenderResult:
         vr.background = background
         vr.dtf.update(tf)
         vr.tf = tf
-    result = vr.render(_camera_spec(camera), width, height, options)
+    host = None
+    if world.device.ep.rank == 0:
+        # two pinned frames: the read-back of this frame never overwrites the previous frame's buffer, which
+        # stays mapped until this render completes (the previous result is invalidated below)
+        if len(frame._host_ring) != 2 or tuple(frame._host_ring[0].shape) != (height, width, 3):
+            if frame._result is not None:
+                frame._result._wait()
+            frame._host_ring = [torch.empty((height, width, 3), dtype=torch.uint8, pin_memory=True)
+                                for _ in range(2)]
+            frame._host_next = 0
+        host = frame._host_ring[frame._host_next]
+        frame._host_next ^= 1
+    hf = vr.render_to_host(_camera_spec(camera), width, height, host, options)
     frame.sequence += 1
     if frame._result is not None:
         frame._result._invalidate()
         frame._result = None
     if world.device.ep.rank == 0:
-        if frame._host_frame is None or tuple(frame._host_frame.shape) != (height, width, 3):
-            frame._host_frame = torch.empty((height, width, 3), dtype=torch.uint8, pin_memory=True)
-        frame._host_frame.copy_(result.rgb8, non_blocking=True)
-        torch.cuda.current_stream(world.device.cuda).synchronize()
-        frame._result = FrameResult(width, height, frame._host_frame.numpy().tobytes(), frame.sequence)
+        frame._result = FrameResult(width, height, hf, frame.sequence)
     frame._complete = True
-    return result
+    return hf.result
 
 
 def map_frame(frame: Frame) -> Union[FrameResult, _NotRoot]:

@@ -9,12 +9,16 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
 
 namespace dprt {
 cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream);
+cudaError_t launch_march_mark(const MarchArgs& a, cudaStream_t stream);
+cudaError_t launch_mark_reduce(const uint8_t* mark, const int mcd[3], const int cells[3], unsigned long long* out,
+                               cudaStream_t stream);
 cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t* tmp, cudaStream_t stream);
 cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cudaStream_t stream);
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream);
@@ -54,12 +58,18 @@ int cuda_fail(cudaError_t e, const char* what) {
         if (_e != cudaSuccess) return cuda_fail(_e, what); \
     } while (0)
 
+// Device binding on every call (a rank thread may have touched another device): the device count is
+// queried once per process, and cudaSetDevice is skipped when the thread is already on `device`.
 int bind(int device) {
-    int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
-    if (device < 0 || device >= n) return fail(DPRT_E_USAGE, "device %d outside [0, %d)", device, n);
-    e = cudaSetDevice(device);
+    static std::once_flag once;
+    static int n_dev = 0;
+    static cudaError_t count_err = cudaSuccess;
+    std::call_once(once, [] { count_err = cudaGetDeviceCount(&n_dev); });
+    if (count_err != cudaSuccess) return cuda_fail(count_err, "cudaGetDeviceCount");
+    if (device < 0 || device >= n_dev) return fail(DPRT_E_USAGE, "device %d outside [0, %d)", device, n_dev);
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur == device) return DPRT_OK;
+    cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
     return DPRT_OK;
 }
@@ -149,7 +159,7 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
     if (e == cudaSuccess)  // 16 B per apron-grid voxel (8 B with fp16 quads)
         e = cudaMalloc(&b->quad, (size_t)nq * (b->half_quads ? sizeof(uint2) : sizeof(float4)));
-    if (e == cudaSuccess) e = cudaMalloc(&b->counters, 2 * DPRT_MARCH_COUNTER_SLOTS * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&b->counters, (2 * DPRT_MARCH_COUNTER_SLOTS + 1) * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
     if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc);
     if (e == cudaSuccess) e = cudaMalloc(&b->skip_tmp, (size_t)nmc);
@@ -182,8 +192,17 @@ int dprt_brick_build_macrocells(DprtBrick* b, void* stream) {
     if (!b) return fail(DPRT_E_USAGE, "null brick");
     int rc = bind(b->device);
     if (rc) return rc;
+    int* flag = b->counters + 2 * DPRT_MARCH_COUNTER_SLOTS;
+    if (b->half_quads) CK(cudaMemsetAsync(flag, 0, sizeof(int), (cudaStream_t)stream), "range flag reset");
     CK(dprt::launch_macrocells(*b, (cudaStream_t)stream), "macrocell kernel launch");
     b->skip_version = 0;  // TF-dependent skip distances must be rebuilt from the new min/max grid
+    if (b->half_quads) {  // commit-time check of the fp16 quads' value range (one 4-byte read-back)
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream), "range flag read");
+        CK(cudaStreamSynchronize((cudaStream_t)stream), "range flag sync");
+        if (h) return fail(DPRT_E_USAGE, "fp16 quads need field values within [-%g, %g] (the stated bound is for [0, 1]); "
+                           "use f32 quads for this field", (double)dprt::kHalfQuadRange, (double)dprt::kHalfQuadRange);
+    }
     return DPRT_OK;
 }
 
@@ -302,7 +321,8 @@ static int box_footprint(const double lo[3], const double hi[3], const DprtCamer
 }
 
 static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
-                      const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream);
+                      const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream,
+                      uint64_t* stats = nullptr);
 
 int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
                uint32_t* samples, int W, int H, void* stream) {
@@ -316,8 +336,15 @@ int dprt_march_rgb8(const DprtBrick* b, const DprtCamera* cam, const DprtMarchPa
     return march_impl(b, cam, p, nullptr, bg, rgb8, samples, W, H, stream);
 }
 
+int dprt_march_stats(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, int W, int H, uint64_t out[4],
+                     void* stream) {
+    if (!out) return fail(DPRT_E_USAGE, "null stats output");
+    return march_impl(b, cam, p, nullptr, nullptr, nullptr, nullptr, W, H, stream, out);
+}
+
 static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
-                      const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream) {
+                      const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream,
+                      uint64_t* stats) {
     if (!b || !cam || !p) return fail(DPRT_E_USAGE, "null march argument");
     if (W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "frame size %dx%d must be positive", W, H);
     if (p->n_tf < 2 || p->n_tf > dprt::kMaxTf || !p->tf_rgba)
@@ -325,6 +352,16 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     if (!(p->vmax > p->vmin)) return fail(DPRT_E_USAGE, "transfer function range needs vmax > vmin");
     if (!(p->dt > 0.0) || !isfinite(p->dt)) return fail(DPRT_E_USAGE, "dt must be finite and > 0");
     if (!(cam->half_w > 0.0) || !(cam->half_h > 0.0)) return fail(DPRT_E_USAGE, "camera half extents must be > 0");
+    {
+        // the sample loop indexes a ray's samples in f32 (exact below 2^24) and 32-bit counts: bound the
+        // samples any ray can own in this brick by the owned box's diagonal / dt
+        double lo[3], hi[3], d2 = 0.0;
+        owned_box(b, lo, hi);
+        for (int a = 0; a < 3; ++a) d2 += (hi[a] - lo[a]) * (hi[a] - lo[a]);
+        if (sqrt(d2) / p->dt + 2.0 >= 16777216.0)
+            return fail(DPRT_E_USAGE, "dt %g gives up to %.0f samples per ray in this brick; the limit is 2^24",
+                        p->dt, sqrt(d2) / p->dt + 2.0);
+    }
     if (p->counter_slot < 0 || p->counter_slot >= DPRT_MARCH_COUNTER_SLOTS)
         return fail(DPRT_E_USAGE, "counter slot %d outside [0, %d)", p->counter_slot, DPRT_MARCH_COUNTER_SLOTS);
     int rc = bind(b->device);
@@ -377,7 +414,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.pix0 = window ? (long long)p->row0 * W : 0;
     a.npix_buf = window ? (long long)(p->row1 - p->row0) * W : (long long)W * H;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
-    if (rgb8 || a.accum || window || a.half_out) a.beam = 1;  // these outputs exist in the beam marcher only
+    if (rgb8 || a.accum || window || a.half_out || stats) a.beam = 1;  // these exist in the beam marcher only
     if (!a.beam && a.wide) return fail(DPRT_E_USAGE, "the queue marcher takes bricks of < 2^31 quads; use the beam marcher");
     if (!a.beam && a.half_quads) return fail(DPRT_E_USAGE, "fp16 quads need the beam marcher");
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
@@ -427,7 +464,35 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
         CK(dprt::launch_skip_build(*mb, a, mb->skip_tmp, (cudaStream_t)stream), "skip-distance build");
         mb->skip_version = p->tf_version;
     }
-    CK(dprt::launch_march(a, (cudaStream_t)stream), "march kernel launch");
+    if (!stats) {
+        CK(dprt::launch_march(a, (cudaStream_t)stream), "march kernel launch");
+        return DPRT_OK;
+    }
+    // dprt_march_stats: instrumented march into a per-macrocell mark grid, reduced to the needed voxels
+    const long long nmc = (long long)b->mcd[0] * b->mcd[1] * b->mcd[2];
+    uint8_t* mark = nullptr;
+    unsigned long long* cnt = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMalloc(&mark, (size_t)nmc), "mark grid");
+    cudaError_t e = cudaMalloc(&cnt, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(mark, 0, (size_t)nmc, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), st);
+    a.mark = mark;
+    a.stats = cnt;
+    if (e == cudaSuccess) e = dprt::launch_march_mark(a, st);
+    const int mcd[3] = {(int)b->mcd[0], (int)b->mcd[1], (int)b->mcd[2]};
+    const int cells[3] = {(int)(b->sd[0] - 1), (int)(b->sd[1] - 1), (int)(b->sd[2] - 1)};
+    if (e == cudaSuccess) e = dprt::launch_mark_reduce(mark, mcd, cells, cnt + 2, st);
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(mark);
+    cudaFree(cnt);
+    if (e != cudaSuccess) return cuda_fail(e, "march stats");
+    stats[0] = h[2];  // voxels (cells) of the marked macrocells
+    stats[1] = h[0];  // shaded samples (real samples of live rays)
+    stats[2] = h[1];  // contributing samples (w > 0)
+    stats[3] = h[3];  // marked macrocells
     return DPRT_OK;
 }
 

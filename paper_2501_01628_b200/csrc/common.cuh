@@ -28,6 +28,7 @@ constexpr int kMaxTf = 1024;       // transfer-function entries held in shared m
 #define DPRT_SKIP_CAP 15
 #endif
 constexpr int kSkipCap = DPRT_SKIP_CAP;  // Chebyshev skip distances are capped at this many macrocells
+constexpr float kHalfQuadRange = 8.0f;  // fp16 quads (DPRT_BRICK_HALF_QUADS) take field values within +-8
 
 struct DeviceBrick {
     int device;
@@ -46,7 +47,7 @@ struct DeviceBrick {
     uint64_t skip_version;  // tf_version the skip distances were built for (0 = never)
     float4* rays;      // ray queue scratch (2 float4 per pixel of the largest frame marched so far)
     long long ray_cap; // pixels the queue can hold
-    int* counters;     // queue counters
+    int* counters;     // queue counters (2 per slot), then the fp16-quad range flag
 };
 
 // Everything the marcher needs, by value (kernel parameter space).
@@ -94,6 +95,8 @@ struct MarchArgs {
     uint32_t* __restrict__ samples;
     float4* rays;   // compacted ray queue: 2 float4 per ray {p0, pixel}, {step, n}
     int* counters;  // [0] rays queued by ray_setup, [1] rays taken by march
+    uint8_t* mark;                    // dprt_march_stats: per-macrocell "a real sample was shaded here" bytes
+    unsigned long long* stats;        // dprt_march_stats: {shaded samples, contributing samples}
     int W, H;
     int rect[4];
 };

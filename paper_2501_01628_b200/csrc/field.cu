@@ -130,7 +130,7 @@ __global__ void macrocell_kernel(const float* __restrict__ vox, long long sd0, l
 // axis, coordinates clamped, hence zero slopes there): sample positions that float rounding puts a hair
 // outside the stored box need no clamp in the marcher and reproduce the oracle's clamped cell exactly.
 __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
-                            float4* __restrict__ quad, int half) {
+                            float4* __restrict__ quad, int half, int* __restrict__ range_flag) {
     const long long qd0 = sd0 + 2, qd1 = sd1 + 2;
     const long long qx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (qx >= qd0) return;
@@ -144,6 +144,9 @@ __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long l
     const float a = r0[x0], b = r0[x1], c = r1[x0], d = r1[x1];
     const long long qi = (qz * qd1 + qy) * qd0 + qx;
     if (half) {  // DPRT_BRICK_HALF_QUADS: the same coefficients, each rounded once to fp16
+        // the stated fp16 bound is for values in [0, 1]; the rounding error grows with |value|
+        // and the slopes overflow past 65504: flag any voxel outside [-kHalfQuadRange, kHalfQuadRange]
+        if (!(fabsf(a) <= kHalfQuadRange)) *range_flag = 1;
         const __half2 ab = __floats2half2_rn(a, b - a), cd = __floats2half2_rn(c - a, (d - c) - (b - a));
         reinterpret_cast<uint2*>(quad)[qi] = make_uint2(*reinterpret_cast<const unsigned*>(&ab),
                                                         *reinterpret_cast<const unsigned*>(&cd));
@@ -156,7 +159,8 @@ cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream) {
     {
         dim3 qb(256);
         dim3 qg((unsigned)((b.qd[0] + 255) / 256), (unsigned)b.qd[1], (unsigned)b.qd[2]);
-        quad_kernel<<<qg, qb, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], b.quad, b.half_quads);
+        quad_kernel<<<qg, qb, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], b.quad, b.half_quads,
+                                           b.counters + 2 * DPRT_MARCH_COUNTER_SLOTS);
     }
     dim3 block(64);
     dim3 grid((unsigned)((b.mcd[0] + 63) / 64), (unsigned)b.mcd[1], (unsigned)b.mcd[2]);

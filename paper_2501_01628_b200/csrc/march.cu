@@ -20,6 +20,8 @@
 
 #include <math.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 #ifndef DPRT_BOUNDS_CHECK
@@ -462,7 +464,10 @@ constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are indep
 // flight per warp (c3 slowest ranks -6 to -12 %, c2 +15 %).  Chosen per launch from the
 // brick size (launch_march).
 // kHalf: the brick's quads are 4 x fp16 (DPRT_BRICK_HALF_QUADS, opt-in): 8-byte loads, widened to f32 at once.
-template <bool kWide, int kUnroll, int kMinBlocks, bool kHalf>
+// kMark (diagnostic instantiation, dprt_march_stats): no image output; every real sample of a live ray sets
+// its macrocell's byte in a.mark and the launch counts shaded / contributing samples into a.stats -- the
+// macrocells the march must read (the roofline's needed bytes) and the shaded-sample rate.
+template <bool kWide, int kUnroll, int kMinBlocks, bool kHalf, bool kMark = false>
 __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
@@ -493,6 +498,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
 #if DPRT_COUNTERS
     unsigned long long c_shade = 0, c_contrib = 0, c_skip = 0, c_rays = 0;
 #endif
+    unsigned long long m_shade = 0, m_contrib = 0;  // kMark only
     while (true) {
         int tile = 0;
         if (lane == 0) tile = atomicAdd(a.counters + 1, 1);
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             int64_t k0 = 0;
             primary_dir(a, px, py, d);
             const int64_t n = lattice_range(a, d, &k0);
-            if (a.samples) a.samples[pix - a.pix0] = (uint32_t)n;
+            if (!kMark && a.samples) a.samples[pix - a.pix0] = (uint32_t)n;
             if (n > 0) {
                 const double t0 = __dmul_rn((double)k0, a.dt);
 #pragma unroll
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         }
         const unsigned hitm = __ballot_sync(FULL, nn > 0);
         if (!hitm) {
-            if (inside && !a.accum) write_clear(a, pix);  // no ray of this beam meets the brick
+            if (!kMark && inside && !a.accum) write_clear(a, pix);  // no ray of this beam meets the brick
             continue;
         }
 #if DPRT_COUNTERS
@@ -728,6 +734,17 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     c_shade += m != 0.f;
                     c_contrib += w > 0.f;
 #endif
+                    if constexpr (kMark) {
+                        if (m != 0.f) {
+                            const float fs = fj + (float)u;
+                            const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
+                            const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
+                            const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                            a.mark[((long long)mz * mcd1 + my) * mcd0 + mx] = 1;
+                            ++m_shade;
+                            m_contrib += w > 0.f;
+                        }
+                    }
                     if (A >= ert) m = 0.f;  // early ray termination: the rest of the batch adds nothing
                 }
                 j += cnt;
@@ -738,7 +755,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             }
             if (j >= nn) live = false;
         }
-        if (inside && (nn > 0 || !a.accum)) {  // accumulated state of a skipped ray stays as it was
+        if (!kMark && inside && (nn > 0 || !a.accum)) {  // accumulated state of a skipped ray stays as it was
             if (a.rgb8) {
                 // single-rank frame: the over-background + tone map of the compositor, fused
                 // (engine.py:500-502); a miss inside the footprint is the background itself
@@ -755,6 +772,11 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 a.out[pix - a.pix0] = make_float4(C0, C1, C2, A);
             }
         }
+    }
+    if constexpr (kMark) {
+        atomicAdd(a.stats, m_shade);
+        atomicAdd(a.stats + 1, m_contrib);
+        return;
     }
     if (!a.accum) {
         // fused clear / background of the pixels no beam covers (no memset pass), done by each warp once
@@ -852,6 +874,37 @@ cudaError_t read_counters(unsigned long long out[4], int reset) {
 }
 
 // Host launchers (called from abi.cu).
+//
+// Per-launch host work is a cache lookup: the SM count per device and the occupancy per (kernel, shared
+// memory, device) are queried once, not on every frame (a frame is ~0.2 ms of device time).
+namespace {
+struct OccKey {
+    const void* kern;
+    size_t smem;
+    int dev;
+    int per_sm;
+};
+std::mutex g_occ_mu;
+OccKey g_occ[64];
+int g_occ_n = 0;
+int g_sms[64];
+
+int grid_for(const void* kern, int block, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    if (g_sms[dev] == 0) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    for (int i = 0; i < g_occ_n; ++i)
+        if (g_occ[i].kern == kern && g_occ[i].smem == smem && g_occ[i].dev == dev) return g_sms[dev] * g_occ[i].per_sm;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (g_occ_n < 64) g_occ[g_occ_n++] = OccKey{kern, smem, dev, per_sm};
+    return g_sms[dev] * per_sm;
+}
+}  // namespace
+
 cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), stream);
     if (e != cudaSuccess) return e;
@@ -862,9 +915,6 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = 2 * a.n_tf * sizeof(float4);
     if (a.beam) {
         // no clear pass: the beam kernel itself writes every pixel it is responsible for -- zero (RGBA
@@ -883,14 +933,57 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
              {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, true>,
               march_beam_kernel<true, kDeepUnroll, kDeepBlocks, true>}}};
         const K kern = kerns[a.half_quads ? 1 : 0][a.deep ? 1 : 0][a.wide ? 1 : 0];
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBeamBlock, smem);
-        if (per_sm < 1) per_sm = 1;
-        kern<<<sms * per_sm, kBeamBlock, smem, stream>>>(a);
+        kern<<<grid_for((const void*)kern, kBeamBlock, smem), kBeamBlock, smem, stream>>>(a);
         return cudaGetLastError();
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, kTileX * kTileY, smem);
-    if (per_sm < 1) per_sm = 1;
-    march_kernel<<<sms * per_sm, block, smem, stream>>>(a);
+    march_kernel<<<grid_for((const void*)march_kernel, kTileX * kTileY, smem), block, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+// dprt_march_stats: the instrumented beam march (the production kernel's ray setup, skipping and batching
+// decisions, no image output) marking the macrocells it shades samples in.
+cudaError_t launch_march_mark(const MarchArgs& a, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(a.counters, 0, 2 * sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+    const size_t smem = 2 * a.n_tf * sizeof(float4);
+    using K = void (*)(const MarchArgs);
+    const K kerns[2][2] = {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false, true>,
+                            march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false, true>},
+                           {march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true, true>,
+                            march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true, true>}};
+    const K kern = kerns[a.half_quads ? 1 : 0][a.wide ? 1 : 0];
+    kern<<<grid_for((const void*)kern, kBeamBlock, smem), kBeamBlock, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+// Sum over the marked macrocells of their cell counts (the f32 voxels a perfect marcher reads once) and the
+// number of marked macrocells.
+__global__ void mark_reduce_kernel(const uint8_t* __restrict__ mark, int m0, int m1, int m2, int c0, int c1, int c2,
+                                   unsigned long long* __restrict__ out) {
+    unsigned long long cells = 0, n = 0;
+    const long long total = (long long)m0 * m1 * m2;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (!mark[i]) continue;
+        const int x = (int)(i % m0), y = (int)((i / m0) % m1), z = (int)(i / ((long long)m0 * m1));
+        const long long ex = min(kMacro, c0 - x * kMacro), ey = min(kMacro, c1 - y * kMacro),
+                        ez = min(kMacro, c2 - z * kMacro);
+        cells += (unsigned long long)(ex * ey * ez);
+        ++n;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        cells += __shfl_down_sync(0xffffffffu, cells, o);
+        n += __shfl_down_sync(0xffffffffu, n, o);
+    }
+    if ((threadIdx.x & 31) == 0 && n) {
+        atomicAdd(out, cells);
+        atomicAdd(out + 1, n);
+    }
+}
+
+cudaError_t launch_mark_reduce(const uint8_t* mark, const int mcd[3], const int cells[3], unsigned long long* out,
+                               cudaStream_t stream) {
+    mark_reduce_kernel<<<148 * 4, 256, 0, stream>>>(mark, mcd[0], mcd[1], mcd[2], cells[0], cells[1], cells[2], out);
     return cudaGetLastError();
 }
 

@@ -346,6 +346,21 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
     _lib.check(rc, "dprt_march")
 
 
+def march_stats(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, width: int, height: int,
+                skip: bool = True) -> dict:
+    """dprt_march_stats (synchronous diagnostic): what the production march reads and shades for this view --
+    ``needed_voxels`` = cells of the macrocells holding a shaded sample (x 4 B: the brick bytes a perfect
+    marcher must read once), ``shaded`` / ``contributing`` samples and the number of such macrocells."""
+    p = tf.params(dt, ert, 0 if skip else _lib.MARCH_NO_SKIP)
+    c = camera_struct(cam)
+    out = (ctypes.c_uint64 * 4)()
+    brick.join_lanes()
+    _lib.check(_lib.lib().dprt_march_stats(brick.handle, ctypes.byref(c), ctypes.byref(p), width, height, out,
+                                           _stream(brick.device)), "dprt_march_stats")
+    return {"needed_voxels": int(out[0]), "needed_bytes": 4 * int(out[0]), "shaded_samples": int(out[1]),
+            "contributing_samples": int(out[2]), "macrocells": int(out[3])}
+
+
 def march_rgb8(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, background,
                rgb8: torch.Tensor, width: int, height: int, samples: Optional[torch.Tensor] = None,
                skip: bool = True, lane: Optional[torch.cuda.Stream] = None,
@@ -473,6 +488,11 @@ def composite_ptrs(device_index: int, ptrs: Sequence[int], npix: int, background
     rc = _lib.lib().dprt_composite_ranged(device_index, arr, rng, len(ptrs), npix, bg_arr, flags,
                                           ctypes.c_void_p(rgb8_ptr), ctypes.c_void_p(rgba_ptr), s)
     _lib.check(rc, "dprt_composite")
+
+
+def enable_peer(device_index: int, peer_index: int) -> None:
+    """NVLink peer access from ``device_index`` to ``peer_index`` (idempotent; TransportError if impossible)."""
+    _lib.check(_lib.lib().dprt_enable_peer(device_index, peer_index), "dprt_enable_peer")
 
 
 def ipc_handle(device_index: int, ptr: int) -> bytes:

@@ -60,7 +60,9 @@ class RenderOptions:
     skip_empty: bool = True            # exact empty-space skipping
     disable_compositing: bool = False  # debug: root shows only its own brick (negative test, engine.py:172)
     frame_index: int = 0
-    keep_float: bool = False           # also return the float RGB image before quantisation (rank 0)
+    keep_float: bool = False           # also return the float RGB image before quantisation on rank 0; COLLECTIVE:
+                                       # it changes the exchange (RGBA gather / peer mapping), so every rank
+                                       # must pass the same value (it is part of the render digest)
     collect_samples: bool = False      # also return per-pixel owned sample counts (this rank)
     mode: str = "dvr"                  # "dvr" or "rankcolor" (rank-ownership visualisation, engine.py:327-332)
     clip_exchange: bool = True         # direct-send / p2p move only each rank's footprint rows;
@@ -164,7 +166,7 @@ def render_digest(cam: CameraSpec, width: int, height: int, options: RenderOptio
         "size": [width, height],
         "dt": options.dt, "ert": options.ert, "composite": options.composite,
         "skip": options.skip_empty, "disableCompositing": options.disable_compositing, "mode": options.mode,
-        "clipExchange": options.clip_exchange, "fragments": options.fragment_dtype,
+        "clipExchange": options.clip_exchange, "fragments": options.fragment_dtype, "keepFloat": options.keep_float,
         "tf": [_tf_hash(tf), tf.vmin, tf.vmax],
         "field": [list(f.dims), list(f.origin), list(f.spacing)],
         "bricks": [[list(lo), list(hi)] for lo, hi in decomposition.boxes],
@@ -218,6 +220,10 @@ class VolumeRenderer:
         self._band_cache = None
 
     def set_tf(self, tf: TransferFunction1D) -> None:
+        # marches of frames still in flight on lane streams may read the old table: the current stream (the
+        # allocator's reuse order for the tensor being dropped) waits for them first
+        if getattr(self, "dtf", None) is not None:
+            self.join()
         self.tf = tf
         self.dtf = dev.DeviceTF(tf, self.brick.device)
 
@@ -254,6 +260,8 @@ class VolumeRenderer:
         if options.mode == "rankcolor":
             rc = rankcolor_tf(self.tf, self.ep.rank)
             if self._rank_dtf is None or self._rank_tf_src is not self.tf:
+                if self._rank_dtf is not None:
+                    self.join()  # lane marches may still read the table being replaced
                 self._rank_dtf = dev.DeviceTF(rc, self.device)
                 self._rank_tf_src = self.tf
             dtf = self._rank_dtf

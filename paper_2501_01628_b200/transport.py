@@ -397,8 +397,21 @@ class InprocEndpoint(RankEndpoint):
             self._get(self.session.acks[(self.rank, peer)], f"receipt from rank {peer}")
 
     def share_pointers(self, device_index: int, ptr: int) -> List[int]:
-        """Same process: peer pointers are plain pointers."""
-        return [int(b) for b in self.all_gather_bytes(str(ptr).encode())]
+        """Same process: peer pointers are plain pointers.  A peer on another GPU is usable once peer access
+        to its device is enabled (NVLink P2P); where that fails the entry is 0, like a refused IPC mapping."""
+        from . import device as dev
+
+        entries = [b.decode().split(":") for b in self.all_gather_bytes(f"{ptr}:{device_index}".encode())]
+        out = []
+        for r, (p, d) in enumerate(entries):
+            p, d = int(p), int(d)
+            if r != self.rank and p and d != device_index:
+                try:
+                    dev.enable_peer(device_index, d)
+                except Exception:  # noqa: BLE001 - no P2P between these GPUs: report the mapping as failed
+                    p = 0
+            out.append(p)
+        return out
 
     def device_barrier(self) -> None:
         import threading
@@ -411,20 +424,31 @@ class InprocEndpoint(RankEndpoint):
             raise TransportError(f"rank {self.rank}: collective aborted") from None
 
 
-def run_collective(num_ranks: int, body, device: Optional[torch.device] = None, timeout: Optional[float] = None):
+def run_collective(num_ranks: int, body, device=None, timeout: Optional[float] = None):
     """Drive ``body(ep)`` on R rank threads of one process (transport.py:519-566); returns per-rank
-    results, re-raising the first rank failure.  A failing rank aborts the others' pending calls."""
+    results, re-raising the first rank failure.  A failing rank aborts the others' pending calls.
+
+    ``device``: one torch device for every rank (tests on one GPU), or a sequence of devices -- rank r is
+    bound to ``device[r % len(device)]``, so one process drives every GPU of the box with one thread per
+    rank, the reference's harness shape (transport.py:545-548).  Rank threads bind their device in each
+    native call (dprt_* bind themselves) and ctypes releases the GIL, so the ranks' launches overlap."""
     import threading
 
     session = _InprocSession(num_ranks, resolve_timeout(timeout))
-    eps = [InprocEndpoint(r, session, device) for r in range(num_ranks)]
+    if isinstance(device, (list, tuple)):
+        if not device:
+            raise TransportError("run_collective needs at least one device")
+        devs = [device[r % len(device)] for r in range(num_ranks)]
+    else:
+        devs = [device] * num_ranks
+    eps = [InprocEndpoint(r, session, devs[r]) for r in range(num_ranks)]
     results: List[object] = [None] * num_ranks
     errors: Dict[int, BaseException] = {}
 
     def runner(ep):
         try:
-            if device is not None and device.type == "cuda":
-                torch.cuda.set_device(device)
+            if ep.device is not None and ep.device.type == "cuda":
+                torch.cuda.set_device(ep.device)
             results[ep.rank] = body(ep)
         except BaseException as exc:  # noqa: BLE001
             errors[ep.rank] = exc
