@@ -512,6 +512,28 @@ def events_ms(fn, steps: int, stream) -> float:
     return a.elapsed_time(b) / steps
 
 
+def graph_ms(fn, steps: int, device) -> float:
+    """Per-launch device ms of ``fn`` captured ``steps`` times into one CUDA graph (replay timed by events):
+    kernels of a few microseconds are otherwise separated by host launch gaps."""
+    import torch
+
+    side = torch.cuda.Stream(device)
+    side.wait_stream(torch.cuda.current_stream(device))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for _ in range(steps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize(device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream(device)
+    a.record(st)
+    g.replay()
+    b.record(st)
+    b.synchronize()
+    return a.elapsed_time(b) / steps
+
+
 def march_leg(dev, brick, desc, cam, dtf, tf, W, H, steps, fused: bool, partial=None, band_clear=False) -> dict:
     """The march kernel alone (CUDA events on its launch stream, K back-to-back launches of the call the
     step makes) + the instrumented march (needed bytes, shaded samples).  SURVEY §8(d) roofline."""
@@ -710,6 +732,77 @@ def per_rank_leg(cfg: str, strategy: str, device, steps: int, warmup: int, R_vir
         if g is not None:
             out["reference_gather"] = g
     return out
+
+
+def c4_orbit_leg(device, steps: int = 5, every: int = 6) -> dict:
+    """Config 4 on one GPU: the lander-like field's 8 uneven mass-balanced bricks all resident, every
+    ``every``-th frame of the 36-frame orbit; per frame every rank's march timed alone (the sort-last frame
+    waits for the slowest) and the visibility order recorded.  Reports the load imbalance the orbit causes."""
+    import torch
+
+    from paper_2501_01628_b200 import device as dev
+
+    wl = build_workload("c4", 8, "mass", mass_device=device)
+    torch.cuda.empty_cache()
+    dtf = dev.DeviceTF(wl.tf, device)
+    bricks = [dev.DeviceBrick(wl.dec.brick(r), device).generate(wl.field) for r in range(8)]
+    part = torch.empty(wl.W * wl.H * 4, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream(device)
+    frames = []
+    with ClockSampler(device.index) as clocks:
+        for i in range(0, len(wl.cams), every):
+            cam = wl.cams[i]
+            ms = []
+            for b in bricks:
+                for _ in range(2):
+                    dev.march(b, cam, dtf, DT, ERT, part, wl.W, wl.H)
+                torch.cuda.synchronize(device)
+                ms.append(events_ms(lambda: dev.march(b, cam, dtf, DT, ERT, part, wl.W, wl.H), steps, stream))
+            frames.append({"frame": i, "order": wl.dec.visibility_order(cam.position), "max_ms": max(ms),
+                           "mean_ms": sum(ms) / len(ms), "rank_ms": ms})
+    for b in bricks:
+        b.close()
+    del bricks, part
+    torch.cuda.empty_cache()
+    return {"workload": wl.text + ", 8 mass-balanced bricks", "bricks": [[list(map(int, lo)), list(map(int, hi))]
+                                                                       for lo, hi in wl.dec.boxes],
+            "frames": frames, "mean_slowest_ms": sum(f["max_ms"] for f in frames) / len(frames),
+            "mean_imbalance": sum(f["max_ms"] / f["mean_ms"] for f in frames) / len(frames),
+            "distinct_orders": len({tuple(f["order"]) for f in frames}), "clocks": clocks.summary()}
+
+
+def c5_blend_leg(device, steps: int = 20) -> dict:
+    """Config 5's per-rank compute on one GPU: the blend + tone map of a rank's row block from P fragments
+    (what each rank runs after the exchange), 1080p-8K x P = 2, 4, 8; bytes = 16 B x P fragments in + 3 B
+    out per pixel, GB/s against the HBM copy peak."""
+    import torch
+
+    from paper_2501_01628_b200 import device as dev
+
+    peak, kind = load_peaks()
+    rows = []
+    stream = torch.cuda.current_stream(device)
+    g = torch.Generator(device=device)
+    g.manual_seed(5)
+    with ClockSampler(device.index) as clocks:
+        for (W, H) in ((1920, 1080), (3840, 2160), (7680, 4320)):
+            for P in (2, 4, 8):
+                n = (H // P) * W
+                frags = [torch.rand(n * 4, generator=g, device=device) * 0.5 for _ in range(P)]
+                out = torch.empty(n * 3, dtype=torch.uint8, device=device)
+                fn = lambda: dev.composite(frags, BACKGROUND, rgb8=out)  # noqa: E731
+                for _ in range(3):
+                    fn()
+                torch.cuda.synchronize(device)
+                ms = graph_ms(fn, steps, device)
+                nbytes = 16 * P * n + 3 * n
+                rows.append({"image": [W, H], "P": P, "block_px": n, "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9,
+                             "frac_hbm": nbytes / (ms * 1e-3) / 1e9 / peak})
+                del frags, out
+    return {"what": "per-rank blend + tone map of a row block (H/P rows) from P fp32 RGBA fragments; "
+                    f"{steps} launches captured in one CUDA graph, replay timed with CUDA events (no host launch "
+                    "gaps between these 10-90 us kernels)", "rows": rows,
+            "peak": peak, "peak_kind": peak_kind_text(kind), "clocks": clocks.summary()}
 
 
 def composite_sweep(ep, device, sizes, modes, steps: int) -> list:
@@ -961,6 +1054,9 @@ def run_ours(args):
         log("[bench] config 3 per-rank leg (8 bricks of 2048^3 at 3840x2160)")
         extras["c3_per_rank"] = {s: per_rank_leg("c3", s, device, 10, 3, cpu=(s == "even") and not args.no_cpu_baseline)
                                  for s in ("even", "mass")}
+        log("[bench] config 4 orbit leg and config 5 blend leg")
+        extras["c4_orbit"] = c4_orbit_leg(device)
+        extras["c5_blend"] = c5_blend_leg(device)
     if rank == 0 and R == 1 and not args.no_traffic:
         log("[bench] ncu child: DRAM bytes of one march launch")
         tr = measure_traffic(cfg)

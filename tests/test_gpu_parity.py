@@ -435,18 +435,20 @@ def test_partial_writes_stay_in_bounds(cuda_device, oracle_lib):
     b.close()
 
 
-def test_wide_quad_offsets_are_bit_identical(cuda_device, oracle_lib):
+@pytest.mark.parametrize("half", [False, True])
+def test_wide_quad_offsets_are_bit_identical(cuda_device, oracle_lib, half):
     """Bricks of >= 2^31 apron quads march with unsigned offsets from the apron base (kWide), bricks of
     >= 2^28 voxels with 6-sample batches at 2 CTAs/SM (deep); forced onto a small brick, every
     combination writes exactly the bytes of the default kernel (padded slots and ERT-masked slots add
-    exact zeros whatever the batch length)."""
+    exact zeros whatever the batch length).  The same holds among the four fp16-quad kernels (``half``),
+    including half+deep (the even config-3 bricks) and half+deep+wide (the mass-balanced ones)."""
     f = blob_field((70, 61, 53), seed=12)
     dec = decompose(f, 2)
     W, H = 150, 110
     cam = auto_camera(f.bounds(), W, H)
     dtf = dev.DeviceTF(dense_tf(), cuda_device)
     for r in range(2):
-        b = dev.DeviceBrick(dec.brick(r), cuda_device).generate(f)
+        b = dev.DeviceBrick(dec.brick(r), cuda_device, half_quads=half).generate(f)
         out = []
         for wide, deep in ((False, False), (True, False), (False, True), (True, True)):
             p = torch.empty(H * W * 4, dtype=torch.float32, device=cuda_device)
