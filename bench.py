@@ -712,17 +712,22 @@ def per_rank_leg(cfg: str, strategy: str, device, steps: int, warmup: int, R_vir
            "mean_march_ms": sum(x["kernel_ms"] for x in ranks) / len(ranks),
            "march_critical_path_frames_per_s": 1000.0 / mx,
            "frame_roofline_per_gpu": {
-               "frac": alg / R_virtual / (mx * 1e-3) / 1e9 / peak,
                "frac_needed": need / R_virtual / (mx * 1e-3) / 1e9 / peak,
-               "slowest_rank_frac": slow["frac"], "slowest_rank_frac_needed": slow["frac_needed"],
+               "frac_survey_8d_bytes": alg / R_virtual / (mx * 1e-3) / 1e9 / peak,
+               "slowest_rank_frac_needed": slow["frac_needed"], "slowest_rank_frac_survey_8d_bytes": slow["frac"],
+               "note": "needed bytes = f32 voxels of the macrocells the march shades in (dprt_march_stats); SURVEY "
+                       "8(d) bytes count whole bricks, which a skipping marcher never reads in full (above 1 on "
+                       "light or oversized mass-balanced bricks)",
                "peak": peak, "peak_kind": peak_kind_text(kind),
                "how": "sum over ranks of bytes / (ranks x slowest rank's march ms) / peak: every GPU of the "
                       "frame waits for the slowest march"},
            "exchange_bytes_per_rank_unclipped": int((1 - 1 / R_virtual) * W * H * 16),
            "rgb8_into_root_bytes": int((R_virtual - 1) / R_virtual * W * H * 3),
-           "ranks": [{k: v for k, v in x.items() if k in (
-               "rank", "box", "kernel_ms", "frac", "frac_needed", "algorithmic_bytes", "needed_bytes",
-               "footprint_px", "shaded_samples", "contributing_samples")} for x in ranks],
+           "ranks": [{"rank": x["rank"], "box": x["box"], "kernel_ms": x["kernel_ms"], "frac_needed": x["frac_needed"],
+                      "frac_survey_8d_bytes": x["frac"], "algorithmic_bytes": x["algorithmic_bytes"],
+                      "needed_bytes": x["needed_bytes"], "footprint_px": x["footprint_px"],
+                      "shaded_samples": x["shaded_samples"], "contributing_samples": x["contributing_samples"],
+                      "shaded_samples_per_s": x["shaded_samples_per_s"]} for x in ranks],
            "clocks": clocks.summary()}
     if cpu:
         log(f"[bench] {cfg} CPU baseline (oracle, strided 1/64 pixel lattice, {R_virtual} bricks)")
@@ -788,20 +793,28 @@ def c5_blend_leg(device, steps: int = 20) -> dict:
         for (W, H) in ((1920, 1080), (3840, 2160), (7680, 4320)):
             for P in (2, 4, 8):
                 n = (H // P) * W
-                frags = [torch.rand(n * 4, generator=g, device=device) * 0.5 for _ in range(P)]
+                nbytes = 16 * P * n + 3 * n
+                # rotate over enough fragment sets that consecutive launches never find their inputs in L2
+                nsets = max(2, -(-3 * 126_000_000 // nbytes))
+                sets = [[torch.rand(n * 4, generator=g, device=device) * 0.5 for _ in range(P)] for _ in range(nsets)]
                 out = torch.empty(n * 3, dtype=torch.uint8, device=device)
-                fn = lambda: dev.composite(frags, BACKGROUND, rgb8=out)  # noqa: E731
+                k = [0]
+
+                def fn():
+                    dev.composite(sets[k[0] % nsets], BACKGROUND, rgb8=out)
+                    k[0] += 1
+
                 for _ in range(3):
                     fn()
                 torch.cuda.synchronize(device)
-                ms = graph_ms(fn, steps, device)
-                nbytes = 16 * P * n + 3 * n
+                ms = graph_ms(fn, max(steps, 2 * nsets), device)
                 rows.append({"image": [W, H], "P": P, "block_px": n, "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9,
-                             "frac_hbm": nbytes / (ms * 1e-3) / 1e9 / peak})
-                del frags, out
+                             "frac_hbm": nbytes / (ms * 1e-3) / 1e9 / peak, "input_sets": nsets})
+                del sets, out
     return {"what": "per-rank blend + tone map of a row block (H/P rows) from P fp32 RGBA fragments; "
-                    f"{steps} launches captured in one CUDA graph, replay timed with CUDA events (no host launch "
-                    "gaps between these 10-90 us kernels)", "rows": rows,
+                    "launches captured in one CUDA graph, replay timed with CUDA events (no host launch gaps between "
+                    "these 10-90 us kernels), rotating over input sets > 3x L2 so no launch reads L2-resident "
+                    "fragments", "rows": rows,
             "peak": peak, "peak_kind": peak_kind_text(kind), "clocks": clocks.summary()}
 
 
@@ -1068,6 +1081,17 @@ def run_ours(args):
                 roof["warp_instructions_per_shaded_sample"] = tr["warp_instructions"] / roof["shaded_samples"]
             if tr.get("thread_instructions") and roof["shaded_samples"]:
                 roof["thread_instructions_per_shaded_sample"] = tr["thread_instructions"] / roof["shaded_samples"]
+            if tr.get("warp_instructions"):
+                # the compute-side roofline of this latency / issue-bound kernel: warp instructions per second
+                # against 4 issue slots per SM per cycle at the max SM clock
+                sms = torch.cuda.get_device_properties(device).multi_processor_count
+                mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("sm_max_mhz", 1965.0)) \
+                    if (ROOT / "MEASURED_PEAKS.json").exists() else 1965.0
+                ipeak = sms * 4 * mhz * 1e6
+                roof["issue_roofline"] = {"achieved_warp_inst_per_s": tr["warp_instructions"] / (roof["kernel_ms"] * 1e-3),
+                                          "peak_warp_inst_per_s": ipeak,
+                                          "frac": tr["warp_instructions"] / (roof["kernel_ms"] * 1e-3) / ipeak,
+                                          "how": f"{sms} SMs x 4 schedulers x {mhz:.0f} MHz"}
         roof["traffic_probe"] = tr
 
     if rank == 0:
