@@ -371,6 +371,9 @@ constexpr int kSlabShift = DPRT_SLAB_SHIFT;
 #ifndef DPRT_TILE_ORDER
 #define DPRT_TILE_ORDER 1
 #endif
+#ifndef DPRT_BLEND_PREFIX
+#define DPRT_BLEND_PREFIX 0
+#endif
 #ifndef DPRT_TILE_PREFETCH
 #define DPRT_TILE_PREFETCH 0  // measured: c2 0.227 -> 0.313 ms (the live index register spills in the 80-register budget)
 #endif
@@ -731,6 +734,45 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     wz[u] = __saturatef(uz - (float)iz);
                 }
                 const int cnt = min(kUnroll, jend - j);
+#if DPRT_BLEND_PREFIX
+                // transmittance form with the per-slot dependency cut to one FMUL: w_u = T_u a_u and
+                // T_{u+1} = T_u (1 - a_u); a slot contributes while the ray is live before it, (1 - T_u) < ert
+                // (the same early-termination rule as A >= ert); A = 1 - T after the last live slot
+                float T = 1.f - A, Tend = T;
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const float v = trilerp(qa[u], qb[u], wx[u], wy[u], wx[u] * wy[u], wz[u]);
+                    const float x = __saturatef(fmaf(v, tns, tno)) * top;
+                    const int ti = (int)x;
+                    const float tfr = x - (float)ti;
+                    const float4 e0 = s_tf[ti], de = s_dtf[ti];
+                    const float al = u < cnt ? fmaf(tfr, de.w, e0.w) : 0.f;
+                    const bool lv = (1.f - T) < ert;
+                    const float w = lv ? T * al : 0.f;
+                    C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
+                    C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
+                    C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
+                    const float m = (lv && u < cnt) ? 1.f : 0.f;
+#if DPRT_COUNTERS
+                    c_shade += m != 0.f;
+                    c_contrib += w > 0.f;
+#endif
+                    if constexpr (kMark) {
+                        if (m != 0.f) {
+                            const float fs = fj + (float)u;
+                            const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
+                            const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
+                            const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                            a.mark[((long long)mz * mcd1 + my) * mcd0 + mx] = 1;
+                            ++m_shade;
+                            m_contrib += w > 0.f;
+                        }
+                    }
+                    T *= 1.f - al;
+                    Tend = lv ? T : Tend;
+                }
+                A = 1.f - Tend;
+#else
                 float m = 1.f;  // 1 while the slot is a real sample of a live ray, then 0
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
@@ -762,6 +804,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     }
                     if (A >= ert) m = 0.f;  // early ray termination: the rest of the batch adds nothing
                 }
+#endif
                 j += cnt;
                 if (A >= ert) {
                     live = false;
