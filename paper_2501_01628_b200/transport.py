@@ -202,6 +202,8 @@ class DistEndpoint(RankEndpoint):
         return allb[(self.rank - 1) % self.R]
 
     def exchange(self, sends, recvs) -> None:
+        if self.backend != "nccl" and any(t.is_cuda for _, t in list(sends) + list(recvs)):
+            return self._exchange_staged(sends, recvs)
         ops = []
         for peer, t in sends:
             ops.append(dist.P2POp(dist.isend, t, peer, group=self.group))
@@ -216,6 +218,28 @@ class DistEndpoint(RankEndpoint):
                 w.wait()
         except Exception as exc:  # noqa: BLE001
             raise TransportError(f"rank {self.rank}: fragment exchange failed: {exc}") from exc
+
+    def _exchange_staged(self, sends, recvs) -> None:
+        """Non-NCCL backends (gloo) move CPU tensors only: device fragments are staged through host memory
+        (the functional multi-process mode on a shared GPU and CPU hosts; NCCL moves them device to device)."""
+        hs = [(peer, t.detach().to("cpu")) if t.is_cuda else (peer, t) for peer, t in sends]
+        hr = [(peer, torch.empty(t.shape, dtype=t.dtype) if t.is_cuda else t) for peer, t in recvs]
+        ops = [dist.P2POp(dist.isend, t, peer, group=self.group) for peer, t in hs]
+        ops += [dist.P2POp(dist.irecv, t, peer, group=self.group) for peer, t in hr]
+        for _, t in hs:
+            self.stats.device_bytes_sent += t.numel() * t.element_size()
+        for _, t in hr:
+            self.stats.device_bytes_received += t.numel() * t.element_size()
+        if not ops:
+            return
+        try:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        except Exception as exc:  # noqa: BLE001
+            raise TransportError(f"rank {self.rank}: fragment exchange failed: {exc}") from exc
+        for (_, dst), (_, src) in zip(recvs, hr):
+            if dst.is_cuda:
+                dst.copy_(src)
 
     def share_pointers(self, device_index: int, ptr: int) -> List[int]:
         """CUDA IPC: export this rank's buffer, map every peer's (lazily enabling NVLink peer access)."""

@@ -63,6 +63,27 @@ def test_ipc_p2p_frame_across_processes(cuda_device, oracle_lib, mode, R, fdt):
                 assert image is None and rgb8 is None
 
 
+@pytest.mark.parametrize("mode,R", [("direct_send", 2), ("binary_swap", 4), ("direct_send", 3)])
+def test_exchange_modes_across_processes(cuda_device, oracle_lib, mode, R):
+    """The exchange schedules through DistEndpoint.exchange (batched isend/irecv, the code NCCL runs at
+    N > 1) in separate processes; gloo moves the device fragments through host staging buffers here."""
+    W, H = 144, 104
+    results = run_ranks(R, _rank_body, mode, W, H, "f32", timeout=240.0)
+    s = c1(P=R, W=W, H=H)
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    ref, _ = oracle_partials(vox, s.dec, s.cam, s.tf, s.dt, s.ert, W, H)
+    want = oracle.composite(ref, s.dec.visibility_order(s.cam.position), s.background)
+    for r, (used, frames) in enumerate(results):
+        assert used == mode
+        for image, rgb8 in frames:
+            if r == 0:
+                assert np.abs(image - want).max() <= RGBA_ATOL
+                q = rgb8.astype(np.int16) - oracle.tone_map_rgb8(want).astype(np.int16)
+                assert np.abs(q).max() <= RGB8_MAX_LSB
+            else:
+                assert image is None and rgb8 is None
+
+
 @pytest.mark.parametrize("fragments", ["f32", "f16"])
 def test_bench_multi_rank_code_path(tmp_path, fragments):
     """bench.py's N > 1 leg (weak-scaled bricks, compositor roofline, e2e, max over ranks) run as two
