@@ -63,7 +63,11 @@ _PARAMS: Dict[str, Dict[str, object]] = {
 
 
 class ApiObject(RefCounted):
-    """Render-graph object with staged and committed parameter sets (api.py:53-95)."""
+    """Render-graph object with two parameter sets (the reference's contract, api.py:53-95): ``set_param``
+    writes the staged set only; ``commit`` publishes a copy of it atomically and locally (no transport
+    traffic), runs the kind's validation hook, and rolls back to the previous committed set if that hook
+    rejects it.  Object-valued parameters keep their children alive: one hold per staged and one per
+    committed reference."""
 
     def __init__(self, device: "Device", kind: str):
         super().__init__()
@@ -76,51 +80,52 @@ class ApiObject(RefCounted):
     def __repr__(self) -> str:
         return f"<{self.kind} refcount={self.refcount}>"
 
-    def set_param(self, name: str, value) -> None:
-        """Stage a parameter; takes effect only at the next commit."""
-        self._check_alive()
-        if name not in _PARAMS[self.kind]:
-            valid = ", ".join(sorted(_PARAMS[self.kind]))
-            raise UsageError(f"{self.kind} has no parameter {name!r}; valid names: {valid}")
-        for child in _handles(self.staged.get(name)):
-            self.drop(child)
-        for child in _handles(value):
+    def _retarget(self, drop_from, hold_in) -> None:
+        """Take holds on the children of ``hold_in`` first, then give up those of ``drop_from`` (a child in
+        both never reaches zero in between)."""
+        for child in _children(hold_in):
             self.hold(child)
+        for child in _children(drop_from):
+            self.drop(child)
+
+    def set_param(self, name: str, value) -> None:
+        self._check_alive()
+        known = _PARAMS[self.kind]
+        if name not in known:
+            raise UsageError(f"{self.kind} has no parameter {name!r}; valid names: {', '.join(sorted(known))}")
+        self._retarget(self.staged.get(name), value)
         self.staged[name] = value
 
     def commit(self) -> None:
-        """Atomically publish the staged parameters; local, no communication."""
         self._check_alive()
-        old = self.committed
-        self.committed = dict(self.staged)
-        for value in self.committed.values():
-            for child in _handles(value):
-                self.hold(child)
-        self.commit_epoch += 1
+        previous, previous_epoch = self.committed, self.commit_epoch
+        snapshot = dict(self.staged)
+        self._retarget((), list(snapshot.values()))
+        self.committed, self.commit_epoch = snapshot, previous_epoch + 1
         try:
             self._on_commit()
         except Exception:
             # a rejected commit leaves the previously committed state in force
-            for value in self.committed.values():
-                for child in _handles(value):
-                    self.drop(child)
-            self.committed = old
-            self.commit_epoch -= 1
+            self._retarget(list(snapshot.values()), ())
+            self.committed, self.commit_epoch = previous, previous_epoch
             raise
-        for value in old.values():
-            for child in _handles(value):
-                self.drop(child)
+        self._retarget(list(previous.values()), ())
 
     def _on_commit(self) -> None:
         pass
 
 
-def _handles(value) -> List[ApiObject]:
-    if isinstance(value, ApiObject):
-        return [value]
-    if isinstance(value, (list, tuple)):
-        return [v for v in value if isinstance(v, ApiObject)]
-    return []
+def _children(value) -> List["ApiObject"]:
+    """ApiObjects referenced by a parameter value (the object itself, or the objects in a list / tuple,
+    one level deep -- the parameter shapes _PARAMS allows)."""
+    items = value if isinstance(value, (list, tuple)) else (value,)
+    out = []
+    for v in items:
+        if isinstance(v, (list, tuple)):
+            out.extend(x for x in v if isinstance(x, ApiObject))
+        elif isinstance(v, ApiObject):
+            out.append(v)
+    return out
 
 
 def _triple(value, name: str, kind=float) -> Tuple:
@@ -344,19 +349,20 @@ class Device:
         self.cuda = cuda
 
     def create(self, kind: str) -> ApiObject:
+        """A new object of ``kind`` with refcount 1; UsageError names the valid kinds otherwise."""
         if kind not in OBJECT_KINDS:
             raise UsageError(f"unknown object kind {kind!r}; valid kinds: {', '.join(OBJECT_KINDS)}")
-        if kind == "world":
-            return World(self)
-        if kind == "frame":
-            return Frame(self)
-        if kind == "spatialField":
-            return SpatialField(self, kind)
-        if kind == "transferFunction1D":
-            return TransferFunctionObject(self, kind)
-        if kind == "volume":
-            return Volume(self, kind)
-        return ApiObject(self, kind)
+        factory = _FACTORIES.get(kind)
+        return factory(self) if factory is not None else ApiObject(self, kind)
+
+
+_FACTORIES = {
+    "world": World,
+    "frame": Frame,
+    "spatialField": lambda d: SpatialField(d, "spatialField"),
+    "transferFunction1D": lambda d: TransferFunctionObject(d, "transferFunction1D"),
+    "volume": lambda d: Volume(d, "volume"),
+}
 
 
 def create_object(device: Device, kind: str) -> ApiObject:
@@ -425,11 +431,8 @@ def render_frame_collective(frame: Frame) -> RenderResult:
 
 
 def map_frame(frame: Frame) -> Union[FrameResult, _NotRoot]:
-    """Rank 0 gets the pixel buffer of the last completed render (api.py:363-371)."""
+    """The last completed render's pixels: a FrameResult on rank 0, NOT_ROOT elsewhere (api.py:363-371)."""
     frame._check_alive()
     if not frame._complete:
         raise UsageError("map_frame before any completed render")
-    if frame.device.ep.rank != 0:
-        return NOT_ROOT
-    assert frame._result is not None
-    return frame._result
+    return frame._result if frame.device.ep.rank == 0 else NOT_ROOT
