@@ -483,7 +483,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": R,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
             "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": wl.config(R, composite=args.composite if R > 1 else "single"),
+            "config": wl.config(R),
             "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                              "host": host_info()},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -1102,8 +1102,9 @@ def run_ours(args):
             "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": R, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": wl.config(R, composite=renderer_mode(args, R), fragments=args.fragments, frames_in_flight=fif,
-                                empty_space_skipping=skip),
+            "config": wl.config(R),
+            "run": {"composite": renderer.compositor.mode if R > 1 else "single (fused into the march)",
+                    "fragments": args.fragments, "frames_in_flight": fif, "empty_space_skipping": skip},
             "roofline": roof,
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "VolumeRenderer.render_to_host (TF from pinned memory, digest verified, RGB8 read-back)"},
@@ -1121,10 +1122,6 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if R > 1:
         dist.destroy_process_group()
-
-
-def renderer_mode(args, R: int) -> str:
-    return "single" if R == 1 else args.composite
 
 
 def api_e2e(ep, device, wl: Workload, args) -> dict:

@@ -42,11 +42,10 @@ def test_default_configs():
 
 def test_reference_arm_config_matches_ours():
     """Both arms build ``config`` from the same Workload.config, so the driver's same-config check holds."""
-    wl = bench.build_workload("c1", 2, "even")
-    ours = wl.config(2, composite="auto", fragments="f32", frames_in_flight=1, empty_space_skipping=True)
-    ref = bench.build_workload("c1", 2, "even").config(2, composite="auto")
-    for k in ("workload", "field", "bricks", "decomposition", "image", "dt_voxels", "ert"):
-        assert ours[k] == ref[k]
+    for cfg, R in (("c1", 2), ("c2", 1), ("c3", 8)):
+        assert bench.build_workload(cfg, R, "even").config(R) == bench.build_workload(cfg, R, "even").config(R)
+    src = (ROOT / "bench.py").read_text()
+    assert src.count('"config": wl.config(R),') == 2  # the reference arm and ours: nothing arm-specific added
 
 
 def test_reference_arm_runs_and_prints_one_line():

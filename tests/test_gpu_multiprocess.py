@@ -107,4 +107,4 @@ def test_bench_multi_rank_code_path(tmp_path, fragments):
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["compositor_roofline"]["mode"] in ("p2p", "direct_send")
-    assert line["config"]["bricks"] == 2 and line["config"]["fragments"] == fragments
+    assert line["config"]["bricks"] == 2 and line["run"]["fragments"] == fragments
