@@ -818,6 +818,69 @@ def c5_blend_leg(device, steps: int = 20) -> dict:
             "peak": peak, "peak_kind": peak_kind_text(kind), "clocks": clocks.summary()}
 
 
+def triangle_trace_leg(device, n_tri: int = 200_000, W: int = 1920, H: int = 1080, steps: int = 10) -> Optional[dict]:
+    """SURVEY §8(f) row 4 (triangle half): the reference's own per-rank compute slot -- numba
+    trace_nearest_batch / trace_any_batch over its BVH (pkg/src/dprt/bvh.py:284-311) -- against
+    dprt_trace_nearest / dprt_trace_any (csrc/trace.cu, bit-identical) on the same Accel and the same
+    1920x1080 primary rays of the reference's auto camera; the reference install in baseline/_ref builds the
+    scene and BVH and runs the CPU side (one thread, as each rank runs it).  None without that install."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "dprt").exists():
+        return None
+    import torch
+
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/dprt_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    from dprt import bvh as ref_bvh, cli as ref_cli, engine as ref_engine, scene as ref_scene
+
+    from paper_2501_01628_b200 import trace
+
+    sc = ref_scene.generate_uneven_cloud(7, n_tri, 8)
+    acc = ref_bvh.build_bvh(sc.triangles)
+    cam = ref_cli.default_camera(sc, W, H)
+
+    class _Ep:
+        rank, R = 0, 1
+
+    prim = ref_engine.gen_primary_batch(_Ep(), cam, W, H)
+    n = len(prim)
+    args = (acc.node_lo, acc.node_hi, acc.node_left, acc.node_right, acc.node_first, acc.node_count, acc.root,
+            acc.tri_v, acc.tri_id)
+    # CPU: the numba slot on a bounded slice of the rays (compile excluded)
+    k = min(n, 20_000)
+    bt, bi = np.full(k, np.inf), np.full(k, trace.MISS_ID, np.int64)
+    ref_bvh.trace_nearest_batch(*args, prim.org[:64], prim.dirn[:64], prim.tmin[:64], prim.tmax[:64], bt[:64], bi[:64])
+    t0 = time.perf_counter()
+    ref_bvh.trace_nearest_batch(*args, prim.org[:k], prim.dirn[:k], prim.tmin[:k], prim.tmax[:k], bt, bi)
+    cpu_s = time.perf_counter() - t0
+    # GPU: all rays, device resident, events
+    b = trace.DeviceBvh.from_accel(acc, device)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+    org, dirn, tmin, tmax = dv(prim.org), dv(prim.dirn), dv(prim.tmin), dv(prim.tmax)
+    best_t = torch.full((n,), float("inf"), dtype=torch.float64, device=device)
+    best_id = torch.full((n,), int(trace.MISS_ID), dtype=torch.int64, device=device)
+
+    def once():
+        best_t.fill_(float("inf"))
+        best_id.fill_(int(trace.MISS_ID))
+        b.trace_nearest(org, dirn, tmin, tmax, best_t, best_id)
+
+    for _ in range(3):
+        once()
+    torch.cuda.synchronize(device)
+    ms = events_ms(once, steps, torch.cuda.current_stream(device))
+    same = bool(np.array_equal(best_t[:k].cpu().numpy().view(np.uint64), bt.view(np.uint64)) and
+                np.array_equal(best_id[:k].cpu().numpy(), bi))
+    hits = int((best_id != int(trace.MISS_ID)).sum().item())
+    return {"what": "nearest-hit traversal of the reference's BVH (200k-triangle uneven cloud, one rank) for the "
+                    f"{W}x{H} primary rays of its auto camera",
+            "rays": n, "hits": hits, "gpu_ms": ms, "gpu_rays_per_s": n / (ms * 1e-3),
+            "reference_numba_rays_per_s": k / cpu_s, "reference_sample_rays": k,
+            "speedup": (n / (ms * 1e-3)) / (k / cpu_s), "bit_identical_on_sample": same,
+            "timing": "GPU: CUDA events over 10 launches incl. the 2 result resets; CPU: one numba call, 1 thread"}
+
+
 def composite_sweep(ep, device, sizes, modes, steps: int) -> list:
     """Config 5: random premultiplied RGBA partials (alpha <= 0.5), every rank composites with each mode;
     device ms per frame (max over ranks), fragment bytes moved, GB/s."""
@@ -1070,6 +1133,10 @@ def run_ours(args):
         log("[bench] config 4 orbit leg and config 5 blend leg")
         extras["c4_orbit"] = c4_orbit_leg(device)
         extras["c5_blend"] = c5_blend_leg(device)
+        log("[bench] triangle traversal leg (the reference's numba slot vs dprt_trace_nearest)")
+        tri = triangle_trace_leg(device)
+        if tri is not None:
+            extras["f4_triangle_trace"] = tri
     if rank == 0 and R == 1 and not args.no_traffic:
         log("[bench] ncu child: DRAM bytes of one march launch")
         tr = measure_traffic(cfg)

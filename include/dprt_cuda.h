@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 7
+#define DPRT_ABI_VERSION 8
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -201,6 +201,34 @@ int dprt_kat_primary_dirs(int device, const DprtCamera* cam, int W, int H, doubl
 /* Instrumented builds (-DDPRT_COUNTERS=1) count {shaded samples, contributing samples, skip steps, rays}
  * in march_kernel; other builds report zeros. */
 int dprt_march_counters(int device, uint64_t out[4], int reset);
+
+/* Triangle BVH traversal (the triangle half): replaces the reference's numba compute slot
+ * trace_nearest_batch / trace_any_batch (pkg/src/dprt/bvh.py:284-311) as called by engine.trace_local_round
+ * (engine.py:254-279), over the same flat Accel arrays (bvh.py:46-60), all DEVICE pointers.  Traversal
+ * stack depth 64 like the reference (bvh.py:23): the caller guarantees a tree depth below 63
+ * (paper_2501_01628_b200/trace.py checks it when it uploads a BVH).  Results are bit-identical to the
+ * reference: float64 throughout, explicitly rounded in its evaluation order. */
+typedef struct DprtBvh {
+    const double* node_lo;      /* (num_nodes, 3) */
+    const double* node_hi;      /* (num_nodes, 3) */
+    const int64_t* node_left;   /* (num_nodes,), -1 for leaves */
+    const int64_t* node_right;  /* (num_nodes,), -1 for leaves */
+    const int64_t* node_first;  /* (num_nodes,) leaf range start */
+    const int64_t* node_count;  /* (num_nodes,) 0 for inner nodes */
+    int64_t num_nodes;
+    int64_t root;               /* -1: empty */
+    const double* tri_v;        /* (num_prims, 9) v0 v1 v2, leaf order */
+    const int64_t* tri_id;      /* (num_prims,) global ids */
+    int64_t num_prims;
+} DprtBvh;
+
+/* In place: (best_t[i], best_id[i]) = min over hits with tmin <= t <= tmax of (t, global id), starting from
+ * the values passed in (the reference's cross-rank (t, gid) reduction, bvh.py:246-248).  org / dirn (n, 3). */
+int dprt_trace_nearest(int device, const DprtBvh* bvh, int64_t n, const double* org, const double* dirn,
+                       const double* tmin, const double* tmax, double* best_t, int64_t* best_id, void* stream);
+/* In place: occluded[i] |= any hit strictly inside (tmin, tmax); rays already occluded are skipped. */
+int dprt_trace_any(int device, const DprtBvh* bvh, int64_t n, const double* org, const double* dirn,
+                   const double* tmin, const double* tmax, uint8_t* occluded, void* stream);
 
 /* Per-frame inputs (TF table, small parameter blocks) from PINNED host memory into device memory, copied
  * by the SMs through the mapped host pointer (one tiny kernel on `stream`), not by a copy engine: a

@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -47,6 +47,7 @@ EXPORTS = (
     "dprt_march", "dprt_march_rgb8", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
     "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters", "dprt_kat_slab", "dprt_kat_primary_dirs",
     "dprt_stage_input", "dprt_composite_ranged", "dprt_desc_footprint", "dprt_march_stats",
+    "dprt_trace_nearest", "dprt_trace_any",
 )
 
 c_double3 = ctypes.c_double * 3
@@ -75,6 +76,13 @@ class MarchParams(ctypes.Structure):
 
 
 MARCH_COUNTER_SLOTS = 4  # DPRT_MARCH_COUNTER_SLOTS
+
+
+class Bvh(ctypes.Structure):
+    _fields_ = [("node_lo", ctypes.c_void_p), ("node_hi", ctypes.c_void_p), ("node_left", ctypes.c_void_p),
+                ("node_right", ctypes.c_void_p), ("node_first", ctypes.c_void_p), ("node_count", ctypes.c_void_p),
+                ("num_nodes", ctypes.c_int64), ("root", ctypes.c_int64), ("tri_v", ctypes.c_void_p),
+                ("tri_id", ctypes.c_void_p), ("num_prims", ctypes.c_int64)]
 
 
 _lib: Optional[ctypes.CDLL] = None
@@ -112,6 +120,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_composite_ranged": ([I, P, P, I, ctypes.c_int64, P, I, P, P, P], I),
         "dprt_desc_footprint": ([P, P, I, I, P], I),
         "dprt_march_stats": ([P, P, P, I, I, P, P], I),
+        "dprt_trace_nearest": ([I, P, ctypes.c_int64, P, P, P, P, P, P, P], I),
+        "dprt_trace_any": ([I, P, ctypes.c_int64, P, P, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -19,7 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libdprt_cuda.so"
-SOURCES = ["abi.cu", "march.cu", "field.cu", "composite.cu"]
+SOURCES = ["abi.cu", "march.cu", "field.cu", "composite.cu", "trace.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

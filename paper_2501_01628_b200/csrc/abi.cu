@@ -16,6 +16,9 @@
 
 namespace dprt {
 cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream);
+struct BvhArgs;
+cudaError_t launch_trace(const BvhArgs& b, long long n, const double* org, const double* dirn, const double* tmin,
+                         const double* tmax, double* best_t, int64_t* best_id, uint8_t* occluded, cudaStream_t stream);
 cudaError_t launch_march_mark(const MarchArgs& a, cudaStream_t stream);
 cudaError_t launch_mark_reduce(const uint8_t* mark, const int mcd[3], const int cells[3], unsigned long long* out,
                                cudaStream_t stream);
@@ -594,6 +597,55 @@ int dprt_kat_primary_dirs(int device, const DprtCamera* cam, int W, int H, doubl
     cudaFree(buf);
     if (e != cudaSuccess) return cuda_fail(e, "primary-ray KAT");
     return DPRT_OK;
+}
+
+namespace dprt {
+struct BvhArgs {  // layout shared with trace.cu
+    const double* lo;
+    const double* hi;
+    const int64_t* left;
+    const int64_t* right;
+    const int64_t* first;
+    const int64_t* count;
+    int64_t root;
+    const double* tv;
+    const int64_t* tid;
+};
+}  // namespace dprt
+
+static int trace_impl(int device, const DprtBvh* bvh, int64_t n, const double* org, const double* dirn,
+                      const double* tmin, const double* tmax, double* best_t, int64_t* best_id, uint8_t* occluded,
+                      void* stream) {
+    if (!bvh) return fail(DPRT_E_USAGE, "null BVH");
+    if (n < 0) return fail(DPRT_E_USAGE, "negative ray count");
+    if (n == 0) return DPRT_OK;
+    if (!org || !dirn || !tmin || !tmax || (!occluded && (!best_t || !best_id)))
+        return fail(DPRT_E_USAGE, "null ray array");
+    if (bvh->root >= bvh->num_nodes || bvh->root < -1) return fail(DPRT_E_USAGE, "BVH root %lld outside [-1, %lld)",
+                                                                  (long long)bvh->root, (long long)bvh->num_nodes);
+    if (bvh->root >= 0 && (!bvh->node_lo || !bvh->node_hi || !bvh->node_left || !bvh->node_right || !bvh->node_first ||
+                           !bvh->node_count || !bvh->tri_v || !bvh->tri_id))
+        return fail(DPRT_E_USAGE, "null BVH array");
+    if (bvh->num_nodes >= (1LL << 31)) return fail(DPRT_E_USAGE, "BVH has %lld nodes; the limit is 2^31 - 1",
+                                                   (long long)bvh->num_nodes);
+    int rc = bind(device);
+    if (rc) return rc;
+    const dprt::BvhArgs b{bvh->node_lo, bvh->node_hi, bvh->node_left, bvh->node_right, bvh->node_first,
+                          bvh->node_count, bvh->root, bvh->tri_v, bvh->tri_id};
+    CK(dprt::launch_trace(b, (long long)n, org, dirn, tmin, tmax, best_t, best_id, occluded, (cudaStream_t)stream),
+       "trace kernel launch");
+    return DPRT_OK;
+}
+
+int dprt_trace_nearest(int device, const DprtBvh* bvh, int64_t n, const double* org, const double* dirn,
+                       const double* tmin, const double* tmax, double* best_t, int64_t* best_id, void* stream) {
+    return trace_impl(device, bvh, n, org, dirn, tmin, tmax, best_t, best_id, nullptr, stream);
+}
+
+int dprt_trace_any(int device, const DprtBvh* bvh, int64_t n, const double* org, const double* dirn,
+                   const double* tmin, const double* tmax, uint8_t* occluded, void* stream) {
+    if (!occluded && n > 0) return fail(DPRT_E_USAGE, "null occlusion array");
+    return trace_impl(device, bvh, n, org, dirn, tmin, tmax, nullptr, nullptr, occluded, stream);
 }
 
 namespace {
