@@ -28,8 +28,10 @@ struct BvhArgs {
 };
 
 // bvh.py:191-220 _node_interval: false on a definite miss (the reference's (1.0, -1.0)).
+// ``inv[axis]`` = 1.0 / d[axis], the reference's per-node reciprocal -- the same correctly rounded value for
+// every node, so it is formed once per ray (a float64 division is a long instruction sequence).
 __device__ __forceinline__ bool node_interval(const BvhArgs& b, int64_t ni, const double o[3], const double d[3],
-                                              double* pt0, double* pt1) {
+                                              const double inv[3], double* pt0, double* pt1) {
     double t0 = -INFINITY, t1 = INFINITY;
 #pragma unroll
     for (int axis = 0; axis < 3; ++axis) {
@@ -38,9 +40,8 @@ __device__ __forceinline__ bool node_interval(const BvhArgs& b, int64_t ni, cons
             if (o[axis] < lo || o[axis] > hi) return false;
             continue;
         }
-        const double inv = __ddiv_rn(1.0, d[axis]);
-        double ta = __dmul_rn(__dsub_rn(lo, o[axis]), inv);
-        double tb = __dmul_rn(__dsub_rn(hi, o[axis]), inv);
+        double ta = __dmul_rn(__dsub_rn(lo, o[axis]), inv[axis]);
+        double tb = __dmul_rn(__dsub_rn(hi, o[axis]), inv[axis]);
         if (ta > tb) {
             const double s = ta;
             ta = tb;
@@ -78,6 +79,32 @@ __device__ __forceinline__ double tri_t(const double* __restrict__ tv, int64_t k
     return __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz)), inv_det);
 }
 
+// Push an inner node's children so that the one whose box centre lies nearer along the ray is popped first.
+// The reference always descends left first (bvh.py:253-255); the order cannot change a result -- every hit is
+// min-reduced with the (t, id) tie-break and a node is pruned only when its entry t exceeds the current best
+// -- but nearer-first lets best_t shrink early and prune more.  The ordering key is float (a heuristic only).
+#ifndef DPRT_TRACE_ORDERED
+#define DPRT_TRACE_ORDERED 1
+#endif
+__device__ __forceinline__ void push_children(const BvhArgs& b, int ni, const float df[3], int* stack, int& sp) {
+    const int l = (int)__ldg(b.left + ni), r = (int)__ldg(b.right + ni);
+#if DPRT_TRACE_ORDERED
+    float kl = 0.f, kr = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        kl = fmaf((float)(__ldg(b.lo + 3 * l + a) + __ldg(b.hi + 3 * l + a)), df[a], kl);
+        kr = fmaf((float)(__ldg(b.lo + 3 * r + a) + __ldg(b.hi + 3 * r + a)), df[a], kr);
+    }
+    const bool left_first = kl <= kr;
+    stack[sp] = left_first ? r : l;
+    stack[sp + 1] = left_first ? l : r;
+#else
+    stack[sp] = r;
+    stack[sp + 1] = l;
+#endif
+    sp += 2;
+}
+
 // bvh.py:223-256 _nearest_one, one thread per ray, (best_t, best_id) min-reduced in place.
 __global__ void __launch_bounds__(128) trace_nearest_kernel(const BvhArgs b, long long n, const double* __restrict__ org,
                                                             const double* __restrict__ dirn,
@@ -91,13 +118,17 @@ __global__ void __launch_bounds__(128) trace_nearest_kernel(const BvhArgs b, lon
             const double o[3] = {org[3 * i], org[3 * i + 1], org[3 * i + 2]};
             const double d[3] = {dirn[3 * i], dirn[3 * i + 1], dirn[3 * i + 2]};
             const double tmin = tmin_a[i], tmax = tmax_a[i];
+            double inv[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) inv[a] = d[a] != 0.0 ? __ddiv_rn(1.0, d[a]) : 0.0;
+            const float df[3] = {(float)d[0], (float)d[1], (float)d[2]};
             int stack[kTraceStack];
             int sp = 0;
             stack[sp++] = (int)b.root;
             while (sp > 0) {
                 const int ni = stack[--sp];
                 double t0, t1;
-                const bool hit = node_interval(b, ni, o, d, &t0, &t1);
+                const bool hit = node_interval(b, ni, o, d, inv, &t0, &t1);
                 const double limit = tmax < best_t ? tmax : best_t;
                 if (!hit || t1 < tmin || t0 > limit) continue;
                 const int64_t cnt = __ldg(b.count + ni);
@@ -113,9 +144,7 @@ __global__ void __launch_bounds__(128) trace_nearest_kernel(const BvhArgs b, lon
                         }
                     }
                 } else {
-                    stack[sp] = (int)__ldg(b.right + ni);
-                    stack[sp + 1] = (int)__ldg(b.left + ni);
-                    sp += 2;
+                    push_children(b, ni, df, stack, sp);
                 }
             }
         }
@@ -134,6 +163,10 @@ __global__ void __launch_bounds__(128) trace_any_kernel(const BvhArgs b, long lo
         const double o[3] = {org[3 * i], org[3 * i + 1], org[3 * i + 2]};
         const double d[3] = {dirn[3 * i], dirn[3 * i + 1], dirn[3 * i + 2]};
         const double tmin = tmin_a[i], tmax = tmax_a[i];
+        double inv[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) inv[a] = d[a] != 0.0 ? __ddiv_rn(1.0, d[a]) : 0.0;
+            const float df[3] = {(float)d[0], (float)d[1], (float)d[2]};
         int stack[kTraceStack];
         int sp = 0;
         stack[sp++] = (int)b.root;
@@ -141,7 +174,7 @@ __global__ void __launch_bounds__(128) trace_any_kernel(const BvhArgs b, long lo
         while (sp > 0 && !occ) {
             const int ni = stack[--sp];
             double t0, t1;
-            if (!node_interval(b, ni, o, d, &t0, &t1) || t1 < tmin || t0 > tmax) continue;
+            if (!node_interval(b, ni, o, d, inv, &t0, &t1) || t1 < tmin || t0 > tmax) continue;
             const int64_t cnt = __ldg(b.count + ni);
             if (cnt > 0) {
                 const int64_t f = __ldg(b.first + ni);
@@ -153,9 +186,7 @@ __global__ void __launch_bounds__(128) trace_any_kernel(const BvhArgs b, long lo
                     }
                 }
             } else {
-                stack[sp] = (int)__ldg(b.right + ni);
-                stack[sp + 1] = (int)__ldg(b.left + ni);
-                sp += 2;
+                push_children(b, ni, df, stack, sp);
             }
         }
         if (occ) occluded[i] = 1;
