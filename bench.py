@@ -1127,6 +1127,7 @@ def run_ours(args):
     if rank == 0 and R == 1 and not args.no_cpu_baseline and cfg in ("c1", "c2", "c3"):
         log("[bench] timing the CPU oracle on a row sample")
         cpu = cpu_baseline_rows(brick.download(), wl)
+    comp_mode = renderer.compositor.mode if R > 1 else "single (fused into the march)"
     brick.close()
     del renderer, brick
     torch.cuda.empty_cache()
@@ -1176,7 +1177,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": wl.config(R),
-            "run": {"composite": renderer.compositor.mode if R > 1 else "single (fused into the march)",
+            "run": {"composite": comp_mode,
                     "fragments": args.fragments, "frames_in_flight": fif, "empty_space_skipping": skip},
             "roofline": roof,
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -397,9 +397,10 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.sy = (long long)b->sd[0];
     a.sz = (long long)b->sd[0] * b->sd[1];
     a.vox = b->vox;
-    a.qsy = (int)b->qd[0];
+    a.qsx = DPRT_QUAD_YFAST ? (int)b->qd[1] : 1;
+    a.qsy = DPRT_QUAD_YFAST ? 1 : (int)b->qd[0];
     a.qsz = (int)(b->qd[0] * b->qd[1]);
-    a.qorg = b->quad + a.qsz + a.qsy + 1;  // fp16 quads: reinterpreted as uint2 at the same element offsets
+    a.qorg = b->quad + a.qsz + a.qsy + a.qsx;  // fp16 quads: reinterpreted as uint2 at the same element offsets
     a.half_quads = b->half_quads;
     a.wide = ((long long)b->qd[0] * b->qd[1] * b->qd[2] >= (1LL << 31) || (p->flags & DPRT_MARCH_WIDE)) ? 1 : 0;
     // bricks of >= 2^28 stored voxels (4.3 GB of quads; c3's 1026^3 bricks, not c2's 513^3) touch far more

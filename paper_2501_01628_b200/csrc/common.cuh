@@ -14,6 +14,15 @@
 #define DPRT_COUNTERS 0
 #endif
 
+// Quad memory order: 0 = x fastest (default), 1 = y fastest, then x, then z.  A warp beam is
+// 4 x 8 pixels, tall in screen y, so with a y-up camera y-fastest quads put one batch's 32 loads into fewer
+// 128-byte lines (c2 host replay: 13.6 -> 9.4 lines per load).  Measured (round 2): c2 0.2270 -> 0.2286 ms,
+// config 3 even rank 5 0.774 -> 0.752, mass rank 7 0.543 -> 0.546 -- line count is not what bounds the
+// loads (profiles/r02_variant_quad_order.json), so x-fastest stays.
+#ifndef DPRT_QUAD_YFAST
+#define DPRT_QUAD_YFAST 0
+#endif
+
 namespace dprt {
 
 #ifndef DPRT_MACRO_SHIFT
@@ -69,7 +78,7 @@ struct MarchArgs {
     long long sy, sz;      // voxel strides
     const float* __restrict__ vox;
     const float4* __restrict__ qorg;  // coefficient quad of stored voxel (0,0,0); apron at index -1 and sd
-    int qsy, qsz;                     // quad strides (apron grid)
+    int qsx, qsy, qsz;                // quad strides (apron grid; DPRT_QUAD_YFAST: y is the unit stride)
     int wide;                         // >= 2^31 apron quads: unsigned offsets from the apron base (kWide)
     int deep;                         // large brick: the memory-latency-bound configuration (kDeepUnroll)
     int half_quads;                   // quads stored as 4 x fp16 (DPRT_BRICK_HALF_QUADS)

@@ -132,9 +132,15 @@ __global__ void macrocell_kernel(const float* __restrict__ vox, long long sd0, l
 __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
                             float4* __restrict__ quad, int half, int* __restrict__ range_flag) {
     const long long qd0 = sd0 + 2, qd1 = sd1 + 2;
+#if DPRT_QUAD_YFAST
+    const long long qy = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (qy >= qd1) return;
+    const long long qx = blockIdx.y, qz = blockIdx.z;
+#else
     const long long qx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (qx >= qd0) return;
     const long long qy = blockIdx.y, qz = blockIdx.z;
+#endif
     auto cl = [](long long v, long long n) { return v < 0 ? 0 : (v >= n ? n - 1 : v); };
     const long long x0 = cl(qx - 1, sd0), x1 = cl(qx, sd0);
     const long long y0 = cl(qy - 1, sd1), y1 = cl(qy, sd1);
@@ -142,7 +148,11 @@ __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long l
     const float* r0 = vox + (z * sd1 + y0) * sd0;
     const float* r1 = vox + (z * sd1 + y1) * sd0;
     const float a = r0[x0], b = r0[x1], c = r1[x0], d = r1[x1];
+#if DPRT_QUAD_YFAST
+    const long long qi = (qz * qd0 + qx) * qd1 + qy;
+#else
     const long long qi = (qz * qd1 + qy) * qd0 + qx;
+#endif
     if (half) {  // DPRT_BRICK_HALF_QUADS: the same coefficients, each rounded once to fp16
         // the stated fp16 bound is for values in [0, 1]; the rounding error grows with |value|
         // and the slopes overflow past 65504: flag any voxel outside [-kHalfQuadRange, kHalfQuadRange]
@@ -158,7 +168,11 @@ __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long l
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream) {
     {
         dim3 qb(256);
+#if DPRT_QUAD_YFAST
+        dim3 qg((unsigned)((b.qd[1] + 255) / 256), (unsigned)b.qd[0], (unsigned)b.qd[2]);
+#else
         dim3 qg((unsigned)((b.qd[0] + 255) / 256), (unsigned)b.qd[1], (unsigned)b.qd[2]);
+#endif
         quad_kernel<<<qg, qb, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], b.quad, b.half_quads,
                                            b.counters + 2 * DPRT_MARCH_COUNTER_SLOTS);
     }

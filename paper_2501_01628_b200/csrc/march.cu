@@ -201,10 +201,23 @@ __device__ __forceinline__ void load_half_quads(const uint2* q, int qsz, float4&
     qb = make_float4(b0.x, b0.y, b1.x, b1.y);
 }
 
+// Quad offset of cell (ix, iy, iz) from the stored voxel (0, 0, 0) (memory order: DPRT_QUAD_YFAST); the unit
+// stride is a plain add, so the index costs two IMADs in either order.
+template <typename T>
+__device__ __forceinline__ T quad_offset(T ix, T iy, T iz, T qsx, T qsy, T qsz) {
+#if DPRT_QUAD_YFAST
+    (void)qsy;
+    return iz * qsz + ix * qsx + iy;
+#else
+    (void)qsx;
+    return iz * qsz + iy * qsy + ix;
+#endif
+}
+
 // DPRT_BOUNDS_CHECK builds trap on a quad index (relative to qorg, both loads) outside the apron grid.
 __device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, long long qi) {
 #if DPRT_BOUNDS_CHECK
-    const long long org = (long long)a.qsz + a.qsy + 1, total = (long long)a.qsz * (a.sd[2] + 2);
+    const long long org = (long long)a.qsz + a.qsy + a.qsx, total = (long long)a.qsz * (a.sd[2] + 2);
     if (qi + org < 0 || qi + org + a.qsz >= total) __trap();
 #endif
 }
@@ -246,7 +259,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
     const int total = a.counters[0];  // written by ray_setup_kernel, which completed before this launch
     const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
     const float4* __restrict__ qorg = a.qorg;
-    const int qsy = a.qsy, qsz = a.qsz;
+    const int qsx = a.qsx, qsy = a.qsy, qsz = a.qsz;
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1], skip = a.skip;
     const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
@@ -331,7 +344,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                 continue;
             }
             // trilinear + TF (§2.6) + front-to-back blend (§2.7) of one sample
-            const int qi = iz * qsz + iy * qsy + ix;
+            const int qi = quad_offset(ix, iy, iz, qsx, qsy, qsz);
             quad_bounds_check(a, qi);
             const float4* q = qorg + qi;
             const float fx = __saturatef(ux - (float)ix), fy = __saturatef(uy - (float)iy);
@@ -492,11 +505,11 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
     const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
     const float4* __restrict__ qorg = a.qorg;
     const float4* __restrict__ qorg1 = a.qorg + a.qsz;  // the cell's far z-face
-    const unsigned qk = (unsigned)a.qsz + (unsigned)a.qsy + 1u;  // apron offset of stored voxel (0, 0, 0)
+    const unsigned qk = (unsigned)a.qsz + (unsigned)a.qsy + (unsigned)a.qsx;  // apron offset of stored voxel (0, 0, 0)
     const float4* __restrict__ qbase = a.qorg - qk;            // the apron grid's first quad (kWide)
     const float4* __restrict__ qbase1 = qbase + a.qsz;
     const uint2* __restrict__ hq_org = reinterpret_cast<const uint2*>(qbase) + qk;  // fp16 quads: 8-byte slots
-    const int qsy = a.qsy, qsz = a.qsz;
+    const int qsx = a.qsx, qsy = a.qsy, qsz = a.qsz;
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1];
     const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
@@ -711,7 +724,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                         // >= 2^31 quads: offset from the apron grid's first quad as unsigned 32-bit (exact
                         // below 2^32 quads -- modular arithmetic, the true offset is non-negative); one IADD
                         // more than the signed form, no 64-bit registers
-                        const unsigned qu = (unsigned)iz * (unsigned)qsz + (unsigned)iy * (unsigned)qsy + (unsigned)ix + qk;
+                        const unsigned qu = quad_offset((unsigned)ix, (unsigned)iy, (unsigned)iz, (unsigned)qsx, (unsigned)qsy, (unsigned)qsz) + qk;
                         quad_bounds_check(a, (long long)qu - qk);
                         if constexpr (kHalf) {
                             load_half_quads(reinterpret_cast<const uint2*>(qbase) + qu, qsz, qa[u], qb[u]);
@@ -720,7 +733,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                             qb[u] = __ldg(qbase1 + qu);
                         }
                     } else {
-                        const int qi = iz * qsz + iy * qsy + ix;
+                        const int qi = quad_offset(ix, iy, iz, qsx, qsy, qsz);
                         quad_bounds_check(a, qi);
                         if constexpr (kHalf) {
                             load_half_quads(hq_org + qi, qsz, qa[u], qb[u]);
