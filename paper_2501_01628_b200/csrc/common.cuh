@@ -18,7 +18,7 @@
 // 4 x 8 pixels, tall in screen y, so with a y-up camera y-fastest quads put one batch's 32 loads into fewer
 // 128-byte lines (c2 host replay: 13.6 -> 9.4 lines per load).  Measured (round 2): c2 0.2270 -> 0.2286 ms,
 // config 3 even rank 5 0.774 -> 0.752, mass rank 7 0.543 -> 0.546 -- line count is not what bounds the
-// loads (profiles/r02_variant_quad_order.json), so x-fastest stays.
+// loads (profiles/r02_variant_memory_side.json), so x-fastest stays.
 #ifndef DPRT_QUAD_YFAST
 #define DPRT_QUAD_YFAST 0
 #endif
