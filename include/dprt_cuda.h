@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 8
+#define DPRT_ABI_VERSION 9
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -181,6 +181,47 @@ int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, 
  * (DESIGN.md §6); ranges = NULL means every fragment covers the whole tile. */
 int dprt_composite_ranged(int device, const float* const* inputs, const int64_t* ranges, int P, int64_t npix,
                           const float bg[3], int flags, uint8_t* rgb8, float* rgba_out, void* stream);
+
+/* Fused march + exchange ("p2p_push"): the march of one rank writes each row block b of its
+ * RGBA partial (assign_pixels rows [row_start[b], row_start[b+1]), engine.py:216-221) straight into block
+ * b's owner -- a peer pointer over NVLink -- as its tiles finish, so the fragment exchange overlaps the
+ * march tile by tile (the reference's cycle_batch / ring_exchange step, engine.py:282-310,
+ * transport.py:457-462, and the pull of the fused P2P compositor both disappear).  When the launch's last
+ * CTA retires, every CTA having fenced its stores at system scope, it release-stores `epoch` into flags[b]
+ * for every b (the slot for THIS rank in block b's owner's flag array).  The owner blends once all P flags
+ * of its block reach the frame's epoch (dprt_wait_flags, then dprt_composite_ranged on local memory).
+ * All arrays are HOST arrays of P entries; pointers are device pointers (local or peer-mapped). */
+#define DPRT_MAX_PUSH 16
+typedef struct DprtPushTargets {
+    int32_t P;                 /* row blocks (ranks), 2..DPRT_MAX_PUSH */
+    int32_t reserved;
+    const int32_t* row_start;  /* P + 1 row boundaries, row_start[0] = 0, row_start[P] = H */
+    void* const* dst;          /* dst[b]: this rank's fragment of block b at its owner; pixel (x, y) of the
+                                  block at element (y - row_start[b]) * W + x (16 B f32 / 8 B fp16 RGBA) */
+    uint32_t* const* flags;    /* flags[b]: this rank's epoch word at block b's owner */
+    uint32_t* counter;         /* device word, zero before the first launch (self-resetting CTA count) */
+    uint32_t epoch;            /* frame tag written to every flags[b]; nonzero, increasing per frame */
+    uint32_t reserved2;
+} DprtPushTargets;
+
+/* dprt_march into peers' inboxes (DprtPushTargets).  Row windows and accumulation are not available here;
+ * DPRT_MARCH_HALF selects fp16 fragments, DPRT_MARCH_BAND_CLEAR clears only the footprint's row band. */
+int dprt_march_push(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, const DprtPushTargets* t,
+                    uint32_t* samples, int W, int H, void* stream);
+
+/* Stream-ordered wait: work issued on `stream` after this call runs once every flags[i] (i < n, device words,
+ * e.g. written by peers' dprt_march_push or dprt_signal_flags) has reached `epoch` (wrap-safe compare).  One
+ * 32-thread CTA spins with acquire loads at system scope.  Only for flags written by work that does not
+ * itself wait on this stream -- other GPUs, or work already complete. */
+int dprt_wait_flags(int device, const uint32_t* flags, int n, uint32_t epoch, void* stream);
+
+/* dprt_composite_ranged that also signals: when its last CTA retires (every CTA having fenced its stores
+ * -- e.g. RGB8 rows written into rank 0's frame over NVLink -- at system scope) it release-stores `epoch`
+ * into flags[i] (i < n_flags; HOST array of device pointers, local or peer).  counter: a device word, zero
+ * before the first launch (self-resetting). */
+int dprt_composite_signal(int device, const float* const* inputs, const int64_t* ranges, int P, int64_t npix,
+                          const float bg[3], int flags, uint8_t* rgb8, float* rgba_out, uint32_t* counter,
+                          uint32_t* const* signal, int n_signal, uint32_t epoch, void* stream);
 
 /* Peer memory over NVLink for the fused direct-send compositor (one process per GPU).  Buffers that peers
  * map must come from dprt_device_alloc so the IPC handle covers exactly [ptr, ptr + bytes). */

@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -47,8 +47,9 @@ EXPORTS = (
     "dprt_march", "dprt_march_rgb8", "dprt_composite", "dprt_ipc_handle", "dprt_ipc_open", "dprt_ipc_close",
     "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters", "dprt_kat_slab", "dprt_kat_primary_dirs",
     "dprt_stage_input", "dprt_composite_ranged", "dprt_desc_footprint", "dprt_march_stats",
-    "dprt_trace_nearest", "dprt_trace_any",
+    "dprt_trace_nearest", "dprt_trace_any", "dprt_march_push", "dprt_wait_flags", "dprt_composite_signal",
 )
+MAX_PUSH = 16  # DPRT_MAX_PUSH
 
 c_double3 = ctypes.c_double * 3
 c_int64_3 = ctypes.c_int64 * 3
@@ -83,6 +84,12 @@ class Bvh(ctypes.Structure):
                 ("node_right", ctypes.c_void_p), ("node_first", ctypes.c_void_p), ("node_count", ctypes.c_void_p),
                 ("num_nodes", ctypes.c_int64), ("root", ctypes.c_int64), ("tri_v", ctypes.c_void_p),
                 ("tri_id", ctypes.c_void_p), ("num_prims", ctypes.c_int64)]
+
+
+class PushTargets(ctypes.Structure):
+    _fields_ = [("P", ctypes.c_int32), ("reserved", ctypes.c_int32), ("row_start", ctypes.c_void_p),
+                ("dst", ctypes.c_void_p), ("flags", ctypes.c_void_p), ("counter", ctypes.c_void_p),
+                ("epoch", ctypes.c_uint32), ("reserved2", ctypes.c_uint32)]
 
 
 _lib: Optional[ctypes.CDLL] = None
@@ -122,6 +129,9 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_march_stats": ([P, P, P, I, I, P, P], I),
         "dprt_trace_nearest": ([I, P, ctypes.c_int64, P, P, P, P, P, P, P], I),
         "dprt_trace_any": ([I, P, ctypes.c_int64, P, P, P, P, P, P], I),
+        "dprt_march_push": ([P, P, P, P, P, I, I, P], I),
+        "dprt_wait_flags": ([I, P, I, ctypes.c_uint32, P], I),
+        "dprt_composite_signal": ([I, P, P, I, ctypes.c_int64, P, I, P, P, P, P, I, ctypes.c_uint32, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

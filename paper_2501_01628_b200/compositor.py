@@ -14,6 +14,9 @@ non-commutative 'over' in brick visibility order instead, so this module exchang
 * ``p2p``: one kernel per rank reads the P fragments of its row block straight out of the peers'
   partial buffers over NVLink (CUDA IPC mappings), blends, tone-maps and writes the RGB8 tile directly
   into rank 0's frame -- the exchange, the blend and the gather fused.
+* ``p2p_push``: the march itself writes each row block of its partial into the block owner's inbox over
+  NVLink as its tiles finish (the exchange overlaps the march), epoch flags in peer memory replace the
+  barriers, and the blend reads local memory only (``p2p.P2PPushCompositor``).
 
 Fragment bytes per rank per frame are (1 - 1/P)*W*H*16 in both exchange modes.  The
 blend itself always runs in libdprt_cuda.so (``CudaBlender``); there is no CPU blend in the product.
@@ -136,7 +139,7 @@ class Compositor:
             return "auto"  # p2p if every rank can map its peers (decided collectively), else direct_send
         if mode == "binary_swap" and P & (P - 1):
             raise UsageError(f"binary_swap needs a power-of-two rank count, got {P}")
-        if mode not in ("direct_send", "binary_swap", "p2p", "cycle"):
+        if mode not in ("direct_send", "binary_swap", "p2p", "p2p_push", "cycle"):
             raise UsageError(f"unknown composite mode {mode!r}")
         return mode  # "cycle": the renderer moves rays, this object only gathers the tiles
 
@@ -159,7 +162,7 @@ class Compositor:
 
     def clips_bands(self) -> bool:
         """True when this mode reads only each rank's footprint row band (``bands`` in composite)."""
-        return self.mode in ("direct_send", "p2p")
+        return self.mode in ("direct_send", "p2p", "p2p_push")
 
     # ------------------------------------------------------------------------------------------
     def composite(self, partial: torch.Tensor, order: Sequence[int], background, keep_float: bool = False,
@@ -180,7 +183,29 @@ class Compositor:
             return self._direct_send(partial, order, background, keep_float, bands)
         if self.mode == "binary_swap":
             return self._binary_swap(partial, order, background, keep_float)
+        if self.mode == "p2p_push":
+            # the march already pushed this frame's fragments (push_targets); blend what arrived
+            out = self._push().composite(order, background, keep_float, bands)
+            self.last_bytes = self._push_impl.last_bytes
+            return out
         return self._p2p_composite(partial, order, background, keep_float, bands)
+
+    def _push(self):
+        if getattr(self, "_push_impl", None) is None:
+            from .p2p import P2PPushCompositor
+            impl = P2PPushCompositor.try_create(self.ep, self.W, self.H, self.device, self.fdt)
+            if impl is None:
+                raise TransportError("p2p_push needs every rank on its own GPU with its peers' buffers mapped "
+                                     "(CUDA IPC over NVLink); use composite='p2p' or 'direct_send'")
+            self._push_impl = impl
+        return self._push_impl
+
+    def push_targets(self):
+        """p2p_push: start a frame and return the march's push targets (row_start, dst, flags, counter,
+        epoch); None in every other mode (the march writes the local partial)."""
+        if self.mode != "p2p_push":
+            return None
+        return self._push().march_targets()
 
     def _single(self, partial, background, keep_float) -> CompositeOutput:
         if self.ep.rank != 0:

@@ -26,6 +26,7 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
 cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cudaStream_t stream);
 cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream);
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream);
+cudaError_t launch_wait_flags(const unsigned* flags, int n, unsigned epoch, cudaStream_t stream);
 cudaError_t read_counters(unsigned long long out[4], int reset);
 cudaError_t launch_kat_slab(const double* o, const double* d, const double* lo, const double* hi, int n, double* t01,
                             int* hit);
@@ -37,6 +38,15 @@ struct DprtBrick : dprt::DeviceBrick {};
 namespace {
 
 thread_local std::string g_err;
+
+// dprt_composite_signal's completion signal, handed to dprt_composite_ranged on the calling thread
+struct PendingSignal {
+    int n = 0;
+    uint32_t epoch = 0;
+    uint32_t* counter = nullptr;
+    uint32_t* flags[DPRT_MAX_PUSH] = {};
+};
+thread_local PendingSignal g_sig;
 
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char* fmt, ...) {
@@ -325,7 +335,7 @@ static int box_footprint(const double lo[3], const double hi[3], const DprtCamer
 
 static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
                       const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream,
-                      uint64_t* stats = nullptr);
+                      uint64_t* stats = nullptr, const DprtPushTargets* push = nullptr);
 
 int dprt_march(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
                uint32_t* samples, int W, int H, void* stream) {
@@ -345,9 +355,29 @@ int dprt_march_stats(const DprtBrick* b, const DprtCamera* cam, const DprtMarchP
     return march_impl(b, cam, p, nullptr, nullptr, nullptr, nullptr, W, H, stream, out);
 }
 
+int dprt_march_push(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, const DprtPushTargets* t,
+                    uint32_t* samples, int W, int H, void* stream) {
+    if (!t) return fail(DPRT_E_USAGE, "null push targets");
+    if (t->P < 2 || t->P > DPRT_MAX_PUSH) return fail(DPRT_E_USAGE, "push needs 2..%d row blocks (got %d)", DPRT_MAX_PUSH, t->P);
+    if (!t->row_start || !t->dst || !t->flags || !t->counter) return fail(DPRT_E_USAGE, "null push target array");
+    if (t->epoch == 0) return fail(DPRT_E_USAGE, "push epoch must be nonzero (flags start at 0)");
+    if (t->row_start[0] != 0 || t->row_start[t->P] != H)
+        return fail(DPRT_E_USAGE, "row blocks must cover rows [0, %d) (got [%d, %d))", H, t->row_start[0], t->row_start[t->P]);
+    const int align = (p && (p->flags & DPRT_MARCH_HALF)) ? 8 : 16;
+    for (int i = 0; i < t->P; ++i) {
+        if (t->row_start[i + 1] < t->row_start[i]) return fail(DPRT_E_USAGE, "row block %d is negative", i);
+        if (t->row_start[i + 1] > t->row_start[i] && !t->dst[i]) return fail(DPRT_E_USAGE, "push target %d is null", i);
+        if (reinterpret_cast<uintptr_t>(t->dst[i]) % align) return fail(DPRT_E_USAGE, "push target %d not %d-byte aligned", i, align);
+        if (!t->flags[i]) return fail(DPRT_E_USAGE, "push flag %d is null", i);
+    }
+    if (p && (p->flags & DPRT_MARCH_ACCUM)) return fail(DPRT_E_USAGE, "push marches do not accumulate");
+    if (p && p->row1 > p->row0) return fail(DPRT_E_USAGE, "push marches cover whole row blocks, not a row window");
+    return march_impl(b, cam, p, reinterpret_cast<float*>(t->dst[0]), nullptr, nullptr, samples, W, H, stream, nullptr, t);
+}
+
 static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarchParams* p, float* partial_rgba,
                       const float* bg, uint8_t* rgb8, uint32_t* samples, int W, int H, void* stream,
-                      uint64_t* stats) {
+                      uint64_t* stats, const DprtPushTargets* push) {
     if (!b || !cam || !p) return fail(DPRT_E_USAGE, "null march argument");
     if (W <= 0 || H <= 0) return fail(DPRT_E_USAGE, "frame size %dx%d must be positive", W, H);
     if (p->n_tf < 2 || p->n_tf > dprt::kMaxTf || !p->tf_rgba)
@@ -418,7 +448,17 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.pix0 = window ? (long long)p->row0 * W : 0;
     a.npix_buf = window ? (long long)(p->row1 - p->row0) * W : (long long)W * H;
     a.beam = (p->flags & DPRT_MARCH_BEAM) ? 1 : ((p->flags & DPRT_MARCH_QUEUE) ? 0 : DPRT_BEAM_DEFAULT);
-    if (rgb8 || a.accum || window || a.half_out || stats) a.beam = 1;  // these exist in the beam marcher only
+    if (rgb8 || a.accum || window || a.half_out || stats || push) a.beam = 1;  // these exist in the beam marcher only
+    if (push) {
+        a.push_P = push->P;
+        for (int i = 0; i <= push->P; ++i) a.push_row[i] = push->row_start[i];
+        for (int i = 0; i < push->P; ++i) {
+            a.push_dst[i] = static_cast<char*>(push->dst[i]);
+            a.push_flag[i] = push->flags[i];
+        }
+        a.push_ctr = push->counter;
+        a.push_epoch = push->epoch;
+    }
     if (!a.beam && a.wide) return fail(DPRT_E_USAGE, "the queue marcher takes bricks of < 2^31 quads; use the beam marcher");
     if (!a.beam && a.half_quads) return fail(DPRT_E_USAGE, "fp16 quads need the beam marcher");
     a.tf = reinterpret_cast<const float4*>(p->tf_rgba);
@@ -532,6 +572,10 @@ int dprt_composite_ranged(int device, const float* const* inputs, const int64_t*
     a.flags = flags;
     a.rgb8 = rgb8;
     a.rgba = reinterpret_cast<float4*>(rgba_out);
+    a.n_sig = g_sig.n;  // dprt_composite_signal (this thread's pending signal), else 0
+    a.sig_epoch = g_sig.epoch;
+    a.sig_ctr = g_sig.counter;
+    for (int i = 0; i < g_sig.n; ++i) a.sig[i] = g_sig.flags[i];
     CK(dprt::launch_composite(a, (cudaStream_t)stream), "composite kernel launch");
     return DPRT_OK;
 }
@@ -539,6 +583,30 @@ int dprt_composite_ranged(int device, const float* const* inputs, const int64_t*
 int dprt_composite(int device, const float* const* inputs, int P, int64_t npix, const float bg[3], int flags,
                    uint8_t* rgb8, float* rgba_out, void* stream) {
     return dprt_composite_ranged(device, inputs, nullptr, P, npix, bg, flags, rgb8, rgba_out, stream);
+}
+
+int dprt_composite_signal(int device, const float* const* inputs, const int64_t* ranges, int P, int64_t npix,
+                          const float bg[3], int flags, uint8_t* rgb8, float* rgba_out, uint32_t* counter,
+                          uint32_t* const* signal, int n_signal, uint32_t epoch, void* stream) {
+    if (n_signal < 1 || n_signal > DPRT_MAX_PUSH || !signal || !counter)
+        return fail(DPRT_E_USAGE, "need 1..%d signal flags and a counter", DPRT_MAX_PUSH);
+    for (int i = 0; i < n_signal; ++i)
+        if (!signal[i]) return fail(DPRT_E_USAGE, "signal flag %d is null", i);
+    g_sig.n = n_signal;
+    g_sig.epoch = epoch;
+    g_sig.counter = counter;
+    for (int i = 0; i < n_signal; ++i) g_sig.flags[i] = signal[i];
+    const int rc = dprt_composite_ranged(device, inputs, ranges, P, npix, bg, flags, rgb8, rgba_out, stream);
+    g_sig.n = 0;
+    return rc;
+}
+
+int dprt_wait_flags(int device, const uint32_t* flags, int n, uint32_t epoch, void* stream) {
+    if (n < 1 || !flags) return fail(DPRT_E_USAGE, "need at least one flag to wait on");
+    int rc = bind(device);
+    if (rc) return rc;
+    CK(dprt::launch_wait_flags(flags, n, epoch, (cudaStream_t)stream), "wait-flags kernel launch");
+    return DPRT_OK;
 }
 
 int dprt_march_counters(int device, uint64_t out[4], int reset) {

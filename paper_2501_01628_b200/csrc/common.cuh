@@ -104,6 +104,15 @@ struct MarchArgs {
     uint32_t* __restrict__ samples;
     float4* rays;   // compacted ray queue: 2 float4 per ray {p0, pixel}, {step, n}
     int* counters;  // [0] rays queued by ray_setup, [1] rays taken by march
+    // fused march + exchange (dprt_march_push): row block b of the partial goes to push_dst[b] (its owner's
+    // inbox, a peer pointer), pixel (x, y) at element (y - push_row[b]) * W + x; the launch's last CTA then
+    // release-stores push_epoch into every push_flag[b]
+    int push_P;                          // 0: the partial is out / out16 (local)
+    int push_row[DPRT_MAX_PUSH + 1];
+    char* push_dst[DPRT_MAX_PUSH];
+    unsigned* push_flag[DPRT_MAX_PUSH];
+    unsigned* push_ctr;
+    unsigned push_epoch;
     uint8_t* mark;                    // dprt_march_stats: per-macrocell "a real sample was shaded here" bytes
     unsigned long long* stats;        // dprt_march_stats: {shaded samples, contributing samples}
     int W, H;
@@ -120,6 +129,36 @@ struct CompositeArgs {
     int flags;
     uint8_t* rgb8;
     float4* rgba;
+    // dprt_composite_signal: the launch's last CTA release-stores sig_epoch into sig[0 .. n_sig)
+    int n_sig;
+    unsigned sig_epoch;
+    unsigned* sig_ctr;
+    unsigned* sig[DPRT_MAX_PUSH];
 };
+
+// System-scope release / acquire on a flag word (local or peer memory over NVLink).
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Last-CTA completion signal: every thread fences its own stores at system scope, the CTA counts itself
+// in `ctr` (atomicInc wraps it back to 0 for the next launch), and the CTA that completes the count
+// release-stores `epoch` into flags[0 .. n).  Every thread of every CTA must reach this call.
+__device__ __forceinline__ void grid_signal(unsigned* ctr, unsigned* const* flags, int n, unsigned epoch) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+        if (atomicInc(ctr, total - 1) == total - 1) {
+            __threadfence_system();
+            for (int i = 0; i < n; ++i) st_release_sys(flags[i], epoch);
+        }
+    }
+}
 
 }  // namespace dprt

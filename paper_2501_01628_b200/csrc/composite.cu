@@ -69,7 +69,7 @@ __device__ __forceinline__ void load4(const float4* frag, long long i, float4 f[
 // the 12 RGB8 bytes leave as three aligned 32-bit stores.  A fragment covers only the tile pixels
 // [lo, hi) (a rank's footprint rows): outside them it is clear and is not read at all.
 template <bool kHalf>
-__global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
+__device__ __forceinline__ void composite4_body(const CompositeArgs& a) {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long i0 = q * 4;
     if (i0 >= a.npix) return;
@@ -128,10 +128,16 @@ __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
     }
 }
 
+template <bool kHalf>
+__global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
+    composite4_body<kHalf>(a);
+    if (a.n_sig) grid_signal(a.sig_ctr, a.sig, a.n_sig, a.sig_epoch);  // e.g. rows written into rank 0's frame
+}
+
 // Small tiles (a rank's row block after the exchange): one pixel per thread, so the grid still fills the
 // 148 SMs, with up to 8 fragments' loads issued before the first is blended.
 template <bool kHalf>
-__global__ void __launch_bounds__(256) composite_px_kernel(const CompositeArgs a) {
+__device__ __forceinline__ void composite_px_body(const CompositeArgs& a) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.npix) return;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -152,13 +158,43 @@ __global__ void __launch_bounds__(256) composite_px_kernel(const CompositeArgs a
         for (int ch = 0; ch < 3; ++ch) a.rgb8[3 * i + ch] = (uint8_t)pack_rgb8(acc, a.bg, ch);
 }
 
+template <bool kHalf>
+__global__ void __launch_bounds__(256) composite_px_kernel(const CompositeArgs a) {
+    composite_px_body<kHalf>(a);
+    if (a.n_sig) grid_signal(a.sig_ctr, a.sig, a.n_sig, a.sig_epoch);
+}
+
+// Stream-ordered wait for peers' epoch flags (dprt_wait_flags): one warp spins with system-scope acquire
+// loads; a wait that outlives ~2^35 cycles (~17 s) traps instead of hanging the stream forever.
+__global__ void wait_flags_kernel(const unsigned* __restrict__ flags, int n, unsigned epoch) {
+    const long long t0 = clock64();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        while ((int)(ld_acquire_sys(flags + i) - epoch) < 0) {
+            __nanosleep(128);
+            if (clock64() - t0 > (1LL << 35)) __trap();
+        }
+    }
+}
+
+cudaError_t launch_wait_flags(const unsigned* flags, int n, unsigned epoch, cudaStream_t stream) {
+    wait_flags_kernel<<<1, 32, 0, stream>>>(flags, n, epoch);
+    return cudaGetLastError();
+}
+
 #ifndef DPRT_COMPOSITE_PX_BELOW
 #define DPRT_COMPOSITE_PX_BELOW (1 << 22)  // tiles below this many pixels blending >= 3 fragments use one
 #endif                                     // pixel per thread (graph-timed sweep, profiles/r01_composite_sweep.md)
 
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream) {
     const int block = 256;
-    if (a.npix == 0) return cudaSuccess;
+    if (a.npix == 0) {
+        if (a.n_sig) {  // nothing to blend: still signal (one CTA, no stores to fence but its own)
+            CompositeArgs e = a;
+            composite_px_kernel<false><<<1, 32, 0, stream>>>(e);
+            return cudaGetLastError();
+        }
+        return cudaSuccess;
+    }
     if (a.npix < DPRT_COMPOSITE_PX_BELOW && a.P >= 3) {
         const long long grid = (a.npix + block - 1) / block;
         if (a.flags & DPRT_COMPOSITE_HALF_IN)

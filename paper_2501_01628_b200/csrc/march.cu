@@ -398,10 +398,39 @@ __device__ __forceinline__ int center_out(int k, int n) {
 
 __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int_rd(fmaxf(u, 0.f)), hi); }
 
+// A pixel of the RGBA partial: the local buffer (out / out16 at pix - pix0) or, in the fused march +
+// exchange (kPush, dprt_march_push), its row block's owner's inbox over NVLink.
+template <bool kPush>
+__device__ __forceinline__ void store_partial(const MarchArgs& a, long long pix, int y, float C0, float C1, float C2,
+                                              float A) {
+    if constexpr (kPush) {
+        int b = 0;
+        while (b + 1 < a.push_P && y >= a.push_row[b + 1]) ++b;
+        const long long e = pix - (long long)a.push_row[b] * a.W;
+        if (a.half_out) {
+            const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
+            reinterpret_cast<uint2*>(a.push_dst[b])[e] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
+                                                                    *reinterpret_cast<const unsigned*>(&ba));
+        } else {
+            reinterpret_cast<float4*>(a.push_dst[b])[e] = make_float4(C0, C1, C2, A);
+        }
+    } else {
+        (void)y;
+        if (a.half_out) {
+            const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
+            a.out16[pix - a.pix0] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
+                                               *reinterpret_cast<const unsigned*>(&ba));
+        } else {
+            a.out[pix - a.pix0] = make_float4(C0, C1, C2, A);
+        }
+    }
+}
+
 // The pixels no beam covers -- rows [y0, y1) outside the footprint rectangle -- get their "nothing here"
 // value inside the march kernel itself (no separate fill or memset pass): the tone-mapped background for
 // the fused RGB8 frame, a clear fragment (0) for an RGBA partial.  Blocks take whole rows, threads 4-pixel
 // groups; a group straddling the rectangle's edge writes only its outside pixels (the beams own the inside).
+template <bool kPush>
 __device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1, int unit, int nunits, int t, int nt) {
     const uint32_t cr = (uint32_t)floorf(fminf(fmaxf(a.bg[0], 0.f), 1.f) * 255.f + 0.5f);
     const uint32_t cg = (uint32_t)floorf(fminf(fmaxf(a.bg[1], 0.f), 1.f) * 255.f + 0.5f);
@@ -436,10 +465,7 @@ __device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1, int unit, 
                 for (int k = 0; k < 4; ++k) {
                     const int x = x0 + k;
                     if (x >= W || (!row_out && x >= a.rect[0] && x < a.rect[2])) continue;
-                    if (a.half_out)
-                        a.out16[i0 + k - a.pix0] = make_uint2(0u, 0u);
-                    else
-                        a.out[i0 + k - a.pix0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    store_partial<kPush>(a, i0 + k, y, 0.f, 0.f, 0.f, 0.f);
                 }
             }
         }
@@ -447,15 +473,14 @@ __device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1, int unit, 
 }
 
 // A pixel inside the footprint whose ray adds nothing (no owned sample, or a beam that misses the brick).
-__device__ __forceinline__ void write_clear(const MarchArgs& a, int pix) {
+template <bool kPush>
+__device__ __forceinline__ void write_clear(const MarchArgs& a, int pix, int py) {
     if (a.rgb8) {
         uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
 #pragma unroll
         for (int c = 0; c < 3; ++c) dst[c] = (uint8_t)floorf(fminf(fmaxf(a.bg[c], 0.f), 1.f) * 255.f + 0.5f);
-    } else if (a.half_out) {
-        a.out16[pix - a.pix0] = make_uint2(0u, 0u);
     } else {
-        a.out[pix - a.pix0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        store_partial<kPush>(a, pix, py, 0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -486,7 +511,9 @@ constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are indep
 // kMark (diagnostic instantiation, dprt_march_stats): no image output; every real sample of a live ray sets
 // its macrocell's byte in a.mark and the launch counts shaded / contributing samples into a.stats -- the
 // macrocells the march must read (the roofline's needed bytes) and the shaded-sample rate.
-template <bool kWide, int kUnroll, int kMinBlocks, bool kHalf, bool kMark = false>
+// kPush: the fused march + exchange (dprt_march_push) -- partial pixels go to their row block owners' inboxes
+// and the launch's last CTA raises the owners' epoch flags.
+template <bool kWide, int kUnroll, int kMinBlocks, bool kHalf, bool kMark = false, bool kPush = false>
 __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
@@ -569,7 +596,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         }
         const unsigned hitm = __ballot_sync(FULL, nn > 0);
         if (!hitm) {
-            if (!kMark && inside && !a.accum) write_clear(a, pix);  // no ray of this beam meets the brick
+            if (!kMark && inside && !a.accum) write_clear<kPush>(a, pix, py);  // no ray of this beam meets the brick
             continue;
         }
 #if DPRT_COUNTERS
@@ -835,12 +862,8 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 dst[0] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[0], C0), 0.f), 1.f) * 255.f + 0.5f);
                 dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
                 dst[2] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[2], C2), 0.f), 1.f) * 255.f + 0.5f);
-            } else if (a.half_out) {
-                const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
-                a.out16[pix - a.pix0] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
-                                                   *reinterpret_cast<const unsigned*>(&ba));
             } else {
-                a.out[pix - a.pix0] = make_float4(C0, C1, C2, A);
+                store_partial<kPush>(a, pix, py, C0, C1, C2, A);
             }
         }
     }
@@ -855,8 +878,9 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         const int y0 = a.band_clear ? a.rect[1] : (int)(a.pix0 / a.W);
         const int y1 = a.band_clear ? a.rect[3] : (int)((a.pix0 + a.npix_buf) / a.W);
         const int wpb = blockDim.x >> 5;
-        fill_outside_rect(a, y0, y1, (int)blockIdx.x * wpb + (tid >> 5), (int)gridDim.x * wpb, lane, 32);
+        fill_outside_rect<kPush>(a, y0, y1, (int)blockIdx.x * wpb + (tid >> 5), (int)gridDim.x * wpb, lane, 32);
     }
+    if constexpr (kPush) grid_signal(a.push_ctr, a.push_flag, a.push_P, a.push_epoch);  // fragments landed at owners
 #if DPRT_COUNTERS
     DPRT_COUNT(0, c_shade);
     DPRT_COUNT(1, c_contrib);
@@ -1003,7 +1027,17 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
               march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true>},
              {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, true>,
               march_beam_kernel<true, kDeepUnroll, kDeepBlocks, true>}}};
-        const K kern = kerns[a.half_quads ? 1 : 0][a.deep ? 1 : 0][a.wide ? 1 : 0];
+        const K pushk[2][2][2] = {  // [half][deep][wide], dprt_march_push
+            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false, false, true>,
+              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false, false, true>},
+             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, false, false, true>,
+              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, false, false, true>}},
+            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true, false, true>,
+              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true, false, true>},
+             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, true, false, true>,
+              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, true, false, true>}}};
+        const int hq = a.half_quads ? 1 : 0, dp = a.deep ? 1 : 0, wd = a.wide ? 1 : 0;
+        const K kern = a.push_P ? pushk[hq][dp][wd] : kerns[hq][dp][wd];
         kern<<<grid_for((const void*)kern, kBeamBlock, smem), kBeamBlock, smem, stream>>>(a);
         return cudaGetLastError();
     }

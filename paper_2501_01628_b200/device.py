@@ -346,6 +346,46 @@ def march(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: flo
     _lib.check(rc, "dprt_march")
 
 
+def march_push(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, width: int, height: int,
+               row_start: Sequence[int], dst: Sequence[int], flag_ptrs: Sequence[int], counter_ptr: int, epoch: int,
+               samples: Optional[torch.Tensor] = None, skip: bool = True, band_clear: bool = False,
+               half: bool = False) -> None:
+    """dprt_march_push: the fused march + exchange (DESIGN.md §6 "p2p_push").  Row block b of this brick's
+    RGBA partial is written straight into ``dst[b]`` (block b's owner's inbox slot for this rank; a peer
+    pointer), pixel (x, y) at element (y - row_start[b]) * W + x, and once every CTA's stores are fenced
+    ``epoch`` is release-stored into every ``flag_ptrs[b]``.  ``counter_ptr``: a zeroed device word."""
+    P = len(dst)
+    if len(row_start) != P + 1 or len(flag_ptrs) != P:
+        raise UsageError("push targets need P destinations, P flags and P + 1 row boundaries")
+    sp = ctypes.c_void_p(0)
+    if samples is not None:
+        _require_cuda(samples, "samples", torch.int32)
+        if samples.numel() != width * height:
+            raise UsageError("samples buffer must hold one count per pixel")
+        sp = ctypes.c_void_p(samples.data_ptr())
+    flags = (0 if skip else _lib.MARCH_NO_SKIP) | (_lib.MARCH_BAND_CLEAR if band_clear else 0) | \
+        (_lib.MARCH_HALF if half else 0)
+    p = tf.params(dt, ert, flags)
+    rows = (ctypes.c_int32 * (P + 1))(*[int(r) for r in row_start])
+    dsts = (ctypes.c_void_p * P)(*[int(d) for d in dst])
+    fls = (ctypes.c_void_p * P)(*[int(f) for f in flag_ptrs])
+    t = _lib.PushTargets(P, 0, ctypes.cast(rows, ctypes.c_void_p), ctypes.cast(dsts, ctypes.c_void_p),
+                         ctypes.cast(fls, ctypes.c_void_p), ctypes.c_void_p(counter_ptr), int(epoch) & 0xFFFFFFFF, 0)
+    brick.join_lanes()
+    c = camera_struct(cam)
+    rc = _lib.lib().dprt_march_push(brick.handle, ctypes.byref(c), ctypes.byref(p), ctypes.byref(t), sp, width, height,
+                                    _stream(brick.device))
+    _lib.check(rc, "dprt_march_push")
+
+
+def wait_flags(device_index: int, flags_ptr: int, n: int, epoch: int, stream: Optional[int] = None) -> None:
+    """dprt_wait_flags: later work on the stream runs once the n device words at ``flags_ptr`` reach ``epoch``
+    (written by other GPUs, or by work already complete -- never by work that itself waits on this stream)."""
+    s = ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream(device_index).cuda_stream)
+    _lib.check(_lib.lib().dprt_wait_flags(device_index, ctypes.c_void_p(flags_ptr), n, int(epoch) & 0xFFFFFFFF, s),
+               "dprt_wait_flags")
+
+
 def march_stats(brick: DeviceBrick, cam: CameraSpec, tf: DeviceTF, dt: float, ert: float, width: int, height: int,
                 skip: bool = True) -> dict:
     """dprt_march_stats (synchronous diagnostic): what the production march reads and shades for this view --
@@ -488,6 +528,26 @@ def composite_ptrs(device_index: int, ptrs: Sequence[int], npix: int, background
     rc = _lib.lib().dprt_composite_ranged(device_index, arr, rng, len(ptrs), npix, bg_arr, flags,
                                           ctypes.c_void_p(rgb8_ptr), ctypes.c_void_p(rgba_ptr), s)
     _lib.check(rc, "dprt_composite")
+
+
+def composite_signal(device_index: int, ptrs: Sequence[int], npix: int, background, rgb8_ptr: int, rgba_ptr: int,
+                     ranges: Optional[Sequence[Tuple[int, int]]], counter_ptr: int, signal_ptrs: Sequence[int],
+                     epoch: int, half: bool = False, stream: Optional[int] = None) -> None:
+    """dprt_composite_signal: composite_ptrs whose last CTA, after every CTA fenced its stores (RGB8 rows in
+    rank 0's frame over NVLink), release-stores ``epoch`` into every ``signal_ptrs`` word."""
+    flags = (_lib.COMPOSITE_TONEMAP if rgb8_ptr else 0) | (_lib.COMPOSITE_RGBA if rgba_ptr else 0)
+    if half:
+        flags |= _lib.COMPOSITE_HALF_IN
+    bg_arr = (ctypes.c_float * 3)(*[float(c) for c in background]) if background is not None else None
+    arr = (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+    rng = None if ranges is None else (ctypes.c_int64 * (2 * len(ranges)))(*[int(v) for r in ranges for v in r])
+    sig = (ctypes.c_void_p * len(signal_ptrs))(*signal_ptrs)
+    s = ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream(device_index).cuda_stream)
+    rc = _lib.lib().dprt_composite_signal(device_index, arr, rng, len(ptrs), npix, bg_arr, flags,
+                                          ctypes.c_void_p(rgb8_ptr), ctypes.c_void_p(rgba_ptr),
+                                          ctypes.c_void_p(counter_ptr), sig, len(signal_ptrs),
+                                          int(epoch) & 0xFFFFFFFF, s)
+    _lib.check(rc, "dprt_composite_signal")
 
 
 def enable_peer(device_index: int, peer_index: int) -> None:

@@ -27,7 +27,7 @@ from .geom import CameraSpec, Vec3
 from .transport import RankEndpoint
 from .volume import Decomposition, TransferFunction1D, visibility_order
 
-COMPOSITE_MODES = ("auto", "direct_send", "binary_swap", "p2p", "cycle")
+COMPOSITE_MODES = ("auto", "direct_send", "binary_swap", "p2p", "p2p_push", "cycle")
 FRAGMENT_DTYPES = {"f32": torch.float32, "f16": torch.float16}
 FUSED_SLOTS = 3  # device RGB8 frames the fused single-rank path rotates through (read-back pipeline depth)
 
@@ -56,7 +56,7 @@ class RenderOptions:
 
     dt: float = 1.0                    # lattice spacing along the ray, world units
     ert: float = 0.99                  # early ray termination threshold (per brick)
-    composite: str = "auto"            # auto | direct_send | binary_swap | p2p | cycle (ray cycling, §2.10)
+    composite: str = "auto"            # auto | direct_send | binary_swap | p2p | p2p_push | cycle (§2.10)
     skip_empty: bool = True            # exact empty-space skipping
     disable_compositing: bool = False  # debug: root shows only its own brick (negative test, engine.py:172)
     frame_index: int = 0
@@ -337,9 +337,22 @@ class VolumeRenderer:
         if options.clip_exchange and self.ep.R > 1 and not options.disable_compositing and \
                 self.compositor.clips_bands():
             bands = self._bands(cam, width, height)
-        dev.march(self.brick, cam, dtf, options.dt, options.ert, self.partial, width, height,
-                  samples=self.samples if options.collect_samples else None, skip=options.skip_empty,
-                  band_clear=bands is not None)
+        push = None if options.disable_compositing or self.ep.R == 1 else self.compositor.push_targets()
+        if push is not None:
+            # fused march + exchange: peers write this frame into rank 0's frame buffer once every rank's
+            # march is done, so the previous frame's read-back must drain before this march
+            if self._pending_copy is not None:
+                torch.cuda.current_stream(self.device).wait_event(self._pending_copy)
+                self._pending_copy = None
+            row_start, dst, flag_ptrs, counter, epoch = push
+            dev.march_push(self.brick, cam, dtf, options.dt, options.ert, width, height, row_start, dst, flag_ptrs,
+                           counter, epoch, samples=self.samples if options.collect_samples else None,
+                           skip=options.skip_empty, band_clear=bands is not None,
+                           half=self.compositor.fdt == torch.float16)
+        else:
+            dev.march(self.brick, cam, dtf, options.dt, options.ert, self.partial, width, height,
+                      samples=self.samples if options.collect_samples else None, skip=options.skip_empty,
+                      band_clear=bands is not None)
         if ev is not None:
             ev[1].record(torch.cuda.current_stream(self.device))
         if options.disable_compositing:
@@ -357,7 +370,7 @@ class VolumeRenderer:
         stats.bytes_exchanged += nbytes
         stats.record(options.frame_index, width * height, nbytes, (time.perf_counter() - t0) * 1e3)
         res = RenderResult(rgb8=out.rgb8, stats=stats, order=order,
-                           partial=self.partial.view(height, width, 4))
+                           partial=None if push is not None else self.partial.view(height, width, 4))
         if options.keep_float and out.rgba is not None:
             rgba = out.rgba.view(height, width, 4).double().cpu().numpy()
             bg = np.asarray(self.background, np.float64)

@@ -111,3 +111,178 @@ class P2PCompositor:
         for buf in (self.partial, self.frame, self.frame_rgba):
             if buf is not None:
                 buf.close()
+
+
+# ------------------------------------------------------------------------------------------------------
+# Fused march + exchange ("p2p_push"): the march itself writes each row block of the partial
+# into the block owner's inbox over NVLink while it runs, so the fragment exchange overlaps the march tile
+# by tile; per-source epoch flags in the owner's memory replace the stream-ordered NCCL barriers.
+
+FLAG_WORDS = 2  # per rank beyond the 2P epoch words: [0, P) fragment arrivals, [P, 2P) frame rows done
+                # (read on rank 0), 2P march CTA counter, 2P + 1 composite CTA counter
+
+
+class PushLayout:
+    """Pointer arithmetic of the fused march + exchange -- pure, shared by the compositor and the
+    single-GPU emulation test.  Rank j's inbox holds, per frame parity (epoch & 1) and source rank s, a
+    slot of ``slot`` pixels: s's fragment of j's row block (``assign_pixels``, engine.py:216-221), pixel
+    (x, y) at element (y - block_start) * W + x.  Double buffering by parity is what makes the flags
+    sufficient: source s's march of frame k follows its own blend of frame k-1 on its stream, and that blend
+    waited for every source's march of frame k-1, which followed every rank's blend of frame k-2 -- the
+    last reader of this parity's slots."""
+
+    def __init__(self, P: int, width: int, height: int, px_bytes: int):
+        self.P, self.W, self.H, self.es = P, width, height, px_bytes
+        self.blocks = assign_rows(height, P)
+        self.row_start = [b[0] for b in self.blocks] + [height]
+        self.slot = max(b1 - b0 for b0, b1 in self.blocks) * width  # pixels per (parity, source) slot
+
+    def inbox_pixels(self) -> int:
+        return 2 * self.P * self.slot
+
+    def flag_words(self) -> int:
+        return 2 * self.P + FLAG_WORDS
+
+    def slot_ptr(self, inbox_base: int, epoch: int, src: int) -> int:
+        return inbox_base + self.es * (((epoch & 1) * self.P + src) * self.slot)
+
+    def march_targets(self, peer_inbox: Sequence[int], peer_flags: Sequence[int], rank: int, epoch: int):
+        """(dst, flags) for source ``rank``'s march of frame ``epoch``: its slot at every block owner."""
+        dst = [self.slot_ptr(peer_inbox[j], epoch, rank) for j in range(self.P)]
+        return dst, [peer_flags[j] + 4 * rank for j in range(self.P)]
+
+    def fragments(self, inbox_base: int, rank: int, epoch: int, order: Sequence[int], bands=None):
+        """Blend inputs of ``rank``'s block in visibility order: (pointers, pixel ranges or None, pixels
+        received from other ranks).  With ``bands`` a source's fragment covers only its footprint rows."""
+        rows = self.blocks[rank]
+        ptrs, ranges, recv = [], [], 0
+        for s in order:
+            base = self.slot_ptr(inbox_base, epoch, s)
+            if bands is None:
+                ptrs.append(base)
+                ranges.append((0, (rows[1] - rows[0]) * self.W))
+                recv += 0 if s == rank else (rows[1] - rows[0]) * self.W
+                continue
+            c = clip_rows(rows, bands[s])
+            if c:
+                ptrs.append(base + self.es * (c[0] - rows[0]) * self.W)
+                ranges.append(((c[0] - rows[0]) * self.W, (c[1] - rows[0]) * self.W))
+                recv += 0 if s == rank else (c[1] - c[0]) * self.W
+        if not ptrs:  # no footprint meets this block: the background alone
+            ptrs, ranges = [self.slot_ptr(inbox_base, epoch, rank)], [(0, 0)]
+        return ptrs, (None if bands is None else ranges), recv
+
+
+def _device_identity(index: int) -> str:
+    import socket
+
+    props = torch.cuda.get_device_properties(index)
+    return f"{socket.gethostname()}:{getattr(props, 'uuid', index)}"
+
+
+class P2PPushCompositor:
+    """Fused march + exchange over peer memory (one process, or one thread, per GPU).
+
+    Per frame (epoch e = 1, 2, ...): ``march_targets()`` -> the engine's ``dprt_march_push`` writes this
+    rank's partial straight into every block owner's inbox slot and raises its epoch flag there when its
+    last CTA retires; ``composite()`` waits (one spinning warp, stream-ordered) until all P sources' flags
+    of this rank's block reach e, blends them from local memory into rank 0's frame over NVLink and raises
+    rank 0's done flag for this block; rank 0 then waits for every block's done flag, so its frame is
+    complete in stream order -- no NCCL call per frame.  Needs every rank on its own GPU (a spinning wait
+    must never share a GPU with the work it waits for): ``try_create`` checks that collectively."""
+
+    def __init__(self, ep: RankEndpoint, width: int, height: int, device: torch.device,
+                 fragment_dtype: torch.dtype = torch.float32):
+        self.ep = ep
+        self.fdt = fragment_dtype
+        self.px = 8 if fragment_dtype == torch.float16 else 16
+        self.W, self.H = width, height
+        self.device = device
+        self.index = device.index if device.index is not None else torch.cuda.current_device()
+        self.layout = PushLayout(ep.R, width, height, self.px)
+        self.ok = ep.R <= dev._lib.MAX_PUSH
+        self.inbox = self.flags = self.frame = self.frame_rgba = None
+        self.epoch = 0
+        try:
+            if self.ok:
+                self.inbox = dev.DeviceBuffer(device, self.layout.inbox_pixels() * 4, fragment_dtype)
+                self.flags = dev.DeviceBuffer(device, self.layout.flag_words(), torch.int32)
+                self.flags.tensor.zero_()
+                if ep.rank == 0:
+                    self.frame = dev.DeviceBuffer(device, width * height * 3, torch.uint8)
+                torch.cuda.synchronize(device)
+        except Exception:  # noqa: BLE001 - reported through self.ok
+            self.ok = False
+        ids = ep.all_gather_bytes(_device_identity(self.index).encode() if device.type == "cuda" else b"cpu")
+        self.distinct = len(set(ids)) == len(ids)
+        self.peer_inbox = ep.share_pointers(self.index, self.inbox.ptr if self.inbox else 0)
+        self.peer_flags = ep.share_pointers(self.index, self.flags.ptr if self.flags else 0)
+        self.root_frame = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)[0]
+        self.ok = self.ok and self.distinct and all(self.peer_inbox) and all(self.peer_flags) and self.root_frame != 0
+        self.root_rgba = 0
+        self.last_bytes = 0
+
+    @classmethod
+    def try_create(cls, ep: RankEndpoint, width: int, height: int, device: torch.device,
+                   fragment_dtype: torch.dtype = torch.float32) -> Optional["P2PPushCompositor"]:
+        """Collective: every rank gets the compositor, or every rank gets None (peers not mappable, ranks
+        sharing a GPU, more than DPRT_MAX_PUSH ranks)."""
+        impl = cls(ep, width, height, device, fragment_dtype)
+        flags = ep.all_gather_bytes(b"1" if impl.ok else b"0")
+        if all(f == b"1" for f in flags):
+            return impl
+        impl.close()
+        return None
+
+    def _ensure_rgba(self) -> None:
+        if self.root_rgba:
+            return
+        if self.ep.rank == 0:
+            self.frame_rgba = dev.DeviceBuffer(self.device, self.W * self.H * 4)
+        self.root_rgba = self.ep.share_pointers(self.index, self.frame_rgba.ptr if self.frame_rgba else 0)[0]
+
+    def march_targets(self):
+        """Start a frame: (row_start, dst pointers, flag pointers, counter pointer, epoch) for dprt_march_push."""
+        self.epoch += 1
+        dst, fl = self.layout.march_targets(self.peer_inbox, self.peer_flags, self.ep.rank, self.epoch)
+        counter = self.flags.ptr + 4 * (2 * self.ep.R)
+        return self.layout.row_start, dst, fl, counter, self.epoch
+
+    def composite(self, order: Sequence[int], background, keep_float: bool = False, bands=None) -> CompositeOutput:
+        ep, L, e = self.ep, self.layout, self.epoch
+        if keep_float:
+            self._ensure_rgba()
+        r = ep.rank
+        dev.wait_flags(self.index, self.flags.ptr, ep.R, e)  # every source's fragment of my block has landed
+        rows = L.blocks[r]
+        npix = (rows[1] - rows[0]) * self.W
+        ptrs, ranges, recv = L.fragments(self.inbox.ptr, r, e, order, bands)
+        off = rows[0] * self.W
+        dev.composite_signal(self.index, ptrs, npix, background, self.root_frame + 3 * off,
+                             (self.root_rgba + 16 * off) if keep_float else 0, ranges,
+                             self.flags.ptr + 4 * (2 * ep.R + 1), [self.peer_flags[0] + 4 * (ep.R + r)], e,
+                             half=self.fdt == torch.float16)
+        # bytes this rank moved over NVLink this frame: its pushed fragments (those of the other blocks) and
+        # its RGB8 rows into rank 0's frame
+        sent = 0
+        for j in range(ep.R):
+            if j == r:
+                continue
+            bj = L.blocks[j]
+            c = bj if bands is None else clip_rows(bj, bands[r])
+            if c:
+                sent += (c[1] - c[0]) * self.W
+        self.last_bytes = self.px * sent + (3 * npix if r else 0)
+        if r != 0:
+            return CompositeOutput(None, None)
+        dev.wait_flags(self.index, self.flags.ptr + 4 * ep.R, ep.R, e)  # every block's rows are in my frame
+        frame = self.frame.tensor.view(self.H, self.W, 3)
+        return CompositeOutput(frame, self.frame_rgba.tensor if keep_float else None)
+
+    def close(self) -> None:
+        for ptrs in (getattr(self, "peer_inbox", None), getattr(self, "peer_flags", None)):
+            if ptrs:
+                self.ep.unshare_pointers(self.index, ptrs)
+        for buf in (self.inbox, self.flags, self.frame, self.frame_rgba):
+            if buf is not None:
+                buf.close()

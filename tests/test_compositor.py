@@ -13,7 +13,8 @@ import torch
 
 import oracle
 from dist_util import run_ranks
-from paper_2501_01628_b200.compositor import (Compositor, assign_rows, binary_swap_plan, direct_send_plan)
+from paper_2501_01628_b200.compositor import (Compositor, assign_rows, binary_swap_plan, clip_rows,
+                                              direct_send_plan)
 from paper_2501_01628_b200.volume import binary_swap_compatible, blob_field, decompose
 
 
@@ -189,3 +190,41 @@ def test_kd_orders_are_binary_swap_compatible():
         for _ in range(20):
             eye = tuple(rng.uniform(-100, 200, 3))
             assert binary_swap_compatible(dec.visibility_order(eye))
+
+
+@pytest.mark.parametrize("P,W,H", [(2, 64, 48), (3, 157, 113), (8, 3840, 2160), (5, 33, 7)])
+def test_push_layout_slots_are_disjoint_and_consistent(P, W, H):
+    """p2p_push pointer arithmetic (p2p.PushLayout): per (parity, source) slots tile the inbox without
+    overlap; the slot a source pushes into at owner j is the one owner j blends for that source; the
+    band-clipped ranges are the pull compositor's (clip of the owner's block by the source's band)."""
+    from paper_2501_01628_b200.p2p import PushLayout
+
+    L = PushLayout(P, W, H, 16)
+    assert L.row_start[0] == 0 and L.row_start[-1] == H and len(L.row_start) == P + 1
+    spans = sorted((L.slot_ptr(0, e, s), L.slot_ptr(0, e, s) + 16 * L.slot) for e in (1, 2) for s in range(P))
+    for (a0, a1), (b0, _) in zip(spans, spans[1:]):
+        assert a1 <= b0
+    assert spans[-1][1] <= 16 * L.inbox_pixels()
+    bases = [1 << 40 | (j << 32) for j in range(P)]
+    flags = [1 << 44 | (j << 32) for j in range(P)]
+    rng = np.random.default_rng(P)
+    for epoch in (1, 2, 3):
+        order = list(rng.permutation(P))
+        bands = [tuple(sorted(rng.integers(0, H + 1, 2))) for _ in range(P)]
+        for src in range(P):
+            dst, fl = L.march_targets(bases, flags, src, epoch)
+            assert fl == [flags[j] + 4 * src for j in range(P)]
+            for j in range(P):
+                assert dst[j] == L.slot_ptr(bases[j], epoch, src)
+        for j in range(P):
+            ptrs, ranges, recv = L.fragments(bases[j], j, epoch, order, bands)
+            rows = L.blocks[j]
+            want = [(s, clip_rows(rows, bands[s])) for s in order if clip_rows(rows, bands[s])]
+            if not want:
+                assert ranges == [(0, 0)]
+                continue
+            assert len(ptrs) == len(want)
+            for p, (lo, hi), (s, c) in zip(ptrs, ranges, want):
+                assert p == L.slot_ptr(bases[j], epoch, s) + 16 * (c[0] - rows[0]) * W
+                assert (lo, hi) == ((c[0] - rows[0]) * W, (c[1] - rows[0]) * W)
+            assert recv == sum((c[1] - c[0]) * W for s, c in want if s != j)

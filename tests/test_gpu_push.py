@@ -1,0 +1,113 @@
+"""Fused march + exchange ("p2p_push") on ONE GPU by sequential emulation.
+
+The production path needs every rank on its own GPU: a rank's blend waits (one spinning warp) for the
+epoch flags its peers' marches raise, and such a wait must never share a GPU with the work it waits for.
+Here the R ranks' buffers all live on cuda:0 and one thread issues, on one stream, every rank's
+``dprt_march_push`` first and only then every rank's flag wait + ``dprt_composite_signal`` -- so each
+wait is already satisfied when it is issued and no kernel ever waits on a kernel that is not complete
+(the emulation B200_PROFILING.md prescribes for fewer GPUs than ranks).  The pointer arithmetic is the
+production one (``p2p.PushLayout``); every frame must be byte-identical to marching into local partials
+and compositing them with ``dprt_composite`` (same kernels, same fragment values, other destinations),
+and every epoch flag must carry the frame's epoch afterwards."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2501_01628_b200 import device as dev
+from paper_2501_01628_b200.compositor import assign_rows, clip_rows
+from paper_2501_01628_b200.geom import orbit_camera
+from paper_2501_01628_b200.p2p import PushLayout
+from scenes import c1
+
+pytestmark = pytest.mark.gpu
+
+
+def _bands(dec, cam, W, H):
+    return [tuple(dev.desc_footprint(dec.brick(s), cam, W, H)[1::2]) for s in range(dec.P)]
+
+
+@pytest.mark.parametrize("P,W,H,clip,half", [(2, 160, 122, True, False), (3, 157, 113, True, False),
+                                            (4, 176, 130, False, False), (4, 176, 130, True, True),
+                                            (8, 128, 96, True, False)])
+def test_push_frames_equal_local_march_and_composite(cuda_device, P, W, H, clip, half):
+    s = c1(P=P, W=W, H=H)
+    d = cuda_device
+    fdt = torch.float16 if half else torch.float32
+    L = PushLayout(P, W, H, 8 if half else 16)
+    bricks = [dev.DeviceBrick(s.dec.brick(r), d).generate(s.field) for r in range(P)]
+    dtf = dev.DeviceTF(s.tf, d)
+    inbox = [torch.full((L.inbox_pixels() * 4,), float("nan"), dtype=fdt, device=d) for _ in range(P)]
+    flags = [torch.zeros(L.flag_words(), dtype=torch.int32, device=d) for _ in range(P)]
+    frame = torch.zeros((H, W, 3), dtype=torch.uint8, device=d)
+    ib = [t.data_ptr() for t in inbox]
+    fb = [t.data_ptr() for t in flags]
+    bb = s.field.bounds()
+    cams = [s.cam] + [orbit_camera(bb.center(), 1.3 * bb.diagonal(), math.radians(35.0 * k), math.radians(15.0),
+                                   45.0, W / H) for k in range(1, 4)]
+    for epoch, cam in enumerate(cams, start=1):
+        order = s.dec.visibility_order(cam.position)
+        bands = _bands(s.dec, cam, W, H) if clip else None
+        # every rank's march first (pushing into every owner's inbox slot, raising its flags) ...
+        for r in range(P):
+            dst, fl = L.march_targets(ib, fb, r, epoch)
+            dev.march_push(bricks[r], cam, dtf, s.dt, s.ert, W, H, L.row_start, dst, fl, fb[r] + 4 * 2 * P, epoch,
+                           band_clear=clip, half=half)
+        # ... then every rank's wait + blend into rank 0's frame (+ rank 0's done flag), then rank 0's wait
+        for r in range(P):
+            dev.wait_flags(d.index, fb[r], P, epoch)
+            rows = L.blocks[r]
+            ptrs, ranges, _ = L.fragments(ib[r], r, epoch, order, bands)
+            dev.composite_signal(d.index, ptrs, (rows[1] - rows[0]) * W, s.background, frame.data_ptr() + 3 * rows[0] * W,
+                                 0, ranges, fb[r] + 4 * (2 * P + 1), [fb[0] + 4 * (P + r)], epoch, half=half)
+        dev.wait_flags(d.index, fb[0] + 4 * P, P, epoch)
+        got = frame.cpu().numpy().copy()
+        # reference: local partials + one composite of the whole frame in visibility order
+        parts = []
+        for r in range(P):
+            part = torch.empty(H * W * 4, dtype=fdt, device=d)
+            dev.march(bricks[r], cam, dtf, s.dt, s.ert, part, W, H)
+            parts.append(part)
+        ref = torch.empty(H * W * 3, dtype=torch.uint8, device=d)
+        dev.composite([parts[o] for o in order], s.background, rgb8=ref)
+        assert np.array_equal(got, ref.view(H, W, 3).cpu().numpy()), f"frame {epoch} differs"
+        for r in range(P):
+            f = flags[r].cpu().numpy()
+            assert (f[:P] == epoch).all(), f"rank {r} arrival flags {f[:P]} at epoch {epoch}"
+            assert f[2 * P] == 0 and f[2 * P + 1] == 0  # the CTA counters reset themselves
+        assert (flags[0].cpu().numpy()[P:2 * P] == epoch).all()
+        if clip:  # the pushed rows of each source are exactly its footprint band within each block
+            for r in range(P):
+                for src in range(P):
+                    rows = L.blocks[r]
+                    c = clip_rows(rows, bands[src])
+                    slot = inbox[r][(L.slot_ptr(0, epoch, src) // L.es) * 4:][: (rows[1] - rows[0]) * W * 4]
+                    written = ~torch.isnan(slot.view(-1, 4)[:, 0].float())
+                    if c:
+                        lo, hi = (c[0] - rows[0]) * W, (c[1] - rows[0]) * W
+                        assert bool(written[lo:hi].all())
+    for b in bricks:
+        b.close()
+
+
+def test_push_targets_reject_bad_layouts(cuda_device):
+    s = c1(P=2, W=64, H=48)
+    d = cuda_device
+    b = dev.DeviceBrick(s.dec.brick(0), d).generate(s.field)
+    dtf = dev.DeviceTF(s.tf, d)
+    buf = torch.zeros(64 * 48 * 4, device=d)
+    fl = torch.zeros(8, dtype=torch.int32, device=d)
+    ok = dict(row_start=[0, 24, 48], dst=[buf.data_ptr(), buf.data_ptr()], flag_ptrs=[fl.data_ptr(), fl.data_ptr() + 4],
+              counter_ptr=fl.data_ptr() + 16, epoch=1)
+    dev.march_push(b, s.cam, dtf, s.dt, s.ert, 64, 48, **ok)
+    from paper_2501_01628_b200.errors import UsageError
+    for bad in (dict(row_start=[0, 24, 40]), dict(epoch=0), dict(dst=[buf.data_ptr() + 4, buf.data_ptr()]),
+                dict(flag_ptrs=[fl.data_ptr(), 0])):
+        with pytest.raises(UsageError):
+            dev.march_push(b, s.cam, dtf, s.dt, s.ert, 64, 48, **{**ok, **bad})
+    torch.cuda.synchronize()
+    b.close()
