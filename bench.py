@@ -729,6 +729,9 @@ def per_rank_leg(cfg: str, strategy: str, device, steps: int, warmup: int, R_vir
                       "shaded_samples": x["shaded_samples"], "contributing_samples": x["contributing_samples"],
                       "shaded_samples_per_s": x["shaded_samples_per_s"]} for x in ranks],
            "clocks": clocks.summary()}
+    if cfg == "c3":
+        log(f"[bench] {cfg} fused march + exchange (p2p_push) of the slowest rank, emulated on this GPU")
+        out["p2p_push_slowest_rank"] = push_leg(wl, slow["rank"], device)
     if cpu:
         log(f"[bench] {cfg} CPU baseline (oracle, strided 1/64 pixel lattice, {R_virtual} bricks)")
         res, _, _ = cpu_baseline_lattice(wl, cam, 8)
@@ -737,6 +740,84 @@ def per_rank_leg(cfg: str, strategy: str, device, steps: int, warmup: int, R_vir
         if g is not None:
             out["reference_gather"] = g
     return out
+
+
+def push_leg(wl: "Workload", rank: int, device, steps: int = 10) -> dict:
+    """The fused march + exchange (p2p_push) of one config-3 rank on ONE GPU: its brick
+    marched with every row block pushed into that block owner's inbox slot (all eight inboxes local here, so
+    this times the kernel's work, not NVLink) and the same march into a local band-clipped partial; then the
+    owner side -- the epoch-flag wait and the blend of one row block from the eight inbox slots, tone-mapped
+    into the frame with the completion signal -- against the plain ranged blend.  Stream-ordered on one
+    stream: every wait is satisfied when issued (no kernel waits on another)."""
+    import torch
+
+    from paper_2501_01628_b200 import device as dev
+    from paper_2501_01628_b200.p2p import PushLayout
+
+    P, W, H = wl.dec.P, wl.W, wl.H
+    cam = wl.cams[0]
+    dtf = dev.DeviceTF(wl.tf, device)
+    L = PushLayout(P, W, H, 16)
+    inbox = [torch.zeros(L.inbox_pixels() * 4, dtype=torch.float32, device=device) for _ in range(P)]
+    flags = [torch.zeros(L.flag_words(), dtype=torch.int32, device=device) for _ in range(P)]
+    ib, fb = [t.data_ptr() for t in inbox], [t.data_ptr() for t in flags]
+    bands = [tuple(dev.desc_footprint(wl.dec.brick(s), cam, W, H)[1::2]) for s in range(P)]
+    order = wl.dec.visibility_order(cam.position)
+    brick = dev.DeviceBrick(wl.dec.brick(rank), device).generate(wl.field)
+    part = torch.empty(W * H * 4, dtype=torch.float32, device=device)
+    frame = torch.empty(W * H * 3, dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream(device)
+    epoch = [0]
+
+    def push():
+        epoch[0] += 1
+        dst, fl = L.march_targets(ib, fb, rank, epoch[0])
+        dev.march_push(brick, cam, dtf, DT, ERT, W, H, L.row_start, dst, fl, fb[rank] + L.counter_offset(0), epoch[0],
+                       band_clear=True)
+
+    def local():
+        dev.march(brick, cam, dtf, DT, ERT, part, W, H, band_clear=True)
+
+    owner = 0
+    rows = L.blocks[owner]
+    npix = (rows[1] - rows[0]) * W
+
+    def blend_push():
+        # the owner's side of frame `epoch`: every source's flag was raised by `prime` below
+        dev.wait_flags(device.index, fb[owner], P, epoch[0])
+        ptrs, ranges, _ = L.fragments(ib[owner], owner, epoch[0], order, bands)
+        dev.composite_signal(device.index, ptrs, npix, BACKGROUND, frame.data_ptr() + 3 * rows[0] * W, 0, ranges,
+                             fb[owner] + L.counter_offset(1), [fb[0] + 4 * (P + owner)], epoch[0])
+
+    def blend_plain():
+        ptrs, ranges, _ = L.fragments(ib[owner], owner, epoch[0], order, bands)
+        dev.composite_ptrs(device.index, ptrs, npix, BACKGROUND, rgb8_ptr=frame.data_ptr() + 3 * rows[0] * W,
+                           ranges=ranges)
+
+    for _ in range(3):
+        push()
+        local()
+    torch.cuda.synchronize(device)
+    with ClockSampler(device.index) as clocks:
+        push_ms = events_ms(push, steps, stream)
+        local_ms = events_ms(local, steps, stream)
+        # raise every source's flag of the current epoch (the other ranks' marches, already complete)
+        for s in range(P):
+            for w in range(P):
+                flags[w][s] = epoch[0]
+        torch.cuda.synchronize(device)
+        wait_blend_ms = graph_ms(blend_push, 20, device)
+        blend_ms = graph_ms(blend_plain, 20, device)
+    brick.close()
+    sent = sum((min(b[1], bands[rank][1]) - max(b[0], bands[rank][0])) * W for j, b in enumerate(L.blocks)
+               if j != rank and min(b[1], bands[rank][1]) > max(b[0], bands[rank][0]))
+    return {"rank": rank, "push_march_ms": push_ms, "local_band_march_ms": local_ms,
+            "push_over_local": push_ms / local_ms,
+            "owner_wait_and_blend_ms": wait_blend_ms, "owner_plain_blend_ms": blend_ms,
+            "fragment_bytes_pushed": 16 * sent,
+            "note": "one GPU: the eight inboxes are local, so this is the kernels' own cost; on 8 GPUs the pushed "
+                    "rows cross NVLink during the march instead of after it (DESIGN.md §6)",
+            "clocks": clocks.summary()}
 
 
 def c4_orbit_leg(device, steps: int = 5, every: int = 6) -> dict:

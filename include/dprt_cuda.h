@@ -192,6 +192,7 @@ int dprt_composite_ranged(int device, const float* const* inputs, const int64_t*
  * of its block reach the frame's epoch (dprt_wait_flags, then dprt_composite_ranged on local memory).
  * All arrays are HOST arrays of P entries; pointers are device pointers (local or peer-mapped). */
 #define DPRT_MAX_PUSH 16
+#define DPRT_SIGNAL_COUNTER_WORDS 1056 /* 33 counters 128 bytes apart (a top counter + 32 sub-counters) */
 typedef struct DprtPushTargets {
     int32_t P;                 /* row blocks (ranks), 2..DPRT_MAX_PUSH */
     int32_t reserved;
@@ -199,7 +200,8 @@ typedef struct DprtPushTargets {
     void* const* dst;          /* dst[b]: this rank's fragment of block b at its owner; pixel (x, y) of the
                                   block at element (y - row_start[b]) * W + x (16 B f32 / 8 B fp16 RGBA) */
     uint32_t* const* flags;    /* flags[b]: this rank's epoch word at block b's owner */
-    uint32_t* counter;         /* device word, zero before the first launch (self-resetting CTA count) */
+    uint32_t* counter;         /* DPRT_SIGNAL_COUNTER_WORDS device words, zero before the first launch
+                                  (self-resetting CTA counts); one set per concurrently running launch */
     uint32_t epoch;            /* frame tag written to every flags[b]; nonzero, increasing per frame */
     uint32_t reserved2;
 } DprtPushTargets;
@@ -217,8 +219,8 @@ int dprt_wait_flags(int device, const uint32_t* flags, int n, uint32_t epoch, vo
 
 /* dprt_composite_ranged that also signals: when its last CTA retires (every CTA having fenced its stores
  * -- e.g. RGB8 rows written into rank 0's frame over NVLink -- at system scope) it release-stores `epoch`
- * into flags[i] (i < n_flags; HOST array of device pointers, local or peer).  counter: a device word, zero
- * before the first launch (self-resetting). */
+ * into flags[i] (i < n_flags; HOST array of device pointers, local or peer).  counter: DPRT_SIGNAL_COUNTER_WORDS
+ * device words, zero before the first launch (self-resetting). */
 int dprt_composite_signal(int device, const float* const* inputs, const int64_t* ranges, int P, int64_t npix,
                           const float bg[3], int flags, uint8_t* rgb8, float* rgba_out, uint32_t* counter,
                           uint32_t* const* signal, int n_signal, uint32_t epoch, void* stream);

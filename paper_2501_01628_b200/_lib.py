@@ -50,6 +50,7 @@ EXPORTS = (
     "dprt_trace_nearest", "dprt_trace_any", "dprt_march_push", "dprt_wait_flags", "dprt_composite_signal",
 )
 MAX_PUSH = 16  # DPRT_MAX_PUSH
+SIGNAL_COUNTER_WORDS = 1056  # DPRT_SIGNAL_COUNTER_WORDS
 
 c_double3 = ctypes.c_double * 3
 c_int64_3 = ctypes.c_int64 * 3

@@ -140,23 +140,45 @@ struct CompositeArgs {
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
-// Last-CTA completion signal: every thread fences its own stores at system scope, the CTA counts itself
-// in `ctr` (atomicInc wraps it back to 0 for the next launch), and the CTA that completes the count
-// release-stores `epoch` into flags[0 .. n).  Every thread of every CTA must reach this call.
+// Last-CTA completion signal.  The CTA's threads meet at a barrier and its thread 0 fences at system scope
+// (cumulative: the fence orders every store the barrier ordered before it, the whole CTA's), then counts the
+// CTA in one of up to 32 sub-counters (128-byte apart: a single counter serialised 4,000 CTAs of a 4K
+// row-block blend for ~14 us); the CTA that completes a sub-counter fences and counts it in the top counter,
+// and the one that completes the top counter fences and release-stores `epoch` into flags[0 .. n).
+// atomicInc wraps every counter back to 0, ready for the next launch.  `ctr` points at
+// DPRT_SIGNAL_COUNTER_WORDS zeroed words.  Every thread of every CTA must reach this call.
+constexpr unsigned kSigSub = 32, kSigStride = 32;  // sub-counters, words between counters
+#ifndef DPRT_SIGNAL_FENCE
+#define DPRT_SIGNAL_FENCE 2  // per-CTA fence before counting: 2 = system scope, 1 = GPU scope, 0 = none (timing only)
+#endif
 __device__ __forceinline__ void grid_signal(unsigned* ctr, unsigned* const* flags, int n, unsigned epoch) {
-    __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
+#if DPRT_SIGNAL_FENCE == 2
+        __threadfence_system();
+#elif DPRT_SIGNAL_FENCE == 1
+        __threadfence();
+#endif
         const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-        if (atomicInc(ctr, total - 1) == total - 1) {
+        const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        const unsigned nsub = total < kSigSub ? total : kSigSub;
+        const unsigned i = cta % nsub;
+        const unsigned quota = total / nsub + (i < total % nsub ? 1u : 0u);
+        if (atomicInc(ctr + kSigStride * (1 + i), quota - 1) == quota - 1) {
             __threadfence_system();
-            for (int i = 0; i < n; ++i) st_release_sys(flags[i], epoch);
+            if (atomicInc(ctr, nsub - 1) == nsub - 1) {
+                __threadfence_system();  // one release fence for all n flags (st.release would fence per store)
+                for (int f = 0; f < n; ++f) st_relaxed_sys(flags[f], epoch);
+            }
         }
     }
 }

@@ -69,8 +69,7 @@ __device__ __forceinline__ void load4(const float4* frag, long long i, float4 f[
 // the 12 RGB8 bytes leave as three aligned 32-bit stores.  A fragment covers only the tile pixels
 // [lo, hi) (a rank's footprint rows): outside them it is clear and is not read at all.
 template <bool kHalf>
-__device__ __forceinline__ void composite4_body(const CompositeArgs& a) {
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void composite4_body(const CompositeArgs& a, long long q) {
     const long long i0 = q * 4;
     if (i0 >= a.npix) return;
     if (i0 + 4 <= a.npix) {
@@ -128,17 +127,24 @@ __device__ __forceinline__ void composite4_body(const CompositeArgs& a) {
     }
 }
 
-template <bool kHalf>
+// Grid-stride: one pass for the plain launch; a signalling launch (dprt_composite_signal) runs a capped grid
+// so only a few CTAs per SM pay the system-scope fence of grid_signal.
+template <bool kHalf, bool kSig>
 __global__ void __launch_bounds__(256) composite_kernel(const CompositeArgs a) {
-    composite4_body<kHalf>(a);
-    if (a.n_sig) grid_signal(a.sig_ctr, a.sig, a.n_sig, a.sig_epoch);  // e.g. rows written into rank 0's frame
+    const long long q0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if constexpr (!kSig) {
+        composite4_body<kHalf>(a, q0);
+    } else {
+        const long long n = (a.npix + 3) / 4, stride = (long long)gridDim.x * blockDim.x;
+        for (long long q = q0; q < n; q += stride) composite4_body<kHalf>(a, q);
+        grid_signal(a.sig_ctr, a.sig, a.n_sig, a.sig_epoch);  // e.g. rows written into rank 0's frame
+    }
 }
 
 // Small tiles (a rank's row block after the exchange): one pixel per thread, so the grid still fills the
 // 148 SMs, with up to 8 fragments' loads issued before the first is blended.
 template <bool kHalf>
-__device__ __forceinline__ void composite_px_body(const CompositeArgs& a) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void composite_px_body(const CompositeArgs& a, long long i) {
     if (i >= a.npix) return;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int p0 = 0; p0 < a.P; p0 += 8) {
@@ -158,10 +164,16 @@ __device__ __forceinline__ void composite_px_body(const CompositeArgs& a) {
         for (int ch = 0; ch < 3; ++ch) a.rgb8[3 * i + ch] = (uint8_t)pack_rgb8(acc, a.bg, ch);
 }
 
-template <bool kHalf>
+template <bool kHalf, bool kSig>
 __global__ void __launch_bounds__(256) composite_px_kernel(const CompositeArgs a) {
-    composite_px_body<kHalf>(a);
-    if (a.n_sig) grid_signal(a.sig_ctr, a.sig, a.n_sig, a.sig_epoch);
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if constexpr (!kSig) {
+        composite_px_body<kHalf>(a, i0);
+    } else {
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        for (long long i = i0; i < a.npix; i += stride) composite_px_body<kHalf>(a, i);
+        grid_signal(a.sig_ctr, a.sig, a.n_sig, a.sig_epoch);
+    }
 }
 
 // Stream-ordered wait for peers' epoch flags (dprt_wait_flags): one warp spins with system-scope acquire
@@ -190,25 +202,36 @@ cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t stream) {
     if (a.npix == 0) {
         if (a.n_sig) {  // nothing to blend: still signal (one CTA, no stores to fence but its own)
             CompositeArgs e = a;
-            composite_px_kernel<false><<<1, 32, 0, stream>>>(e);
+            composite_px_kernel<false, true><<<1, 32, 0, stream>>>(e);
             return cudaGetLastError();
         }
         return cudaSuccess;
     }
+    int cap = 0;  // signalling launches: at most 8 CTAs per SM
+    if (a.n_sig) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cap = 8 * sms;
+    }
     if (a.npix < DPRT_COMPOSITE_PX_BELOW && a.P >= 3) {
-        const long long grid = (a.npix + block - 1) / block;
-        if (a.flags & DPRT_COMPOSITE_HALF_IN)
-            composite_px_kernel<true><<<(unsigned)grid, block, 0, stream>>>(a);
+        long long grid = (a.npix + block - 1) / block;
+        if (cap && grid > cap) grid = cap;
+        const bool h = a.flags & DPRT_COMPOSITE_HALF_IN;
+        if (a.n_sig)
+            (h ? composite_px_kernel<true, true> : composite_px_kernel<false, true>)<<<(unsigned)grid, block, 0, stream>>>(a);
         else
-            composite_px_kernel<false><<<(unsigned)grid, block, 0, stream>>>(a);
+            (h ? composite_px_kernel<true, false> : composite_px_kernel<false, false>)<<<(unsigned)grid, block, 0, stream>>>(a);
         return cudaGetLastError();
     }
     const long long threads = (a.npix + 3) / 4;
-    const long long grid = (threads + block - 1) / block;
-    if (a.flags & DPRT_COMPOSITE_HALF_IN)
-        composite_kernel<true><<<(unsigned)grid, block, 0, stream>>>(a);
+    long long grid = (threads + block - 1) / block;
+    if (cap && grid > cap) grid = cap;
+    const bool h = a.flags & DPRT_COMPOSITE_HALF_IN;
+    if (a.n_sig)
+        (h ? composite_kernel<true, true> : composite_kernel<false, true>)<<<(unsigned)grid, block, 0, stream>>>(a);
     else
-        composite_kernel<false><<<(unsigned)grid, block, 0, stream>>>(a);
+        (h ? composite_kernel<true, false> : composite_kernel<false, false>)<<<(unsigned)grid, block, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

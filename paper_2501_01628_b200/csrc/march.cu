@@ -400,12 +400,12 @@ __device__ __forceinline__ int fl2cell(float u, int hi) { return min(__float2int
 
 // A pixel of the RGBA partial: the local buffer (out / out16 at pix - pix0) or, in the fused march +
 // exchange (kPush, dprt_march_push), its row block's owner's inbox over NVLink.
+// s_blk (kPush): the row -> row-block table in shared memory, built once per CTA in the kernel's prologue.
 template <bool kPush>
-__device__ __forceinline__ void store_partial(const MarchArgs& a, long long pix, int y, float C0, float C1, float C2,
-                                              float A) {
+__device__ __forceinline__ void store_partial(const MarchArgs& a, const uint8_t* s_blk, long long pix, int y, float C0,
+                                              float C1, float C2, float A) {
     if constexpr (kPush) {
-        int b = 0;
-        while (b + 1 < a.push_P && y >= a.push_row[b + 1]) ++b;
+        const int b = s_blk[y];
         const long long e = pix - (long long)a.push_row[b] * a.W;
         if (a.half_out) {
             const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
@@ -416,6 +416,7 @@ __device__ __forceinline__ void store_partial(const MarchArgs& a, long long pix,
         }
     } else {
         (void)y;
+        (void)s_blk;
         if (a.half_out) {
             const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
             a.out16[pix - a.pix0] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
@@ -431,7 +432,8 @@ __device__ __forceinline__ void store_partial(const MarchArgs& a, long long pix,
 // the fused RGB8 frame, a clear fragment (0) for an RGBA partial.  Blocks take whole rows, threads 4-pixel
 // groups; a group straddling the rectangle's edge writes only its outside pixels (the beams own the inside).
 template <bool kPush>
-__device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1, int unit, int nunits, int t, int nt) {
+__device__ void fill_outside_rect(const MarchArgs& a, const uint8_t* s_blk, int y0, int y1, int unit, int nunits, int t,
+                                  int nt) {
     const uint32_t cr = (uint32_t)floorf(fminf(fmaxf(a.bg[0], 0.f), 1.f) * 255.f + 0.5f);
     const uint32_t cg = (uint32_t)floorf(fminf(fmaxf(a.bg[1], 0.f), 1.f) * 255.f + 0.5f);
     const uint32_t cb = (uint32_t)floorf(fminf(fmaxf(a.bg[2], 0.f), 1.f) * 255.f + 0.5f);
@@ -465,7 +467,7 @@ __device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1, int unit, 
                 for (int k = 0; k < 4; ++k) {
                     const int x = x0 + k;
                     if (x >= W || (!row_out && x >= a.rect[0] && x < a.rect[2])) continue;
-                    store_partial<kPush>(a, i0 + k, y, 0.f, 0.f, 0.f, 0.f);
+                    store_partial<kPush>(a, s_blk, i0 + k, y, 0.f, 0.f, 0.f, 0.f);
                 }
             }
         }
@@ -474,13 +476,13 @@ __device__ void fill_outside_rect(const MarchArgs& a, int y0, int y1, int unit, 
 
 // A pixel inside the footprint whose ray adds nothing (no owned sample, or a beam that misses the brick).
 template <bool kPush>
-__device__ __forceinline__ void write_clear(const MarchArgs& a, int pix, int py) {
+__device__ __forceinline__ void write_clear(const MarchArgs& a, const uint8_t* s_blk, int pix, int py) {
     if (a.rgb8) {
         uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
 #pragma unroll
         for (int c = 0; c < 3; ++c) dst[c] = (uint8_t)floorf(fminf(fmaxf(a.bg[c], 0.f), 1.f) * 255.f + 0.5f);
     } else {
-        store_partial<kPush>(a, pix, py, 0.f, 0.f, 0.f, 0.f);
+        store_partial<kPush>(a, s_blk, pix, py, 0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -522,6 +524,14 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         const float4 e1 = i + 1 < a.n_tf ? a.tf[i + 1] : e0;
         s_tf[i] = e0;
         s_tf[a.n_tf + i] = make_float4(e1.x - e0.x, e1.y - e0.y, e1.z - e0.z, e1.w - e0.w);
+    }
+    uint8_t* s_blk = reinterpret_cast<uint8_t*>(s_tf + 2 * a.n_tf);  // kPush: row -> row block (H bytes)
+    if constexpr (kPush) {
+        for (int y = tid; y < a.H; y += blockDim.x) {
+            int b = 0;
+            while (b + 1 < a.push_P && y >= a.push_row[b + 1]) ++b;
+            s_blk[y] = (uint8_t)b;
+        }
     }
     __syncthreads();
     const unsigned FULL = 0xffffffffu;
@@ -596,7 +606,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         }
         const unsigned hitm = __ballot_sync(FULL, nn > 0);
         if (!hitm) {
-            if (!kMark && inside && !a.accum) write_clear<kPush>(a, pix, py);  // no ray of this beam meets the brick
+            if (!kMark && inside && !a.accum) write_clear<kPush>(a, s_blk, pix, py);  // no ray of this beam meets the brick
             continue;
         }
 #if DPRT_COUNTERS
@@ -863,7 +873,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
                 dst[2] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[2], C2), 0.f), 1.f) * 255.f + 0.5f);
             } else {
-                store_partial<kPush>(a, pix, py, C0, C1, C2, A);
+                store_partial<kPush>(a, s_blk, pix, py, C0, C1, C2, A);
             }
         }
     }
@@ -878,7 +888,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         const int y0 = a.band_clear ? a.rect[1] : (int)(a.pix0 / a.W);
         const int y1 = a.band_clear ? a.rect[3] : (int)((a.pix0 + a.npix_buf) / a.W);
         const int wpb = blockDim.x >> 5;
-        fill_outside_rect<kPush>(a, y0, y1, (int)blockIdx.x * wpb + (tid >> 5), (int)gridDim.x * wpb, lane, 32);
+        fill_outside_rect<kPush>(a, s_blk, y0, y1, (int)blockIdx.x * wpb + (tid >> 5), (int)gridDim.x * wpb, lane, 32);
     }
     if constexpr (kPush) grid_signal(a.push_ctr, a.push_flag, a.push_P, a.push_epoch);  // fragments landed at owners
 #if DPRT_COUNTERS
@@ -1038,7 +1048,8 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
               march_beam_kernel<true, kDeepUnroll, kDeepBlocks, true, false, true>}}};
         const int hq = a.half_quads ? 1 : 0, dp = a.deep ? 1 : 0, wd = a.wide ? 1 : 0;
         const K kern = a.push_P ? pushk[hq][dp][wd] : kerns[hq][dp][wd];
-        kern<<<grid_for((const void*)kern, kBeamBlock, smem), kBeamBlock, smem, stream>>>(a);
+        const size_t sm = a.push_P ? smem + (size_t)((a.H + 15) & ~15) : smem;  // + the row -> block table
+        kern<<<grid_for((const void*)kern, kBeamBlock, sm), kBeamBlock, sm, stream>>>(a);
         return cudaGetLastError();
     }
     march_kernel<<<grid_for((const void*)march_kernel, kTileX * kTileY, smem), block, smem, stream>>>(a);

@@ -118,8 +118,6 @@ class P2PCompositor:
 # into the block owner's inbox over NVLink while it runs, so the fragment exchange overlaps the march tile
 # by tile; per-source epoch flags in the owner's memory replace the stream-ordered NCCL barriers.
 
-FLAG_WORDS = 2  # per rank beyond the 2P epoch words: [0, P) fragment arrivals, [P, 2P) frame rows done
-                # (read on rank 0), 2P march CTA counter, 2P + 1 composite CTA counter
 
 
 class PushLayout:
@@ -140,8 +138,15 @@ class PushLayout:
     def inbox_pixels(self) -> int:
         return 2 * self.P * self.slot
 
+    # A rank's flag buffer (int32 words): [0, P) fragment arrivals (one epoch word per source), [P, 2P) frame
+    # rows done (read on rank 0), then two DPRT_SIGNAL_COUNTER_WORDS counter sets (march, blend), 128-byte
+    # aligned.
+    def counter_offset(self, which: int) -> int:
+        """Byte offset of counter set ``which`` (0 = march, 1 = blend) in a flag buffer."""
+        return 4 * ((2 * self.P + 31) // 32 * 32 + which * dev._lib.SIGNAL_COUNTER_WORDS)
+
     def flag_words(self) -> int:
-        return 2 * self.P + FLAG_WORDS
+        return self.counter_offset(2) // 4
 
     def slot_ptr(self, inbox_base: int, epoch: int, src: int) -> int:
         return inbox_base + self.es * (((epoch & 1) * self.P + src) * self.slot)
@@ -245,8 +250,7 @@ class P2PPushCompositor:
         """Start a frame: (row_start, dst pointers, flag pointers, counter pointer, epoch) for dprt_march_push."""
         self.epoch += 1
         dst, fl = self.layout.march_targets(self.peer_inbox, self.peer_flags, self.ep.rank, self.epoch)
-        counter = self.flags.ptr + 4 * (2 * self.ep.R)
-        return self.layout.row_start, dst, fl, counter, self.epoch
+        return self.layout.row_start, dst, fl, self.flags.ptr + self.layout.counter_offset(0), self.epoch
 
     def composite(self, order: Sequence[int], background, keep_float: bool = False, bands=None) -> CompositeOutput:
         ep, L, e = self.ep, self.layout, self.epoch
@@ -260,7 +264,7 @@ class P2PPushCompositor:
         off = rows[0] * self.W
         dev.composite_signal(self.index, ptrs, npix, background, self.root_frame + 3 * off,
                              (self.root_rgba + 16 * off) if keep_float else 0, ranges,
-                             self.flags.ptr + 4 * (2 * ep.R + 1), [self.peer_flags[0] + 4 * (ep.R + r)], e,
+                             self.flags.ptr + L.counter_offset(1), [self.peer_flags[0] + 4 * (ep.R + r)], e,
                              half=self.fdt == torch.float16)
         # bytes this rank moved over NVLink this frame: its pushed fragments (those of the other blocks) and
         # its RGB8 rows into rank 0's frame

@@ -19,7 +19,7 @@ import pytest
 import torch
 
 from paper_2501_01628_b200 import device as dev
-from paper_2501_01628_b200.compositor import assign_rows, clip_rows
+from paper_2501_01628_b200.compositor import clip_rows
 from paper_2501_01628_b200.geom import orbit_camera
 from paper_2501_01628_b200.p2p import PushLayout
 from scenes import c1
@@ -55,15 +55,16 @@ def test_push_frames_equal_local_march_and_composite(cuda_device, P, W, H, clip,
         # every rank's march first (pushing into every owner's inbox slot, raising its flags) ...
         for r in range(P):
             dst, fl = L.march_targets(ib, fb, r, epoch)
-            dev.march_push(bricks[r], cam, dtf, s.dt, s.ert, W, H, L.row_start, dst, fl, fb[r] + 4 * 2 * P, epoch,
-                           band_clear=clip, half=half)
+            dev.march_push(bricks[r], cam, dtf, s.dt, s.ert, W, H, L.row_start, dst, fl, fb[r] + L.counter_offset(0),
+                           epoch, band_clear=clip, half=half)
         # ... then every rank's wait + blend into rank 0's frame (+ rank 0's done flag), then rank 0's wait
         for r in range(P):
             dev.wait_flags(d.index, fb[r], P, epoch)
             rows = L.blocks[r]
             ptrs, ranges, _ = L.fragments(ib[r], r, epoch, order, bands)
-            dev.composite_signal(d.index, ptrs, (rows[1] - rows[0]) * W, s.background, frame.data_ptr() + 3 * rows[0] * W,
-                                 0, ranges, fb[r] + 4 * (2 * P + 1), [fb[0] + 4 * (P + r)], epoch, half=half)
+            dev.composite_signal(d.index, ptrs, (rows[1] - rows[0]) * W, s.background,
+                                 frame.data_ptr() + 3 * rows[0] * W, 0, ranges, fb[r] + L.counter_offset(1),
+                                 [fb[0] + 4 * (P + r)], epoch, half=half)
         dev.wait_flags(d.index, fb[0] + 4 * P, P, epoch)
         got = frame.cpu().numpy().copy()
         # reference: local partials + one composite of the whole frame in visibility order
@@ -78,7 +79,7 @@ def test_push_frames_equal_local_march_and_composite(cuda_device, P, W, H, clip,
         for r in range(P):
             f = flags[r].cpu().numpy()
             assert (f[:P] == epoch).all(), f"rank {r} arrival flags {f[:P]} at epoch {epoch}"
-            assert f[2 * P] == 0 and f[2 * P + 1] == 0  # the CTA counters reset themselves
+            assert not f[L.counter_offset(0) // 4:].any()  # the CTA counters reset themselves
         assert (flags[0].cpu().numpy()[P:2 * P] == epoch).all()
         if clip:  # the pushed rows of each source are exactly its footprint band within each block
             for r in range(P):
@@ -100,9 +101,9 @@ def test_push_targets_reject_bad_layouts(cuda_device):
     b = dev.DeviceBrick(s.dec.brick(0), d).generate(s.field)
     dtf = dev.DeviceTF(s.tf, d)
     buf = torch.zeros(64 * 48 * 4, device=d)
-    fl = torch.zeros(8, dtype=torch.int32, device=d)
+    fl = torch.zeros(4 + 2 * 1056, dtype=torch.int32, device=d)
     ok = dict(row_start=[0, 24, 48], dst=[buf.data_ptr(), buf.data_ptr()], flag_ptrs=[fl.data_ptr(), fl.data_ptr() + 4],
-              counter_ptr=fl.data_ptr() + 16, epoch=1)
+              counter_ptr=fl.data_ptr() + 128, epoch=1)
     dev.march_push(b, s.cam, dtf, s.dt, s.ert, 64, 48, **ok)
     from paper_2501_01628_b200.errors import UsageError
     for bad in (dict(row_start=[0, 24, 40]), dict(epoch=0), dict(dst=[buf.data_ptr() + 4, buf.data_ptr()]),
