@@ -47,6 +47,12 @@ if "c3_per_rank" in d:
         for x in c["ranks"]:
             L.append(f"| {x['rank']} | {x['kernel_ms']:.3f} | {x['needed_bytes'] / 1e6:.0f} | {x['shaded_samples'] / 1e6:.1f} | "
                      f"{x['shaded_samples'] / x['kernel_ms'] / 1e6:.0f} | {x['frac_needed']:.3f} |")
+        pu = c.get("p2p_push_slowest_rank")
+        if pu:
+            L.append(f"Fused march + exchange (p2p_push) of rank {pu['rank']}, inboxes local: push march "
+                     f"{pu['push_march_ms']:.3f} ms vs {pu['local_band_march_ms']:.3f} ms into a local band-clipped "
+                     f"partial ({pu['push_over_local']:.3f}x); owner wait + blend {pu['owner_wait_and_blend_ms']:.4f} ms vs "
+                     f"bare blend {pu['owner_plain_blend_ms']:.4f} ms; {pu['fragment_bytes_pushed'] / 1e6:.1f} MB pushed.")
         L.append("")
     ev = d["c3_per_rank"].get("even", {})
     if ev.get("cpu_baseline"):
