@@ -373,6 +373,9 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #ifndef DPRT_BEAM_PROBE
 #define DPRT_BEAM_PROBE 1
 #endif
+#ifndef DPRT_PROBE_LOOP
+#define DPRT_PROBE_LOOP 1  // per-lane probe loops over consecutive empty cubes (0: one jump per warp iteration)
+#endif
 #ifndef DPRT_SLAB_SHIFT
 #define DPRT_SLAB_SHIFT DPRT_MACRO_SHIFT  // slab thickness (cells, log2) of the probe-mode beam step
 #endif
@@ -609,7 +612,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             if (!kMark && inside && !a.accum) write_clear<kPush>(a, s_blk, pix, py);  // no ray of this beam meets the brick
             continue;
         }
-#if DPRT_COUNTERS
+#if DPRT_COUNTERS == 1
         c_rays += nn > 0;
 #endif
         // dominant axis of the beam (from its first ray) and whether every ray agrees with it
@@ -649,18 +652,33 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         while (true) {
             const unsigned livem = __ballot_sync(FULL, live);
             if (!livem) break;
+#if DPRT_COUNTERS == 2
+            if (lane == 0) ++c_shade;  // [0]: warp slab iterations (probe + slab step)
+#endif
 #if DPRT_BEAM_PROBE
             // per-lane probe: a lane whose next sample sits in an empty macrocell jumps over the empty
             // Chebyshev cube around it on its own (exact); only lanes in non-empty macrocells go on to
             // the slab step, which then needs no beam-wide emptiness test
             bool samp = live;
+#if DPRT_PROBE_LOOP
+            // ... and keeps jumping until its next sample sits in a non-empty macrocell (then it shades in
+            // this same iteration) or its ray is done: a jump costs the probe alone, not a whole warp
+            // iteration (ballot, slab selection) per empty cube
+            while (live && a.skip) {
+#else
             if (live && a.skip) {
+#endif
                 const float fj = (float)j;
                 const int mx = fl2cell(fmaf(fj, st[0], p0[0]), chx) >> kMacroShift;
                 const int my = fl2cell(fmaf(fj, st[1], p0[1]), chy) >> kMacroShift;
                 const int mz = fl2cell(fmaf(fj, st[2], p0[2]), chz) >> kMacroShift;
                 const int dist = (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx);
+#if DPRT_PROBE_LOOP
+                if (dist == 0) break;
+                {
+#else
                 if (dist > 0) {
+#endif
                     float je = 3.0e38f;
                     if (st[0] != 0.f)
                         je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0]);
@@ -670,13 +688,20 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                         je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2]);
                     j = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;
                     if (j >= nn) live = false;
+#if DPRT_PROBE_LOOP
+                    samp = live;
+#else
                     samp = false;
-#if DPRT_COUNTERS
+#endif
+#if DPRT_COUNTERS == 1
                     ++c_skip;
 #endif
                 }
             }
             if (!__any_sync(FULL, samp)) continue;
+#if DPRT_COUNTERS == 2
+            if (lane == 0) ++c_contrib;  // [1]: warp iterations that shade
+#endif
 #else
             const bool samp = live;
 #endif
@@ -747,6 +772,10 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             // address, an L1 hit) and contribute w = 0; ERT masks the rest of the batch the same way
             const float fend = (float)(jend - 1);
             while (j < jend) {
+#if DPRT_COUNTERS == 2
+                if (lane == __ffs(__activemask()) - 1) ++c_skip;  // [2]: warp batches
+                ++c_rays;                                         // [3]: lane batches
+#endif
                 float4 qa[kUnroll], qb[kUnroll];
                 float wx[kUnroll], wy[kUnroll], wz[kUnroll];
                 const float fj = (float)j;  // exact: j < 2^24
@@ -803,7 +832,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
                     C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
                     const float m = (lv && u < cnt) ? 1.f : 0.f;
-#if DPRT_COUNTERS
+#if DPRT_COUNTERS == 1
                     c_shade += m != 0.f;
                     c_contrib += w > 0.f;
 #endif
@@ -837,7 +866,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     C0 = fmaf(w, fmaf(tfr, de.x, e0.x), C0);
                     C1 = fmaf(w, fmaf(tfr, de.y, e0.y), C1);
                     C2 = fmaf(w, fmaf(tfr, de.z, e0.z), C2);
-#if DPRT_COUNTERS
+#if DPRT_COUNTERS == 1
                     c_shade += m != 0.f;
                     c_contrib += w > 0.f;
 #endif
