@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 // jumps every lane over the empty slabs at once or lets each lane shade its samples in the slab.  No
 // per-sample skip test, lanes stay in step, and the 32 rays read the same L1 lines.
 #ifndef DPRT_BEAM_UNROLL
-#define DPRT_BEAM_UNROLL 4
+#define DPRT_BEAM_UNROLL 3  // 3 since the per-lane probe loop (c2 0.2236 -> 0.2163 ms; it was 4 before, 3 lost then)
 #endif
 constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 
@@ -508,7 +508,7 @@ constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are indep
 // signed offsets from stored voxel (0, 0, 0).  (A 64-bit z-plane term measured 6-12 % slower.)
 //
 // kUnroll / kMinBlocks: samples per branch-free batch and CTAs per SM.  Small bricks (c2: ~0.3 GB of touched
-// quads, L2 hit ~48 %) are issue / L1 bound and run 4 @ 3 CTAs (24 warps); large ones (c3: 2.5-4.4 GB of
+// quads, L2 hit ~48 %) are issue / L1 bound and run 3 @ 3 CTAs (24 warps); large ones (c3: 2.5-4.4 GB of
 // touched quads, L2 hit ~25 %) are memory-latency bound and run 6 @ 2 CTAs -- fewer warps, more loads in
 // flight per warp (c3 slowest ranks -6 to -12 %, c2 +15 %).  Chosen per launch from the
 // brick size (launch_march).
