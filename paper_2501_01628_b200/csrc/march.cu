@@ -376,6 +376,9 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #ifndef DPRT_PROBE_LOOP
 #define DPRT_PROBE_LOOP 1  // per-lane probe loops over consecutive empty cubes (0: one jump per warp iteration)
 #endif
+#ifndef DPRT_JUMP_BRANCHFREE
+#define DPRT_JUMP_BRANCHFREE 1
+#endif
 #ifndef DPRT_SLAB_SHIFT
 #define DPRT_SLAB_SHIFT DPRT_MACRO_SHIFT  // slab thickness (cells, log2) of the probe-mode beam step
 #endif
@@ -679,6 +682,15 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
 #else
                 if (dist > 0) {
 #endif
+#if DPRT_JUMP_BRANCHFREE
+                    // exit of the empty cube along each axis, branch-free: an axis the ray does not move along
+                    // has ist = 0 and so gives je = 0, which only shortens the jump to one sample (still exact;
+                    // rays with an exactly zero direction component are rare)
+                    const float jx = ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0];
+                    const float jy = ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << kMacroShift) - p0[1]) * ist[1];
+                    const float jz = ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2];
+                    const float je = fminf(fminf(jx, jy), jz);
+#else
                     float je = 3.0e38f;
                     if (st[0] != 0.f)
                         je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0]);
@@ -686,6 +698,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                         je = fminf(je, ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << kMacroShift) - p0[1]) * ist[1]);
                     if (st[2] != 0.f)
                         je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2]);
+#endif
                     j = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;
                     if (j >= nn) live = false;
 #if DPRT_PROBE_LOOP
