@@ -197,7 +197,10 @@ class P2PPushCompositor:
     must never share a GPU with the work it waits for): ``try_create`` checks that collectively."""
 
     def __init__(self, ep: RankEndpoint, width: int, height: int, device: torch.device,
-                 fragment_dtype: torch.dtype = torch.float32):
+                 fragment_dtype: torch.dtype = torch.float32, _emulated: bool = False):
+        """``_emulated`` (tests only): accept ranks that share a GPU.  Such ranks must then issue every
+        rank's march before any rank's ``composite`` and rank 0's last, from ONE thread on one stream, so
+        that every flag wait is satisfied when it is issued (tests/test_gpu_push.py)."""
         self.ep = ep
         self.fdt = fragment_dtype
         self.px = 8 if fragment_dtype == torch.float16 else 16
@@ -219,7 +222,7 @@ class P2PPushCompositor:
         except Exception:  # noqa: BLE001 - reported through self.ok
             self.ok = False
         ids = ep.all_gather_bytes(_device_identity(self.index).encode() if device.type == "cuda" else b"cpu")
-        self.distinct = len(set(ids)) == len(ids)
+        self.distinct = len(set(ids)) == len(ids) or _emulated
         self.peer_inbox = ep.share_pointers(self.index, self.inbox.ptr if self.inbox else 0)
         self.peer_flags = ep.share_pointers(self.index, self.flags.ptr if self.flags else 0)
         self.root_frame = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)[0]

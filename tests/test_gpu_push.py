@@ -112,3 +112,46 @@ def test_push_targets_reject_bad_layouts(cuda_device):
             dev.march_push(b, s.cam, dtf, s.dt, s.ert, 64, 48, **{**ok, **bad})
     torch.cuda.synchronize()
     b.close()
+
+
+def test_push_compositor_class_sequential_emulation(cuda_device):
+    """P2PPushCompositor itself (collective set-up over the in-process endpoint, march_targets, composite
+    with its flag waits and the signal into rank 0's frame), driven for R ranks sharing cuda:0 in the only
+    safe order: every rank's push march, then ranks R-1 .. 1's blends, then rank 0's (whose wait for every
+    block's done flag is then satisfied).  Frames must equal local marches + one composite, byte for byte."""
+    from paper_2501_01628_b200.p2p import P2PPushCompositor
+    from paper_2501_01628_b200.transport import run_collective
+
+    P, W, H = 4, 144, 104
+    s = c1(P=P, W=W, H=H)
+    d = cuda_device
+    comps = run_collective(P, lambda ep: P2PPushCompositor(ep, W, H, d, _emulated=True), device=d)
+    assert all(c.ok for c in comps)
+    bricks = [dev.DeviceBrick(s.dec.brick(r), d).generate(s.field) for r in range(P)]
+    dtf = dev.DeviceTF(s.tf, d)
+    bb = s.field.bounds()
+    cams = [s.cam] + [orbit_camera(bb.center(), 1.25 * bb.diagonal(), math.radians(50.0 * k), math.radians(-10.0),
+                                   45.0, W / H) for k in range(1, 4)]
+    for cam in cams:
+        order = s.dec.visibility_order(cam.position)
+        bands = _bands(s.dec, cam, W, H)
+        for r in range(P):
+            row_start, dst, fl, counter, epoch = comps[r].march_targets()
+            dev.march_push(bricks[r], cam, dtf, s.dt, s.ert, W, H, row_start, dst, fl, counter, epoch, band_clear=True)
+        outs = {r: comps[r].composite(order, s.background, bands=bands) for r in list(range(1, P)) + [0]}
+        assert all(outs[r].rgb8 is None for r in range(1, P))
+        got = outs[0].rgb8.cpu().numpy().copy()
+        parts = []
+        for r in range(P):
+            part = torch.empty(H * W * 4, dtype=torch.float32, device=d)
+            dev.march(bricks[r], cam, dtf, s.dt, s.ert, part, W, H)
+            parts.append(part)
+        ref = torch.empty(H * W * 3, dtype=torch.uint8, device=d)
+        dev.composite([parts[o] for o in order], s.background, rgb8=ref)
+        assert np.array_equal(got, ref.view(H, W, 3).cpu().numpy())
+        assert comps[1].last_bytes > 0
+    torch.cuda.synchronize()
+    for c in comps:
+        c.close()
+    for b in bricks:
+        b.close()
