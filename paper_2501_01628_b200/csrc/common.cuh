@@ -37,6 +37,10 @@ constexpr int kMaxTf = 1024;       // transfer-function entries held in shared m
 #define DPRT_SKIP_CAP 15
 #endif
 constexpr int kSkipCap = DPRT_SKIP_CAP;  // Chebyshev skip distances are capped at this many macrocells
+#ifndef DPRT_SKIP_OCTANT
+#define DPRT_SKIP_OCTANT 1  // the beam marcher's per-lane probe jumps by one-sided (octant) distances
+#endif
+constexpr int kSkipGrids = 9;  // symmetric + 8 octants
 constexpr float kHalfQuadRange = 8.0f;  // fp16 quads (DPRT_BRICK_HALF_QUADS) take field values within +-8
 
 struct DeviceBrick {
@@ -51,8 +55,10 @@ struct DeviceBrick {
     int64_t qd[3];     // quad grid dims = sd + 2 (one apron voxel on every side)
     int64_t mcd[3];    // macrocell grid dims
     float2* macro;     // per macrocell (min, max) over its dilated voxel range
-    uint8_t* skipd;    // per macrocell Chebyshev distance to the nearest non-empty macrocell (TF-dependent)
-    uint8_t* skip_tmp; // scratch for the separable distance passes
+    uint8_t* skipd;    // kSkipGrids grids of nmc bytes (TF-dependent): [0] per macrocell Chebyshev distance to
+                       // the nearest non-empty macrocell; [1 + o] the same restricted to octant o of directions
+                       // (bit i of o: + along axis i), which a ray moving into octant o may jump by
+    uint8_t* skip_tmp; // scratch for the separable distance passes (2 x kSkipGrids x nmc)
     uint64_t skip_version;  // tf_version the skip distances were built for (0 = never)
     float4* rays;      // ray queue scratch (2 float4 per pixel of the largest frame marched so far)
     long long ray_cap; // pixels the queue can hold
@@ -82,7 +88,8 @@ struct MarchArgs {
     int wide;                         // >= 2^31 apron quads: unsigned offsets from the apron base (kWide)
     int deep;                         // large brick: the memory-latency-bound configuration (kDeepUnroll)
     int half_quads;                   // quads stored as 4 x fp16 (DPRT_BRICK_HALF_QUADS)
-    const uint8_t* __restrict__ skipd;
+    const uint8_t* __restrict__ skipd;  // the symmetric grid; octant o's at skipd + (1 + o) * skip_n
+    long long skip_n;                   // macrocells per grid
     int mcd[3];
     int skip;
     int band_clear;  // clear only the footprint's row band of the partial (DPRT_MARCH_BAND_CLEAR)

@@ -639,6 +639,11 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         float ist[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) ist[i] = st[i] != 0.f ? 1.f / st[i] : 0.f;
+        // this ray's skip distances: the one-sided grid of its direction octant (a zero component may take
+        // either side: the ray stays in its layer, which both boxes contain)
+        const uint8_t* __restrict__ skipl =
+            DPRT_SKIP_OCTANT ? skipd + (1 + (st[0] > 0.f ? 1 : 0) + (st[1] > 0.f ? 2 : 0) + (st[2] > 0.f ? 4 : 0)) * a.skip_n
+                             : skipd;
 #endif
         int j = 0;
         float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
@@ -675,7 +680,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 const int mx = fl2cell(fmaf(fj, st[0], p0[0]), chx) >> kMacroShift;
                 const int my = fl2cell(fmaf(fj, st[1], p0[1]), chy) >> kMacroShift;
                 const int mz = fl2cell(fmaf(fj, st[2], p0[2]), chz) >> kMacroShift;
-                const int dist = (int)__ldg(skipd + (mz * mcd1 + my) * mcd0 + mx);
+                const int dist = (int)__ldg(skipl + (mz * mcd1 + my) * mcd0 + mx);
 #if DPRT_PROBE_LOOP
                 if (dist == 0) break;
                 {
@@ -973,9 +978,19 @@ __global__ void skip_classify_kernel(const float2* __restrict__ macro, long long
     }
 }
 
-__global__ void skip_pass_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int n0, int n1, int n2,
-                                 int axis) {
+// One separable pass of the distance transform for grid g = blockIdx.y: out = min over t of max(t, in) along
+// `axis`, t steps towards both sides for the symmetric grid (g = 0) and only towards the octant's side for
+// g = 1 + o (bit `axis` of o set: +).  The octant distance D(m) = min over non-empty c in the forward octant
+// of max_i |c_i - m_i|: the box from m spanning D macrocells forward on every axis is empty, so a ray
+// moving into that octant may jump to the box's exit (exact; the probe uses the same exit formula).
+__global__ void skip_pass_kernel(const uint8_t* __restrict__ in, long long in_grid_stride, uint8_t* __restrict__ out,
+                                 long long out_grid_stride, int n0, int n1, int n2, int axis) {
     const long long total = (long long)n0 * n1 * n2;
+    const int g = blockIdx.y;
+    const uint8_t* gin = in + g * in_grid_stride;
+    uint8_t* gout = out + g * out_grid_stride;
+    const bool both = g == 0;
+    const int sgn = ((g - 1) >> axis) & 1 ? 1 : -1;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const int x = (int)(i % n0);
@@ -984,12 +999,16 @@ __global__ void skip_pass_kernel(const uint8_t* __restrict__ in, uint8_t* __rest
         const int c = axis == 0 ? x : (axis == 1 ? y : z);
         const int n = axis == 0 ? n0 : (axis == 1 ? n1 : n2);
         const long long stride = axis == 0 ? 1 : (axis == 1 ? n0 : (long long)n0 * n1);
-        int best = in[i];
+        int best = gin[i];
         for (int k = 1; k < best && k < kSkipCap; ++k) {
-            if (c - k >= 0) best = min(best, max(k, (int)in[i - k * stride]));
-            if (c + k < n) best = min(best, max(k, (int)in[i + k * stride]));
+            if (both) {
+                if (c - k >= 0) best = min(best, max(k, (int)gin[i - k * stride]));
+                if (c + k < n) best = min(best, max(k, (int)gin[i + k * stride]));
+            } else if (c + sgn * k >= 0 && c + sgn * k < n) {
+                best = min(best, max(k, (int)gin[i + sgn * k * stride]));
+            }
         }
-        out[i] = (uint8_t)best;
+        gout[i] = (uint8_t)best;
     }
 }
 
@@ -998,11 +1017,17 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
     const int block = 256;
     const long long want = (nmc + block - 1) / block;
     const int grid = (int)(want < 148LL * 16 ? (want > 0 ? want : 1) : 148LL * 16);
+    const int ng = DPRT_SKIP_OCTANT ? kSkipGrids : 1;
+    uint8_t* t1 = tmp;
+    uint8_t* t2 = tmp + nmc * kSkipGrids;
+    const int m0 = (int)b.mcd[0], m1 = (int)b.mcd[1], m2 = (int)b.mcd[2];
+    // emptiness (0 or the cap) into grid 0, then z, y, x passes for every grid at once; the z pass reads the
+    // same emptiness for all grids (input grid stride 0) and the x pass writes the final grids
     skip_classify_kernel<<<grid, block, 0, stream>>>(b.macro, nmc, a.tf, a.n_tf, a.vmin, a.tf_scale, b.skipd);
-    skip_pass_kernel<<<grid, block, 0, stream>>>(b.skipd, tmp, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 2);
-    skip_pass_kernel<<<grid, block, 0, stream>>>(tmp, b.skipd, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 1);
-    skip_pass_kernel<<<grid, block, 0, stream>>>(b.skipd, tmp, (int)b.mcd[0], (int)b.mcd[1], (int)b.mcd[2], 0);
-    return cudaMemcpyAsync(b.skipd, tmp, (size_t)nmc, cudaMemcpyDeviceToDevice, stream);
+    skip_pass_kernel<<<dim3(grid, ng), block, 0, stream>>>(b.skipd, 0, t1, nmc, m0, m1, m2, 2);
+    skip_pass_kernel<<<dim3(grid, ng), block, 0, stream>>>(t1, nmc, t2, nmc, m0, m1, m2, 1);
+    skip_pass_kernel<<<dim3(grid, ng), block, 0, stream>>>(t2, nmc, b.skipd, nmc, m0, m1, m2, 0);
+    return cudaGetLastError();
 }
 
 cudaError_t read_counters(unsigned long long out[4], int reset) {
