@@ -879,6 +879,20 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
 #if DPRT_COUNTERS == 1
                     c_shade += m != 0.f;
                     c_contrib += w > 0.f;
+#elif DPRT_COUNTERS == 3
+                    // shaded samples by their macrocell: [0] all, [1] in an empty macrocell, [2] contributing,
+                    // [3] non-contributing in a non-empty macrocell
+                    if (m != 0.f) {
+                        const float fs = fj + (float)u;
+                        const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
+                        const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
+                        const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                        const bool empty = __ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) > 0;
+                        ++c_shade;
+                        c_contrib += empty;
+                        c_skip += w > 0.f;
+                        c_rays += !empty && !(w > 0.f);
+                    }
 #endif
                     if constexpr (kMark) {
                         if (m != 0.f) {
@@ -913,6 +927,20 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
 #if DPRT_COUNTERS == 1
                     c_shade += m != 0.f;
                     c_contrib += w > 0.f;
+#elif DPRT_COUNTERS == 3
+                    // shaded samples by their macrocell: [0] all, [1] in an empty macrocell, [2] contributing,
+                    // [3] non-contributing in a non-empty macrocell
+                    if (m != 0.f) {
+                        const float fs = fj + (float)u;
+                        const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
+                        const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
+                        const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                        const bool empty = __ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) > 0;
+                        ++c_shade;
+                        c_contrib += empty;
+                        c_skip += w > 0.f;
+                        c_rays += !empty && !(w > 0.f);
+                    }
 #endif
                     if constexpr (kMark) {
                         if (m != 0.f) {
