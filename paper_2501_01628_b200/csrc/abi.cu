@@ -161,6 +161,8 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     }
     b->vox = nullptr;
     b->macro = nullptr;
+    b->sub = nullptr;
+    b->subm = nullptr;
     b->skipd = nullptr;
     b->skip_tmp = nullptr;
     b->skip_version = 0;
@@ -174,11 +176,15 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
         e = cudaMalloc(&b->quad, (size_t)nq * (b->half_quads ? sizeof(uint2) : sizeof(float4)));
     if (e == cudaSuccess) e = cudaMalloc(&b->counters, (2 * DPRT_MARCH_COUNTER_SLOTS + 1) * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
+    if (DPRT_SUBBLOCK && e == cudaSuccess) e = cudaMalloc(&b->sub, (size_t)nmc * 8 * sizeof(float2));
+    if (DPRT_SUBBLOCK && e == cudaSuccess) e = cudaMalloc(&b->subm, (size_t)nmc);
     if (e == cudaSuccess) e = cudaMalloc(&b->skipd, (size_t)nmc * dprt::kSkipGrids);
     if (e == cudaSuccess) e = cudaMalloc(&b->skip_tmp, (size_t)nmc * 2 * dprt::kSkipGrids);
     if (e != cudaSuccess) {
         cudaFree(b->vox);
         cudaFree(b->macro);
+        cudaFree(b->sub);
+        cudaFree(b->subm);
         cudaFree(b->skipd);
         cudaFree(b->skip_tmp);
         cudaFree(b->counters);
@@ -261,6 +267,8 @@ int dprt_brick_destroy(DprtBrick* b) {
     if (rc) return rc;
     cudaFree(b->vox);
     cudaFree(b->macro);
+    cudaFree(b->sub);
+    cudaFree(b->subm);
     cudaFree(b->skipd);
     cudaFree(b->skip_tmp);
     cudaFree(b->rays);
@@ -438,6 +446,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.deep = ((long long)b->sd[0] * b->sd[1] * b->sd[2] >= (1LL << 28) || (p->flags & DPRT_MARCH_DEEP)) ? 1 : 0;
     a.skipd = b->skipd;
     a.skip_n = (long long)b->mcd[0] * b->mcd[1] * b->mcd[2];
+    a.subm = b->subm;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.band_clear = (p->flags & DPRT_MARCH_BAND_CLEAR) ? 1 : 0;
     a.accum = (p->flags & DPRT_MARCH_ACCUM) ? 1 : 0;

@@ -123,6 +123,33 @@ __global__ void macrocell_kernel(const float* __restrict__ vox, long long sd0, l
     macro[((long long)mz * mc1 + my) * mc0 + mx] = make_float2(lo, hi);
 }
 
+// The eight 4^3-cell sub-blocks of every macrocell: (min, max) over the sub-block's voxels dilated by one
+// voxel, like the macrocell's (the TF classifies them per version into the sub-block masks).
+__global__ void subblock_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
+                                int mc0, int mc1, int mc2, float2* __restrict__ sub) {
+    const int sx = blockIdx.x * blockDim.x + threadIdx.x;  // sub-block grid: 2 per macrocell per axis
+    const int sy = blockIdx.y, sz = blockIdx.z;
+    if (sx >= 2 * mc0) return;
+    constexpr int kS = kMacro / 2;
+    const long long x0 = max(0LL, (long long)sx * kS - 1), x1 = min(sd0 - 1, (long long)sx * kS + kS + 1);
+    const long long y0 = max(0LL, (long long)sy * kS - 1), y1 = min(sd1 - 1, (long long)sy * kS + kS + 1);
+    const long long z0 = max(0LL, (long long)sz * kS - 1), z1 = min(sd2 - 1, (long long)sz * kS + kS + 1);
+    float lo = INFINITY, hi = -INFINITY;
+    if (x0 <= x1 && y0 <= y1 && z0 <= z1) {
+        for (long long z = z0; z <= z1; ++z)
+            for (long long y = y0; y <= y1; ++y) {
+                const float* row = vox + (z * sd1 + y) * sd0;
+                for (long long x = x0; x <= x1; ++x) {
+                    const float v = __ldg(row + x);
+                    lo = fminf(lo, v);
+                    hi = fmaxf(hi, v);
+                }
+            }
+    }
+    const long long mc = ((long long)(sz >> 1) * mc1 + (sy >> 1)) * mc0 + (sx >> 1);
+    sub[mc * 8 + ((sx & 1) | ((sy & 1) << 1) | ((sz & 1) << 2))] = make_float2(lo, hi);
+}
+
 // Coefficient quads: the slot of voxel (x, y, z) holds the bilinear coefficients of the
 // z-face of the cell it anchors, {a, b - a, c - a, d - c - b + a} for the corners a = v(x, y), b = v(x+1, y),
 // c = v(x, y+1), d = v(x+1, y+1), so a face value is a + B fx + C fy + D fx fy (3 FFMA) and a trilinear
@@ -180,6 +207,11 @@ cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream) {
     dim3 grid((unsigned)((b.mcd[0] + 63) / 64), (unsigned)b.mcd[1], (unsigned)b.mcd[2]);
     macrocell_kernel<<<grid, block, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], (int)b.mcd[0], (int)b.mcd[1],
                                                  (int)b.mcd[2], b.macro);
+    if (DPRT_SUBBLOCK) {
+        dim3 sgrid((unsigned)((2 * b.mcd[0] + 63) / 64), (unsigned)(2 * b.mcd[1]), (unsigned)(2 * b.mcd[2]));
+        subblock_kernel<<<sgrid, block, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], (int)b.mcd[0],
+                                                     (int)b.mcd[1], (int)b.mcd[2], b.sub);
+    }
     return cudaGetLastError();
 }
 

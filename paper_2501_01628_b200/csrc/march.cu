@@ -683,17 +683,44 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             if (live && a.skip) {
 #endif
                 const float fj = (float)j;
-                const int mx = fl2cell(fmaf(fj, st[0], p0[0]), chx) >> kMacroShift;
-                const int my = fl2cell(fmaf(fj, st[1], p0[1]), chy) >> kMacroShift;
-                const int mz = fl2cell(fmaf(fj, st[2], p0[2]), chz) >> kMacroShift;
+                const int cx = fl2cell(fmaf(fj, st[0], p0[0]), chx);
+                const int cy = fl2cell(fmaf(fj, st[1], p0[1]), chy);
+                const int cz = fl2cell(fmaf(fj, st[2], p0[2]), chz);
+                const int mx = cx >> kMacroShift, my = cy >> kMacroShift, mz = cz >> kMacroShift;
+                const int mci = (mz * mcd1 + my) * mcd0 + mx;
 #if DPRT_PROBE_PREFETCH
                 // the first probe of an iteration may have been loaded during the previous slab step
-                const int dist = pf >= 0 ? pf : (int)__ldg(skipl + (mz * mcd1 + my) * mcd0 + mx);
+#if DPRT_SUBBLOCK == 2
+                const unsigned smask = __ldg(a.subm + mci);  // issued with (not after) the distance load
+#endif
+                const int dist = pf >= 0 ? pf : (int)__ldg(skipl + mci);
                 pf = -1;
 #else
-                const int dist = (int)__ldg(skipl + (mz * mcd1 + my) * mcd0 + mx);
+                const int dist = (int)__ldg(skipl + mci);
 #endif
-#if DPRT_PROBE_LOOP
+#if DPRT_PROBE_LOOP && DPRT_SUBBLOCK
+                if (dist == 0) {
+                    // a non-empty macrocell: is this sample's 4^3 sub-block empty too?  Then jump to its exit
+                    // (the sub-block is the empty box; exact like the macrocell jump)
+                    const int sbit = ((cx >> (kMacroShift - 1)) & 1) | (((cy >> (kMacroShift - 1)) & 1) << 1) |
+                                     (((cz >> (kMacroShift - 1)) & 1) << 2);
+#if DPRT_SUBBLOCK == 2
+                    if ((smask >> sbit) & 1) break;
+#else
+                    if ((__ldg(a.subm + mci) >> sbit) & 1) break;
+#endif
+                    constexpr int kSub = kMacroShift - 1;
+                    const float sx = ((float)(((cx >> kSub) + (st[0] > 0.f ? 1 : 0)) << kSub) - p0[0]) * ist[0];
+                    const float sy = ((float)(((cy >> kSub) + (st[1] > 0.f ? 1 : 0)) << kSub) - p0[1]) * ist[1];
+                    const float sz = ((float)(((cz >> kSub) + (st[2] > 0.f ? 1 : 0)) << kSub) - p0[2]) * ist[2];
+                    const float se = fminf(fminf(sx, sy), sz);
+                    j = se < (float)nn ? max((int)ceilf(se), j + 1) : nn;
+                    if (j >= nn) live = false;
+                    samp = live;
+                    continue;
+                }
+                {
+#elif DPRT_PROBE_LOOP
                 if (dist == 0) break;
                 {
 #else
@@ -1032,6 +1059,41 @@ __global__ void skip_classify_kernel(const float2* __restrict__ macro, long long
     }
 }
 
+// Sub-block masks (DPRT_SUBBLOCK): bit b of a macrocell's byte = its 4^3 sub-block b may map to alpha > 0
+// (the same conservative test as skip_classify_kernel, on the sub-block's dilated range).
+__global__ void sub_classify_kernel(const float2* __restrict__ sub, long long nmc, const float4* __restrict__ tf,
+                                    int n_tf, float vmin, float tf_scale, uint8_t* __restrict__ out) {
+    __shared__ int s_next_nz[kMaxTf];
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        int carry = n_tf;
+        for (int base = ((n_tf - 1) / 32) * 32; base >= 0; base -= 32) {
+            const int i = base + tid;
+            const bool nz = i < n_tf && tf[i].w > 0.0f;
+            const unsigned m = __ballot_sync(0xffffffffu, nz);
+            const unsigned here = m & (0xffffffffu << tid);
+            if (i < n_tf) s_next_nz[i] = here ? base + __ffs(here) - 1 : carry;
+            const int lowest = m ? base + __ffs(m) - 1 : carry;
+            carry = __shfl_sync(0xffffffffu, lowest, 0);
+        }
+    }
+    __syncthreads();
+    const float top = (float)(n_tf - 1);
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < nmc; i += (long long)gridDim.x * blockDim.x) {
+        unsigned mask = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const float2 mm = sub[i * 8 + b];
+            const float xl = fminf(fmaxf((mm.x - vmin) * tf_scale, 0.f), top);
+            const float xh = fminf(fmaxf((mm.y - vmin) * tf_scale, 0.f), top);
+            const int il = max((int)xl - 1, 0);
+            const int ih = min((int)xh + 2, n_tf - 1);
+            if (!(s_next_nz[il] > ih) && mm.x <= mm.y) mask |= 1u << b;
+        }
+        out[i] = (uint8_t)mask;
+    }
+}
+
 // One separable pass of the distance transform for grid g = blockIdx.y: out = min over t of max(t, in) along
 // `axis`, t steps towards both sides for the symmetric grid (g = 0) and only towards the octant's side for
 // g = 1 + o (bit `axis` of o set: +).  The octant distance D(m) = min over non-empty c in the forward octant
@@ -1081,6 +1143,7 @@ cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t*
     skip_pass_kernel<<<dim3(grid, ng), block, 0, stream>>>(b.skipd, 0, t1, nmc, m0, m1, m2, 2);
     skip_pass_kernel<<<dim3(grid, ng), block, 0, stream>>>(t1, nmc, t2, nmc, m0, m1, m2, 1);
     skip_pass_kernel<<<dim3(grid, ng), block, 0, stream>>>(t2, nmc, b.skipd, nmc, m0, m1, m2, 0);
+    if (DPRT_SUBBLOCK) sub_classify_kernel<<<grid, block, 0, stream>>>(b.sub, nmc, a.tf, a.n_tf, a.vmin, a.tf_scale, b.subm);
     return cudaGetLastError();
 }
 
