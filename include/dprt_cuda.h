@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 9
+#define DPRT_ABI_VERSION 10
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -280,8 +280,12 @@ int dprt_trace_any(int device, const DprtBvh* bvh, int64_t n, const double* org,
  * (cudaHostAlloc / torch pin_memory); bytes <= 1 MiB. */
 int dprt_stage_input(int device, void* dst_dev, const void* src_pinned, uint64_t bytes, void* stream);
 
-/* Stream-ordered helpers for the host driver (no torch types): device sync. */
+/* Stream-ordered helpers for the host driver (no torch types): device sync; a pitched 2-D copy between
+ * device and (pinned) host memory -- `rows` rows of `width_bytes`, row pitches in bytes -- used to read back
+ * only the footprint rectangle of a frame whose outside pixels the host buffer already holds. */
 int dprt_device_synchronize(int device);
+int dprt_copy_2d(int device, void* dst, uint64_t dst_pitch, const void* src, uint64_t src_pitch, uint64_t width_bytes,
+                 uint64_t rows, void* stream);
 
 #ifdef __cplusplus
 }

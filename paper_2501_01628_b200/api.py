@@ -320,7 +320,9 @@ class FrameResult:
     def array(self) -> np.ndarray:
         if self._pixels is not None:
             return np.frombuffer(self._pixels, np.uint8).reshape(self.height, self.width, 3)
-        return self._host().numpy()
+        a = self._host().numpy()
+        a.flags.writeable = False  # the pinned buffer is reused: later read-backs rely on its bytes
+        return a
 
     @property
     def pixels(self) -> bytes:

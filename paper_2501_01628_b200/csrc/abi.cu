@@ -760,6 +760,19 @@ int dprt_stage_input(int device, void* dst_dev, const void* src_pinned, uint64_t
     return DPRT_OK;
 }
 
+int dprt_copy_2d(int device, void* dst, uint64_t dst_pitch, const void* src, uint64_t src_pitch, uint64_t width_bytes,
+                 uint64_t rows, void* stream) {
+    if (rows == 0 || width_bytes == 0) return DPRT_OK;
+    if (!dst || !src) return fail(DPRT_E_USAGE, "null copy pointer");
+    if (width_bytes > dst_pitch || width_bytes > src_pitch) return fail(DPRT_E_USAGE, "copy width exceeds a row pitch");
+    int rc = bind(device);
+    if (rc) return rc;
+    CK(cudaMemcpy2DAsync(dst, (size_t)dst_pitch, src, (size_t)src_pitch, (size_t)width_bytes, (size_t)rows,
+                         cudaMemcpyDefault, (cudaStream_t)stream),
+       "dprt_copy_2d");
+    return DPRT_OK;
+}
+
 int dprt_device_alloc(int device, uint64_t bytes, void** out_ptr) {
     if (!out_ptr || bytes == 0) return fail(DPRT_E_USAGE, "bad allocation request");
     *out_ptr = nullptr;

@@ -550,6 +550,14 @@ def composite_signal(device_index: int, ptrs: Sequence[int], npix: int, backgrou
     _lib.check(rc, "dprt_composite_signal")
 
 
+def copy_2d(device_index: int, dst: int, dst_pitch: int, src: int, src_pitch: int, width_bytes: int, rows: int,
+            stream: Optional[int] = None) -> None:
+    """dprt_copy_2d: ``rows`` rows of ``width_bytes`` between device and pinned host memory, stream ordered."""
+    s = ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream(device_index).cuda_stream)
+    _lib.check(_lib.lib().dprt_copy_2d(device_index, ctypes.c_void_p(dst), dst_pitch, ctypes.c_void_p(src), src_pitch,
+                                       width_bytes, rows, s), "dprt_copy_2d")
+
+
 def enable_peer(device_index: int, peer_index: int) -> None:
     """NVLink peer access from ``device_index`` to ``peer_index`` (idempotent; TransportError if impossible)."""
     _lib.check(_lib.lib().dprt_enable_peer(device_index, peer_index), "dprt_enable_peer")

@@ -218,6 +218,8 @@ class VolumeRenderer:
         self._lane_next = 0
         self._band_key = None
         self._band_cache = None
+        self._host_keys = {}  # host frame buffer -> (W, H, background) of the full frame it last received
+        self.d2h_bytes = 0    # bytes render_to_host has copied device -> host so far (its read-back traffic)
 
     def set_tf(self, tf: TransferFunction1D) -> None:
         # marches of frames still in flight on lane streams may read the old table: the current stream (the
@@ -486,8 +488,35 @@ class VolumeRenderer:
             ready = torch.cuda.Event()
             ready.record(main)
         self._copy_stream.wait_event(ready)
+        # one rank: every pixel outside the brick's footprint rectangle is the tone-mapped background, written
+        # by the march itself.  A host buffer that received a full frame of this size and background holds the
+        # background everywhere outside the rectangles written since (FrameResult.array is read-only), so only
+        # the bounding box of those and this frame's rectangle crosses PCIe
+        region = None
+        key = (width, height, tuple(self.background))
+        ent = self._host_keys.get(host.data_ptr())
+        fused = self.ep.R == 1 and res.partial is None
+        rect = dev.desc_footprint(self.brick.desc, cam, width, height) if fused else None
+        if fused and ent is not None and ent[0] is host and ent[1] == key:
+            d = ent[2]
+            region = (min(d[0], rect[0]), min(d[1], rect[1]), max(d[2], rect[2]), max(d[3], rect[3]))
         with torch.cuda.stream(self._copy_stream):
-            host.copy_(res.rgb8, non_blocking=True)
+            if region is not None:
+                x0, y0, x1, y1 = region
+                if x1 > x0 and y1 > y0:
+                    dev.copy_2d(self.device.index, host.data_ptr() + 3 * (y0 * width + x0), 3 * width,
+                                res.rgb8.data_ptr() + 3 * (y0 * width + x0), 3 * width, 3 * (x1 - x0), y1 - y0,
+                                stream=self._copy_stream.cuda_stream)
+                    self.d2h_bytes += 3 * (x1 - x0) * (y1 - y0)
+                # the rendered rectangle alone keeps non-background bytes: the next copy covers it
+                ent[2] = rect
+            else:
+                host.copy_(res.rgb8, non_blocking=True)
+                self.d2h_bytes += host.numel()
+                if fused:
+                    if len(self._host_keys) >= 8:  # a bounded set of recently used host buffers
+                        self._host_keys.pop(next(iter(self._host_keys)))
+                    self._host_keys[host.data_ptr()] = [host, key, tuple(rect)]
         done = torch.cuda.Event()
         done.record(self._copy_stream)
         if self._fused_frames is not None and res.rgb8 is self._fused_frames[self._fused_slot]:

@@ -114,3 +114,33 @@ def test_frames_in_flight_argument_checks(cuda_device):
     with pytest.raises(UsageError, match="slot"):
         dev.march_rgb8(brick, cam, r.dtf, 1.0, 0.99, BG, frame, 32, 32, lane=torch.cuda.Stream(cuda_device), slot=0)
     brick.close()
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_reused_host_buffers_get_whole_frames(cuda_device, n):
+    """render_to_host into reused host buffers copies only the footprint rectangle (and the rectangles written
+    since the last full copy) -- the rest already holds the background.  Across zooming / orbiting cameras
+    whose rectangles grow, shrink and move, a background change and a camera inside the brick (full-frame
+    rectangle), every host frame must equal the device frame byte for byte."""
+    import math
+
+    f = blob_field((97, 89, 81), seed=6)
+    dec = decompose(f, 1)
+    W, H = 320, 200
+    brick = dev.DeviceBrick(dec.brick(0), cuda_device).generate(f)
+    r = VolumeRenderer(SoloEndpoint(cuda_device), brick, dec, default_tf(), BG)
+    bb = f.bounds()
+    hosts = [torch.empty((H, W, 3), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    cams = [orbit_camera(bb.center(), (1.0 + 0.6 * (k % 4)) * bb.diagonal(), math.radians(23.0 * k),
+                         math.radians(12.0), 40.0, W / H) for k in range(12)]
+    cams.insert(6, orbit_camera(bb.center(), 0.2 * bb.diagonal(), 0.3, 0.1, 60.0, W / H))  # eye inside the brick
+    for k, cam in enumerate(cams):
+        if k == 8:
+            r.background = (0.3, 0.2, 0.1)
+        hf = r.render_to_host(cam, W, H, hosts[k % 2], RenderOptions(frames_in_flight=n), verify=False)
+        got = hf.wait().numpy().copy()
+        hf.result.wait_ready() if hf.result.ready is not None else None
+        want = hf.result.rgb8.cpu().numpy()
+        assert np.array_equal(got, want), f"frame {k}"
+    r.join()
+    brick.close()
