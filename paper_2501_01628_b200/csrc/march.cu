@@ -376,6 +376,10 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #ifndef DPRT_PROBE_LOOP
 #define DPRT_PROBE_LOOP 1  // per-lane probe loops over consecutive empty cubes (0: one jump per warp iteration)
 #endif
+#if !DPRT_BEAM_PROBE
+#undef DPRT_PROBE_PREFETCH
+#define DPRT_PROBE_PREFETCH 0  // the prefetch feeds the per-lane probe
+#endif
 #ifndef DPRT_PROBE_PREFETCH
 #define DPRT_PROBE_PREFETCH 1  // the next probe's skip distance loaded during the slab step (c2 -0.6 %, config 3 -1 %)
 #endif
@@ -626,17 +630,22 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         const float rx = __shfl_sync(FULL, st[0], ref), ry = __shfl_sync(FULL, st[1], ref), rz = __shfl_sync(FULL, st[2], ref);
         const float ax = fabsf(rx), ay = fabsf(ry), az = fabsf(rz);
         const int ka = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
-        const int kb = ka == 0 ? 1 : 0, kc = ka == 2 ? 1 : 2;
         // this ray's components permuted to (a, b, c) once, so the loops below index no arrays
         auto sel = [&](const float* v, int k3) { return k3 == 0 ? v[0] : (k3 == 1 ? v[1] : v[2]); };
-        const float sa = sel(st, ka), sb = sel(st, kb), sc = sel(st, kc);
-        const float pa = sel(p0, ka), pb = sel(p0, kb), pc = sel(p0, kc);
+        const float sa = sel(st, ka);
+        const float pa = sel(p0, ka);
         const int cha = ka == 0 ? chx : (ka == 1 ? chy : chz);
+        const bool pos = (ka == 0 ? rx : (ka == 1 ? ry : rz)) > 0.f;
+#if !DPRT_BEAM_PROBE
+        // beam-wide slab skipping (the measured alternative) bounds the beam's cells on the other two axes
+        const int kb = ka == 0 ? 1 : 0, kc = ka == 2 ? 1 : 2;
+        const float sb = sel(st, kb), sc = sel(st, kc);
+        const float pb = sel(p0, kb), pc = sel(p0, kc);
         const int chb = kb == 0 ? chx : (kb == 1 ? chy : chz);
         const int chc = kc == 0 ? chx : (kc == 1 ? chy : chz);
-        const bool pos = (ka == 0 ? rx : (ka == 1 ? ry : rz)) > 0.f;
         const bool ok = nn == 0 || ((sa > 0.f) == pos && sa != 0.f && fabsf(sb) <= fabsf(sa) && fabsf(sc) <= fabsf(sa));
         const bool dominant = __all_sync(FULL, ok);  // multi-slab jumps need |st_b|, |st_c| <= |st_a| on all rays
+#endif
         const float isa = sa != 0.f ? 1.f / sa : 0.f;
 #if DPRT_BEAM_PROBE
         float ist[3];
