@@ -173,7 +173,7 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
     b->half_quads = (desc->flags & DPRT_BRICK_HALF_QUADS) ? 1 : 0;
     cudaError_t e = cudaMalloc(&b->vox, (size_t)nvox * sizeof(float));
     if (e == cudaSuccess)  // 16 B per apron-grid voxel (8 B with fp16 quads)
-        e = cudaMalloc(&b->quad, (size_t)nq * (b->half_quads ? sizeof(uint2) : sizeof(float4)));
+        e = cudaMalloc(&b->quad, (size_t)nq * (b->half_quads ? sizeof(uint2) : dprt::kQuadSlot * sizeof(float4)));
     if (e == cudaSuccess) e = cudaMalloc(&b->counters, (2 * DPRT_MARCH_COUNTER_SLOTS + 1) * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc(&b->macro, (size_t)nmc * sizeof(float2));
     if (DPRT_SUBBLOCK && e == cudaSuccess) e = cudaMalloc(&b->sub, (size_t)nmc * 8 * sizeof(float2));
@@ -438,7 +438,8 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.qsx = DPRT_QUAD_YFAST ? (int)b->qd[1] : 1;
     a.qsy = DPRT_QUAD_YFAST ? 1 : (int)b->qd[0];
     a.qsz = (int)(b->qd[0] * b->qd[1]);
-    a.qorg = b->quad + a.qsz + a.qsy + a.qsx;  // fp16 quads: reinterpreted as uint2 at the same element offsets
+    // fp16 quads: reinterpreted as uint2 at the same element offsets; f32 octets: two float4 per slot
+    a.qorg = b->quad + (long long)(b->half_quads ? 1 : dprt::kQuadSlot) * (a.qsz + a.qsy + a.qsx);
     a.half_quads = b->half_quads;
     a.wide = ((long long)b->qd[0] * b->qd[1] * b->qd[2] >= (1LL << 31) || (p->flags & DPRT_MARCH_WIDE)) ? 1 : 0;
     // bricks of >= 2^28 stored voxels (4.3 GB of quads; c3's 1026^3 bricks, not c2's 513^3) touch far more

@@ -19,6 +19,12 @@
 // 128-byte lines (c2 host replay: 13.6 -> 9.4 lines per load).  Measured (round 2): c2 0.2270 -> 0.2286 ms,
 // config 3 even rank 5 0.774 -> 0.752, mass rank 7 0.543 -> 0.546 -- line count is not what bounds the
 // loads (profiles/r02_variant_memory_side.json), so x-fastest stays.
+// Coefficient octets (DPRT_QUAD_OCTET): the slot of a voxel holds both z-faces of its cell (32 bytes), one
+// 256-bit load per sample instead of two 128-bit ones (f32 quads only; fp16 quads keep one face per slot).
+#ifndef DPRT_QUAD_OCTET
+#define DPRT_QUAD_OCTET 0
+#endif
+
 #ifndef DPRT_QUAD_YFAST
 #define DPRT_QUAD_YFAST 0
 #endif
@@ -29,6 +35,7 @@ namespace dprt {
 #define DPRT_MACRO_SHIFT 3
 #endif
 constexpr int kMacroShift = DPRT_MACRO_SHIFT;
+constexpr int kQuadSlot = DPRT_QUAD_OCTET ? 2 : 1;  // float4s per f32 quad slot
 constexpr int kMacro = 1 << kMacroShift;  // macrocell edge in cells (empty-space skipping granularity)
 constexpr int kTileX = 16;         // marcher CTA screen tile: 16 x 16 pixels, warps are 8 x 4 pixel tiles
 constexpr int kTileY = 16;

@@ -188,7 +188,17 @@ __global__ void quad_kernel(const float* __restrict__ vox, long long sd0, long l
         reinterpret_cast<uint2*>(quad)[qi] = make_uint2(*reinterpret_cast<const unsigned*>(&ab),
                                                         *reinterpret_cast<const unsigned*>(&cd));
     } else {
+#if DPRT_QUAD_OCTET
+        // the cell's far z-face too: the quad the next apron layer would hold
+        const long long zf = cl(qz, sd2);
+        const float* s0 = vox + (zf * sd1 + y0) * sd0;
+        const float* s1 = vox + (zf * sd1 + y1) * sd0;
+        const float e = s0[x0], f = s0[x1], g = s1[x0], h = s1[x1];
+        quad[2 * qi] = make_float4(a, b - a, c - a, (d - c) - (b - a));
+        quad[2 * qi + 1] = make_float4(e, f - e, g - e, (h - g) - (f - e));
+#else
         quad[qi] = make_float4(a, b - a, c - a, (d - c) - (b - a));
+#endif
     }
 }
 

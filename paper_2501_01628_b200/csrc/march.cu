@@ -214,6 +214,13 @@ __device__ __forceinline__ T quad_offset(T ix, T iy, T iz, T qsx, T qsy, T qsz) 
 #endif
 }
 
+// f32 coefficient octet (DPRT_QUAD_OCTET): both z-faces of the cell in one 256-bit load.
+__device__ __forceinline__ void load_octet(const float4* p, float4& qa, float4& qb) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(qa.x), "=f"(qa.y), "=f"(qa.z), "=f"(qa.w), "=f"(qb.x), "=f"(qb.y), "=f"(qb.z), "=f"(qb.w)
+        : "l"(p));
+}
+
 // DPRT_BOUNDS_CHECK builds trap on a quad index (relative to qorg, both loads) outside the apron grid.
 __device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, long long qi) {
 #if DPRT_BOUNDS_CHECK
@@ -346,9 +353,15 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             // trilinear + TF (§2.6) + front-to-back blend (§2.7) of one sample
             const int qi = quad_offset(ix, iy, iz, qsx, qsy, qsz);
             quad_bounds_check(a, qi);
-            const float4* q = qorg + qi;
             const float fx = __saturatef(ux - (float)ix), fy = __saturatef(uy - (float)iy);
+#if DPRT_QUAD_OCTET
+            float4 oa, ob;
+            load_octet(qorg + 2 * (long long)qi, oa, ob);
+            const float v = trilerp(oa, ob, fx, fy, fx * fy, __saturatef(uz - (float)iz));
+#else
+            const float4* q = qorg + qi;
             const float v = trilerp(__ldg(q), __ldg(q + qsz), fx, fy, fx * fy, __saturatef(uz - (float)iz));
+#endif
             tf_blend(s_tf, s_tf + a.n_tf, v, tns, tno, top, C0, C1, C2, A);
             ++j;
             if (A >= ert) j = nn;  // early ray termination: the next step finishes the ray
@@ -556,7 +569,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
     const float4* __restrict__ qorg = a.qorg;
     const float4* __restrict__ qorg1 = a.qorg + a.qsz;  // the cell's far z-face
     const unsigned qk = (unsigned)a.qsz + (unsigned)a.qsy + (unsigned)a.qsx;  // apron offset of stored voxel (0, 0, 0)
-    const float4* __restrict__ qbase = a.qorg - qk;            // the apron grid's first quad (kWide)
+    const float4* __restrict__ qbase = a.qorg - (long long)(kHalf ? 1 : kQuadSlot) * qk;  // the apron grid's first slot (kWide)
     const float4* __restrict__ qbase1 = qbase + a.qsz;
     const uint2* __restrict__ hq_org = reinterpret_cast<const uint2*>(qbase) + qk;  // fp16 quads: 8-byte slots
     const int qsx = a.qsx, qsy = a.qsy, qsz = a.qsz;
@@ -875,8 +888,12 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                         if constexpr (kHalf) {
                             load_half_quads(reinterpret_cast<const uint2*>(qbase) + qu, qsz, qa[u], qb[u]);
                         } else {
+#if DPRT_QUAD_OCTET
+                            load_octet(qbase + 2 * (unsigned long long)qu, qa[u], qb[u]);
+#else
                             qa[u] = __ldg(qbase + qu);
                             qb[u] = __ldg(qbase1 + qu);
+#endif
                         }
                     } else {
                         const int qi = quad_offset(ix, iy, iz, qsx, qsy, qsz);
@@ -884,8 +901,12 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                         if constexpr (kHalf) {
                             load_half_quads(hq_org + qi, qsz, qa[u], qb[u]);
                         } else {
+#if DPRT_QUAD_OCTET
+                            load_octet(qorg + 2 * (long long)qi, qa[u], qb[u]);
+#else
                             qa[u] = __ldg(qorg + qi);
                             qb[u] = __ldg(qorg1 + qi);
+#endif
                         }
                     }
                     wx[u] = __saturatef(ux - (float)ix);
