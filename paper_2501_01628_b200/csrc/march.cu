@@ -400,7 +400,11 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #define DPRT_JUMP_BRANCHFREE 1
 #endif
 #ifndef DPRT_SLAB_SHIFT
-#define DPRT_SLAB_SHIFT DPRT_MACRO_SHIFT  // slab thickness (cells, log2) of the probe-mode beam step
+#if DPRT_BEAM_PROBE
+#define DPRT_SLAB_SHIFT (DPRT_MACRO_SHIFT + 1)  // slab thickness (cells, log2): 16 since the probe loop (c2 -4 %)
+#else
+#define DPRT_SLAB_SHIFT DPRT_MACRO_SHIFT  // beam-wide skipping steps whole macrocell layers
+#endif
 #endif
 constexpr int kSlabShift = DPRT_SLAB_SHIFT;
 
