@@ -8,7 +8,6 @@ reference's exception classes (errors.py); there is no CPU path.
 from __future__ import annotations
 
 import ctypes
-import itertools
 import os
 from typing import Optional, Sequence, Tuple
 
@@ -215,14 +214,26 @@ def field_mass_function(f: FieldSpec, device: torch.device, tau: float, chunk: i
     return mass
 
 
-_TF_VERSIONS = itertools.count(1)
+def skip_key(tf: TransferFunction1D) -> int:
+    """The bricks' TF-dependent skip distances depend on the TF only through which entries have alpha > 0,
+    the entry count and the value range (skip_classify_kernel): a nonzero 63-bit digest of exactly those,
+    used as the ABI's tf_version -- editing colours or scaling opacities keeps the distances, changing the
+    alpha support rebuilds them."""
+    import hashlib
+
+    a = np.ascontiguousarray(tf.as_f32().reshape(-1, 4)[:, 3] > 0.0)
+    h = hashlib.blake2b(digest_size=8)
+    h.update(np.array([tf.n], np.int64).tobytes())
+    h.update(np.array([tf.vmin, tf.vmax], np.float64).tobytes())
+    h.update(np.packbits(a).tobytes())
+    return (int.from_bytes(h.digest(), "little") & ((1 << 63) - 1)) | 1
 
 
 class DeviceTF:
     """A transfer function table resident on one device (4 KiB for 256 entries).
 
-    ``version`` tags the table contents for the bricks' cached skip distances; ``update`` re-uploads
-    and bumps it only when the contents change.  Uploads from a pinned staging buffer alternate between
+    ``version`` tags what the bricks' cached skip distances depend on (``skip_key``: the alpha support and
+    the value range); ``update`` re-uploads the table and recomputes the tag when the contents change.  Uploads from a pinned staging buffer alternate between
     two device tables and run on a side stream (``dprt_stage_input``, SM-driven): frame k's table is
     staged while frame k-1 still marches out of the other one, and the march of frame k waits on it."""
 
@@ -230,7 +241,7 @@ class DeviceTF:
         self.tf = tf
         self._host = tf.as_f32().reshape(-1).copy()
         self.table = torch.from_numpy(self._host.copy()).to(device)
-        self.version = next(_TF_VERSIONS)
+        self.version = skip_key(tf)
         self._tables = None        # the two staging targets (allocated on the first staged update)
         self._slot = 0
         self._side = None          # side stream for the staging copies
@@ -251,7 +262,7 @@ class DeviceTF:
         host = tf.as_f32().reshape(-1)
         if host.shape != self._host.shape or not np.array_equal(host, self._host) or (
                 tf.vmin, tf.vmax) != (self.tf.vmin, self.tf.vmax):
-            self.version = next(_TF_VERSIONS)
+            self.version = skip_key(tf)
             self._host = host.copy()
             if host.shape[0] != self.table.numel():
                 # lane marches may still read the old table: the current stream (its allocator's reuse

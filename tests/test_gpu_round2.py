@@ -230,3 +230,37 @@ def test_skipping_is_bit_exact_in_every_octant(cuda_device, seed):
                     dev.march(b, cam, dtf, 0.7, 0.99, n, W, H, skip=False, force_deep=deep)
                     assert torch.equal(a, n), (P, r, cam, deep)
             b.close()
+
+
+def test_skip_cache_follows_alpha_support(cuda_device):
+    """The bricks cache their skip distances per skip_key (alpha support + value range): an edit that only
+    scales opacities or recolours keeps the key (no rebuild) and a support change gets a new one; in every
+    case the frame equals a fresh renderer's frame for the new TF, byte for byte."""
+    from paper_2501_01628_b200.device import skip_key
+    from paper_2501_01628_b200.engine import VolumeRenderer
+    from paper_2501_01628_b200.transport import SoloEndpoint
+    from paper_2501_01628_b200.volume import TransferFunction1D
+
+    f = blob_field((90, 80, 70), seed=8)
+    dec = decompose(f, 1)
+    W, H = 200, 150
+    cam = auto_camera(f.bounds(), W, H)
+    base = default_tf()
+    t = base.as_f32().copy()
+    scaled = TransferFunction1D(np.column_stack([t[:, :3][:, ::-1], 0.5 * t[:, 3]]).astype(np.float32), base.vmin,
+                                base.vmax)
+    shifted = default_tf(threshold=0.35)
+    assert skip_key(scaled) == skip_key(base) != skip_key(shifted)
+    b = dev.DeviceBrick(dec.brick(0), cuda_device).generate(f)
+    r = VolumeRenderer(SoloEndpoint(cuda_device), b, dec, base, (0.1, 0.1, 0.1))
+    r.render(cam, W, H)
+    for tf in (scaled, shifted, base):
+        r.dtf.update(tf)
+        r.tf = tf
+        got = r.render(cam, W, H).rgb8.clone()
+        fresh = VolumeRenderer(SoloEndpoint(cuda_device), b, dec, tf, (0.1, 0.1, 0.1))
+        fresh.dtf.version = 0  # tf_version 0: rebuild the skip distances on this call
+        want = fresh.render(cam, W, H).rgb8
+        assert torch.equal(got, want)
+    torch.cuda.synchronize()
+    b.close()
