@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define DPRT_ABI_VERSION 10
+#define DPRT_ABI_VERSION 11
 
 /* status codes -> Python exceptions (errors.py:4-29) */
 #define DPRT_OK 0
@@ -133,6 +133,9 @@ int dprt_device_count(int* n);
  * ((stored dims + 2) per axis, multiplied); DPRT_E_USAGE beyond that. */
 int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out);
 int dprt_brick_stored(const DprtBrick* b, int64_t stored_lo[3], int64_t stored_dims[3]);
+/* The brick's macrocell edge (empty-space skipping granularity) as log2 cells: 2 (4^3) for bricks of < 2^28
+ * stored voxels, 3 (8^3) for larger ones. */
+int dprt_brick_macro_shift(const DprtBrick* b, int32_t* shift);
 int dprt_brick_upload(DprtBrick* b, const float* src, int src_is_device, void* stream);
 int dprt_brick_download(const DprtBrick* b, float* dst, int dst_is_device, void* stream);
 int dprt_brick_generate(DprtBrick* b, const DprtFieldSpec* spec, void* stream);

@@ -15,7 +15,7 @@ from typing import Optional
 from .errors import DeviceError, NativeLibraryMissing, TransportError, UsageError
 
 LIB_PATH = Path(__file__).resolve().parent / "libdprt_cuda.so"
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 DPRT_OK = 0
 DPRT_E_USAGE = -1
@@ -48,7 +48,7 @@ EXPORTS = (
     "dprt_enable_peer", "dprt_device_alloc", "dprt_device_free", "dprt_march_counters", "dprt_kat_slab", "dprt_kat_primary_dirs",
     "dprt_stage_input", "dprt_composite_ranged", "dprt_desc_footprint", "dprt_march_stats",
     "dprt_trace_nearest", "dprt_trace_any", "dprt_march_push", "dprt_wait_flags", "dprt_composite_signal",
-    "dprt_copy_2d",
+    "dprt_copy_2d", "dprt_brick_macro_shift",
 )
 MAX_PUSH = 16  # DPRT_MAX_PUSH
 SIGNAL_COUNTER_WORDS = 1056  # DPRT_SIGNAL_COUNTER_WORDS
@@ -134,6 +134,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "dprt_march_push": ([P, P, P, P, P, I, I, P], I),
         "dprt_wait_flags": ([I, P, I, ctypes.c_uint32, P], I),
         "dprt_composite_signal": ([I, P, P, I, ctypes.c_int64, P, I, P, P, P, P, I, ctypes.c_uint32, P], I),
+        "dprt_brick_macro_shift": ([P, P], I),
         "dprt_copy_2d": ([I, P, ctypes.c_uint64, P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, P], I),
     }
     for name, (args, res) in sig.items():

@@ -20,7 +20,7 @@ struct BvhArgs;
 cudaError_t launch_trace(const BvhArgs& b, long long n, const double* org, const double* dirn, const double* tmin,
                          const double* tmax, double* best_t, int64_t* best_id, uint8_t* occluded, cudaStream_t stream);
 cudaError_t launch_march_mark(const MarchArgs& a, cudaStream_t stream);
-cudaError_t launch_mark_reduce(const uint8_t* mark, const int mcd[3], const int cells[3], unsigned long long* out,
+cudaError_t launch_mark_reduce(const uint8_t* mark, const int mcd[3], const int cells[3], int mshift, unsigned long long* out,
                                cudaStream_t stream);
 cudaError_t launch_skip_build(const DeviceBrick& b, const MarchArgs& a, uint8_t* tmp, cudaStream_t stream);
 cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cudaStream_t stream);
@@ -153,10 +153,17 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
         if (hi > desc->dims[a] - 1) hi = desc->dims[a] - 1;
         b->s_lo[a] = lo;
         b->sd[a] = hi - lo + 1;
-        b->mcd[a] = (b->sd[a] - 1 + dprt::kMacro - 1) / dprt::kMacro;
+        b->mcd[a] = 0;  // below, once the macrocell size is chosen
         b->qd[a] = b->sd[a] + 2;
         nvox *= b->sd[a];
         nq *= b->qd[a];
+        nmc *= b->mcd[a];
+    }
+    b->mshift = (nvox >= (1LL << 28) || !DPRT_BEAM_PROBE) ? dprt::kMacroShift : DPRT_MACRO_SHIFT_SMALL;
+    nmc = 1;
+    for (int a = 0; a < 3; ++a) {
+        const long long m = 1LL << b->mshift;
+        b->mcd[a] = (b->sd[a] - 1 + m - 1) / m;
         nmc *= b->mcd[a];
     }
     b->vox = nullptr;
@@ -193,6 +200,12 @@ int dprt_brick_create(int device, const DprtBrickDesc* desc, DprtBrick** out) {
         return cuda_fail(e, "brick allocation");
     }
     *out = b;
+    return DPRT_OK;
+}
+
+int dprt_brick_macro_shift(const DprtBrick* b, int32_t* shift) {
+    if (!b || !shift) return fail(DPRT_E_USAGE, "null brick or output");
+    *shift = b->mshift;
     return DPRT_OK;
 }
 
@@ -447,6 +460,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     a.deep = ((long long)b->sd[0] * b->sd[1] * b->sd[2] >= (1LL << 28) || (p->flags & DPRT_MARCH_DEEP)) ? 1 : 0;
     a.skipd = b->skipd;
     a.skip_n = (long long)b->mcd[0] * b->mcd[1] * b->mcd[2];
+    a.mshift = b->mshift;
     a.subm = b->subm;
     a.skip = (p->flags & DPRT_MARCH_NO_SKIP) ? 0 : 1;
     a.band_clear = (p->flags & DPRT_MARCH_BAND_CLEAR) ? 1 : 0;
@@ -537,7 +551,7 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     if (e == cudaSuccess) e = dprt::launch_march_mark(a, st);
     const int mcd[3] = {(int)b->mcd[0], (int)b->mcd[1], (int)b->mcd[2]};
     const int cells[3] = {(int)(b->sd[0] - 1), (int)(b->sd[1] - 1), (int)(b->sd[2] - 1)};
-    if (e == cudaSuccess) e = dprt::launch_mark_reduce(mark, mcd, cells, cnt + 2, st);
+    if (e == cudaSuccess) e = dprt::launch_mark_reduce(mark, mcd, cells, b->mshift, cnt + 2, st);
     unsigned long long h[4] = {0, 0, 0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -34,7 +34,16 @@ namespace dprt {
 #ifndef DPRT_MACRO_SHIFT
 #define DPRT_MACRO_SHIFT 3
 #endif
-constexpr int kMacroShift = DPRT_MACRO_SHIFT;
+// Macrocell edge per brick (DeviceBrick::mshift): large bricks (>= 2^28 stored voxels, memory-latency bound)
+// keep 8^3 macrocells; smaller ones (issue / L1 bound, where every skipped sample counts) use 4^3 -- c2 -4.7 %,
+// config 3's mass-balanced slowest brick +1.5 % with 4^3 (profiles/r02_variant_memory_side.json).
+#ifndef DPRT_BEAM_PROBE
+#define DPRT_BEAM_PROBE 1  // per-lane skip probes (0: the measured beam-wide alternative, 8^3 macrocells only)
+#endif
+#ifndef DPRT_MACRO_SHIFT_SMALL
+#define DPRT_MACRO_SHIFT_SMALL 2
+#endif
+constexpr int kMacroShift = DPRT_MACRO_SHIFT;  // the large-brick (and upper-bound) macrocell shift
 constexpr int kQuadSlot = DPRT_QUAD_OCTET ? 2 : 1;  // float4s per f32 quad slot
 constexpr int kMacro = 1 << kMacroShift;  // macrocell edge in cells (empty-space skipping granularity)
 constexpr int kTileX = 16;         // marcher CTA screen tile: 16 x 16 pixels, warps are 8 x 4 pixel tiles
@@ -64,6 +73,7 @@ struct DeviceBrick {
     int half_quads;
     int64_t qd[3];     // quad grid dims = sd + 2 (one apron voxel on every side)
     int64_t mcd[3];    // macrocell grid dims
+    int mshift;        // macrocell edge = 1 << mshift cells (chosen by brick size at creation)
     float2* macro;     // per macrocell (min, max) over its dilated voxel range
     float2* sub;       // per macrocell, its eight 4^3-cell sub-blocks' dilated (min, max) (bit b: x, y, z halves)
     uint8_t* subm;     // per macrocell, bit b set = sub-block b is not empty under the current TF
@@ -102,6 +112,7 @@ struct MarchArgs {
     int half_quads;                   // quads stored as 4 x fp16 (DPRT_BRICK_HALF_QUADS)
     const uint8_t* __restrict__ skipd;  // the symmetric grid; octant o's at skipd + (1 + o) * skip_n
     long long skip_n;                   // macrocells per grid
+    int mshift;                         // the brick's macrocell shift (DeviceBrick::mshift)
     const uint8_t* __restrict__ subm;   // per macrocell: non-empty 4^3 sub-blocks (DPRT_SUBBLOCK)
     int mcd[3];
     int skip;

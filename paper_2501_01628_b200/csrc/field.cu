@@ -103,13 +103,14 @@ cudaError_t launch_generate(const DeviceBrick& b, const DprtFieldSpec& spec, cud
 // taken over the 1-voxel dilation [8m - 1, 8m + 9] so that samples whose f32 position rounds across a
 // macrocell face are still bounded by it (skipping is exact, not approximate).
 __global__ void macrocell_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
-                                 int mc0, int mc1, int mc2, float2* __restrict__ macro) {
+                                 int mc0, int mc1, int mc2, int mshift, float2* __restrict__ macro) {
     const int mx = blockIdx.x * blockDim.x + threadIdx.x;
     const int my = blockIdx.y, mz = blockIdx.z;
     if (mx >= mc0) return;
-    const long long x0 = max(0LL, (long long)mx * kMacro - 1), x1 = min(sd0 - 1, (long long)mx * kMacro + kMacro + 1);
-    const long long y0 = max(0LL, (long long)my * kMacro - 1), y1 = min(sd1 - 1, (long long)my * kMacro + kMacro + 1);
-    const long long z0 = max(0LL, (long long)mz * kMacro - 1), z1 = min(sd2 - 1, (long long)mz * kMacro + kMacro + 1);
+    const long long m = 1LL << mshift;  // macrocell edge in cells
+    const long long x0 = max(0LL, (long long)mx * m - 1), x1 = min(sd0 - 1, (long long)mx * m + m + 1);
+    const long long y0 = max(0LL, (long long)my * m - 1), y1 = min(sd1 - 1, (long long)my * m + m + 1);
+    const long long z0 = max(0LL, (long long)mz * m - 1), z1 = min(sd2 - 1, (long long)mz * m + m + 1);
     float lo = INFINITY, hi = -INFINITY;
     for (long long z = z0; z <= z1; ++z)
         for (long long y = y0; y <= y1; ++y) {
@@ -126,11 +127,11 @@ __global__ void macrocell_kernel(const float* __restrict__ vox, long long sd0, l
 // The eight 4^3-cell sub-blocks of every macrocell: (min, max) over the sub-block's voxels dilated by one
 // voxel, like the macrocell's (the TF classifies them per version into the sub-block masks).
 __global__ void subblock_kernel(const float* __restrict__ vox, long long sd0, long long sd1, long long sd2,
-                                int mc0, int mc1, int mc2, float2* __restrict__ sub) {
+                                int mc0, int mc1, int mc2, int mshift, float2* __restrict__ sub) {
     const int sx = blockIdx.x * blockDim.x + threadIdx.x;  // sub-block grid: 2 per macrocell per axis
     const int sy = blockIdx.y, sz = blockIdx.z;
     if (sx >= 2 * mc0) return;
-    constexpr int kS = kMacro / 2;
+    const long long kS = 1LL << (mshift - 1);
     const long long x0 = max(0LL, (long long)sx * kS - 1), x1 = min(sd0 - 1, (long long)sx * kS + kS + 1);
     const long long y0 = max(0LL, (long long)sy * kS - 1), y1 = min(sd1 - 1, (long long)sy * kS + kS + 1);
     const long long z0 = max(0LL, (long long)sz * kS - 1), z1 = min(sd2 - 1, (long long)sz * kS + kS + 1);
@@ -216,11 +217,11 @@ cudaError_t launch_macrocells(const DeviceBrick& b, cudaStream_t stream) {
     dim3 block(64);
     dim3 grid((unsigned)((b.mcd[0] + 63) / 64), (unsigned)b.mcd[1], (unsigned)b.mcd[2]);
     macrocell_kernel<<<grid, block, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], (int)b.mcd[0], (int)b.mcd[1],
-                                                 (int)b.mcd[2], b.macro);
+                                                 (int)b.mcd[2], b.mshift, b.macro);
     if (DPRT_SUBBLOCK) {
         dim3 sgrid((unsigned)((2 * b.mcd[0] + 63) / 64), (unsigned)(2 * b.mcd[1]), (unsigned)(2 * b.mcd[2]));
         subblock_kernel<<<sgrid, block, 0, stream>>>(b.vox, b.sd[0], b.sd[1], b.sd[2], (int)b.mcd[0],
-                                                     (int)b.mcd[1], (int)b.mcd[2], b.sub);
+                                                     (int)b.mcd[1], (int)b.mcd[2], b.mshift, b.sub);
     }
     return cudaGetLastError();
 }

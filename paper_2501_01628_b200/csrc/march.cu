@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
     const int qsx = a.qsx, qsy = a.qsy, qsz = a.qsz;
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1], skip = a.skip;
+    const int ms = a.mshift;  // macrocell shift of this brick
     const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
 
     bool have = false, exhausted = false;
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
             const int ix = min(__float2int_rd(fmaxf(ux, 0.f)), chx);
             const int iy = min(__float2int_rd(fmaxf(uy, 0.f)), chy);
             const int iz = min(__float2int_rd(fmaxf(uz, 0.f)), chz);
-            const int mx = ix >> kMacroShift, my = iy >> kMacroShift, mz = iz >> kMacroShift;
+            const int mx = ix >> ms, my = iy >> ms, mz = iz >> ms;
             // Skip distance of this sample's macrocell.  An empty macrocell's sample would add exact
             // zeros: drop it and jump over the empty cube around it.
             const int mc = (mz * mcd1 + my) * mcd0 + mx;
@@ -338,11 +339,11 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
                 // jump to the exit of the empty cube of macrocells [m - dist + 1, m + dist]
                 float je = 3.0e38f;
                 if (st[0] != 0.f)
-                    je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0]);
+                    je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << ms) - p0[0]) * ist[0]);
                 if (st[1] != 0.f)
-                    je = fminf(je, ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << kMacroShift) - p0[1]) * ist[1]);
+                    je = fminf(je, ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << ms) - p0[1]) * ist[1]);
                 if (st[2] != 0.f)
-                    je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2]);
+                    je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << ms) - p0[2]) * ist[2]);
                 const int jn = je < (float)nn ? (int)ceilf(je) : nn;
                 j = jn > j ? jn : j + 1;
 #if DPRT_COUNTERS
@@ -383,9 +384,6 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 #define DPRT_BEAM_W 4
 #endif
 constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
-#ifndef DPRT_BEAM_PROBE
-#define DPRT_BEAM_PROBE 1
-#endif
 #ifndef DPRT_PROBE_LOOP
 #define DPRT_PROBE_LOOP 1  // per-lane probe loops over consecutive empty cubes (0: one jump per warp iteration)
 #endif
@@ -545,7 +543,10 @@ constexpr int kBeamBlock = DPRT_BEAM_BLOCK;  // threads per CTA (warps are indep
 // macrocells the march must read (the roofline's needed bytes) and the shaded-sample rate.
 // kPush: the fused march + exchange (dprt_march_push) -- partial pixels go to their row block owners' inboxes
 // and the launch's last CTA raises the owners' epoch flags.
-template <bool kWide, int kUnroll, int kMinBlocks, bool kHalf, bool kMark = false, bool kPush = false>
+// kMS: the macrocell shift as a compile-time constant for the natural pairing (small-brick configuration
+// with DPRT_MACRO_SHIFT_SMALL, large-brick configuration with DPRT_MACRO_SHIFT), 0 = read a.mshift at run
+// time (the forced test configurations and the diagnostic instantiation; ~1 % slower).
+template <bool kWide, int kUnroll, int kMinBlocks, bool kHalf, bool kMark = false, bool kPush = false, int kMS = 0>
 __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(const MarchArgs a) {
     extern __shared__ float4 s_tf[];
     const int tid = threadIdx.x;
@@ -579,6 +580,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
     const int qsx = a.qsx, qsy = a.qsy, qsz = a.qsz;
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1];
+    const int ms = kMS ? kMS : a.mshift;  // macrocell shift of this brick (4^3 or 8^3 cells)
     const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
     const float4* __restrict__ s_dtf = s_tf + a.n_tf;
 #if DPRT_COUNTERS
@@ -712,7 +714,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 const int cx = fl2cell(fmaf(fj, st[0], p0[0]), chx);
                 const int cy = fl2cell(fmaf(fj, st[1], p0[1]), chy);
                 const int cz = fl2cell(fmaf(fj, st[2], p0[2]), chz);
-                const int mx = cx >> kMacroShift, my = cy >> kMacroShift, mz = cz >> kMacroShift;
+                const int mx = cx >> ms, my = cy >> ms, mz = cz >> ms;
                 const int mci = (mz * mcd1 + my) * mcd0 + mx;
 #if DPRT_PROBE_PREFETCH
                 // the first probe of an iteration may have been loaded during the previous slab step
@@ -728,14 +730,14 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 if (dist == 0) {
                     // a non-empty macrocell: is this sample's 4^3 sub-block empty too?  Then jump to its exit
                     // (the sub-block is the empty box; exact like the macrocell jump)
-                    const int sbit = ((cx >> (kMacroShift - 1)) & 1) | (((cy >> (kMacroShift - 1)) & 1) << 1) |
-                                     (((cz >> (kMacroShift - 1)) & 1) << 2);
+                    const int sbit = ((cx >> (ms - 1)) & 1) | (((cy >> (ms - 1)) & 1) << 1) |
+                                     (((cz >> (ms - 1)) & 1) << 2);
 #if DPRT_SUBBLOCK == 2
                     if ((smask >> sbit) & 1) break;
 #else
                     if ((__ldg(a.subm + mci) >> sbit) & 1) break;
 #endif
-                    constexpr int kSub = kMacroShift - 1;
+                    const int kSub = ms - 1;
                     const float sx = ((float)(((cx >> kSub) + (st[0] > 0.f ? 1 : 0)) << kSub) - p0[0]) * ist[0];
                     const float sy = ((float)(((cy >> kSub) + (st[1] > 0.f ? 1 : 0)) << kSub) - p0[1]) * ist[1];
                     const float sz = ((float)(((cz >> kSub) + (st[2] > 0.f ? 1 : 0)) << kSub) - p0[2]) * ist[2];
@@ -756,18 +758,18 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     // exit of the empty cube along each axis, branch-free: an axis the ray does not move along
                     // has ist = 0 and so gives je = 0, which only shortens the jump to one sample (still exact;
                     // rays with an exactly zero direction component are rare)
-                    const float jx = ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0];
-                    const float jy = ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << kMacroShift) - p0[1]) * ist[1];
-                    const float jz = ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2];
+                    const float jx = ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << ms) - p0[0]) * ist[0];
+                    const float jy = ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << ms) - p0[1]) * ist[1];
+                    const float jz = ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << ms) - p0[2]) * ist[2];
                     const float je = fminf(fminf(jx, jy), jz);
 #else
                     float je = 3.0e38f;
                     if (st[0] != 0.f)
-                        je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << kMacroShift) - p0[0]) * ist[0]);
+                        je = fminf(je, ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << ms) - p0[0]) * ist[0]);
                     if (st[1] != 0.f)
-                        je = fminf(je, ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << kMacroShift) - p0[1]) * ist[1]);
+                        je = fminf(je, ((float)((st[1] > 0.f ? my + dist : my - dist + 1) << ms) - p0[1]) * ist[1]);
                     if (st[2] != 0.f)
-                        je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << kMacroShift) - p0[2]) * ist[2]);
+                        je = fminf(je, ((float)((st[2] > 0.f ? mz + dist : mz - dist + 1) << ms) - p0[2]) * ist[2]);
 #endif
                     j = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;
                     if (j >= nn) live = false;
@@ -809,9 +811,9 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     pf = 0;
                 } else if (a.skip && jend < nn) {
                     const float fe = (float)jend;
-                    const int ex = fl2cell(fmaf(fe, st[0], p0[0]), chx) >> kMacroShift;
-                    const int ey = fl2cell(fmaf(fe, st[1], p0[1]), chy) >> kMacroShift;
-                    const int ez = fl2cell(fmaf(fe, st[2], p0[2]), chz) >> kMacroShift;
+                    const int ex = fl2cell(fmaf(fe, st[0], p0[0]), chx) >> ms;
+                    const int ey = fl2cell(fmaf(fe, st[1], p0[1]), chy) >> ms;
+                    const int ez = fl2cell(fmaf(fe, st[2], p0[2]), chz) >> ms;
                     pf = (int)__ldg(skipl + (ez * mcd1 + ey) * mcd0 + ex);
                 }
 #endif
@@ -823,10 +825,10 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 const float f0 = (float)j, f1 = (float)(jend - 1);
                 const int ub0 = fl2cell(fmaf(f0, sb, pb), chb), ub1 = fl2cell(fmaf(f1, sb, pb), chb);
                 const int uc0 = fl2cell(fmaf(f0, sc, pc), chc), uc1 = fl2cell(fmaf(f1, sc, pc), chc);
-                b0 = min(ub0, ub1) >> kMacroShift;
-                b1 = max(ub0, ub1) >> kMacroShift;
-                c0 = min(uc0, uc1) >> kMacroShift;
-                c1 = max(uc0, uc1) >> kMacroShift;
+                b0 = min(ub0, ub1) >> ms;
+                b1 = max(ub0, ub1) >> ms;
+                c0 = min(uc0, uc1) >> ms;
+                c1 = max(uc0, uc1) >> ms;
             }
             const int B0 = __reduce_min_sync(FULL, b0), B1 = __reduce_max_sync(FULL, b1);
             const int Cc0 = __reduce_min_sync(FULL, c0), Cc1 = __reduce_max_sync(FULL, c1);
@@ -855,7 +857,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 c_skip += live;
 #endif
                 if (live && ksl == K) {
-                    const float face = (float)((pos ? K + jump : K - jump + 1) << kMacroShift);
+                    const float face = (float)((pos ? K + jump : K - jump + 1) << ms);
                     const float je = (face - pa) * isa;
                     j = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;
                     if (j >= nn) live = false;
@@ -945,9 +947,9 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     // [3] non-contributing in a non-empty macrocell
                     if (m != 0.f) {
                         const float fs = fj + (float)u;
-                        const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
-                        const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
-                        const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                        const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> ms;
+                        const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> ms;
+                        const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> ms;
                         const bool empty = __ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) > 0;
                         ++c_shade;
                         c_contrib += empty;
@@ -958,9 +960,9 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     if constexpr (kMark) {
                         if (m != 0.f) {
                             const float fs = fj + (float)u;
-                            const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
-                            const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
-                            const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                            const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> ms;
+                            const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> ms;
+                            const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> ms;
                             a.mark[((long long)mz * mcd1 + my) * mcd0 + mx] = 1;
                             ++m_shade;
                             m_contrib += w > 0.f;
@@ -993,9 +995,9 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     // [3] non-contributing in a non-empty macrocell
                     if (m != 0.f) {
                         const float fs = fj + (float)u;
-                        const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
-                        const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
-                        const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                        const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> ms;
+                        const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> ms;
+                        const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> ms;
                         const bool empty = __ldg(skipd + (mz * mcd1 + my) * mcd0 + mx) > 0;
                         ++c_shade;
                         c_contrib += empty;
@@ -1006,9 +1008,9 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     if constexpr (kMark) {
                         if (m != 0.f) {
                             const float fs = fj + (float)u;
-                            const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> kMacroShift;
-                            const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> kMacroShift;
-                            const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> kMacroShift;
+                            const int mx = fl2cell(fmaf(fs, st[0], p0[0]), chx) >> ms;
+                            const int my = fl2cell(fmaf(fs, st[1], p0[1]), chy) >> ms;
+                            const int mz = fl2cell(fmaf(fs, st[2], p0[2]), chz) >> ms;
                             a.mark[((long long)mz * mcd1 + my) * mcd0 + mx] = 1;
                             ++m_shade;
                             m_contrib += w > 0.f;
@@ -1246,26 +1248,23 @@ cudaError_t launch_march(const MarchArgs& a, cudaStream_t stream) {
         if (a.samples) e = cudaMemsetAsync(a.samples, 0, (size_t)a.npix_buf * sizeof(uint32_t), stream);
         if (e != cudaSuccess) return e;
         using K = void (*)(const MarchArgs);
-        const K kerns[2][2][2] = {  // [half][deep][wide]
-            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false>,
-              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false>},
-             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, false>,
-              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, false>}},
-            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true>,
-              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true>},
-             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, true>,
-              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, true>}}};
-        const K pushk[2][2][2] = {  // [half][deep][wide], dprt_march_push
-            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false, false, true>,
-              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, false, false, true>},
-             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, false, false, true>,
-              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, false, false, true>}},
-            {{march_beam_kernel<false, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true, false, true>,
-              march_beam_kernel<true, kBeamUnroll, DPRT_BEAM_MINBLOCKS, true, false, true>},
-             {march_beam_kernel<false, kDeepUnroll, kDeepBlocks, true, false, true>,
-              march_beam_kernel<true, kDeepUnroll, kDeepBlocks, true, false, true>}}};
+        constexpr int kSmallMS = DPRT_BEAM_PROBE ? DPRT_MACRO_SHIFT_SMALL : kMacroShift;
+        // [push][natural macro shift][half][deep][wide]
+#define DPRT_BEAM_K(H, D, W, P, N)                                                                           \
+    march_beam_kernel<W, (D) ? kDeepUnroll : kBeamUnroll, (D) ? kDeepBlocks : DPRT_BEAM_MINBLOCKS, H, false, P, \
+                      (N) ? ((D) ? kMacroShift : kSmallMS) : 0>
+#define DPRT_BEAM_K4(H, P, N) {{DPRT_BEAM_K(H, 0, false, P, N), DPRT_BEAM_K(H, 0, true, P, N)}, \
+                               {DPRT_BEAM_K(H, 1, false, P, N), DPRT_BEAM_K(H, 1, true, P, N)}}
+        static const K kerns[2][2][2][2][2] = {
+            {{DPRT_BEAM_K4(false, false, false), DPRT_BEAM_K4(true, false, false)},
+             {DPRT_BEAM_K4(false, false, true), DPRT_BEAM_K4(true, false, true)}},
+            {{DPRT_BEAM_K4(false, true, false), DPRT_BEAM_K4(true, true, false)},
+             {DPRT_BEAM_K4(false, true, true), DPRT_BEAM_K4(true, true, true)}}};
+#undef DPRT_BEAM_K4
+#undef DPRT_BEAM_K
         const int hq = a.half_quads ? 1 : 0, dp = a.deep ? 1 : 0, wd = a.wide ? 1 : 0;
-        const K kern = a.push_P ? pushk[hq][dp][wd] : kerns[hq][dp][wd];
+        const int natural = a.mshift == (a.deep ? kMacroShift : kSmallMS) ? 1 : 0;
+        const K kern = kerns[a.push_P ? 1 : 0][natural][hq][dp][wd];
         const size_t sm = a.push_P ? smem + (size_t)((a.H + 15) & ~15) : smem;  // + the row -> block table
         kern<<<grid_for((const void*)kern, kBeamBlock, sm), kBeamBlock, sm, stream>>>(a);
         return cudaGetLastError();
@@ -1293,7 +1292,8 @@ cudaError_t launch_march_mark(const MarchArgs& a, cudaStream_t stream) {
 // Sum over the marked macrocells of their cell counts (the f32 voxels a perfect marcher reads once) and the
 // number of marked macrocells.
 __global__ void mark_reduce_kernel(const uint8_t* __restrict__ mark, int m0, int m1, int m2, int c0, int c1, int c2,
-                                   unsigned long long* __restrict__ out) {
+                                   int mshift, unsigned long long* __restrict__ out) {
+    const long long kMacro = 1LL << mshift;
     unsigned long long cells = 0, n = 0;
     const long long total = (long long)m0 * m1 * m2;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -1315,9 +1315,10 @@ __global__ void mark_reduce_kernel(const uint8_t* __restrict__ mark, int m0, int
     }
 }
 
-cudaError_t launch_mark_reduce(const uint8_t* mark, const int mcd[3], const int cells[3], unsigned long long* out,
-                               cudaStream_t stream) {
-    mark_reduce_kernel<<<148 * 4, 256, 0, stream>>>(mark, mcd[0], mcd[1], mcd[2], cells[0], cells[1], cells[2], out);
+cudaError_t launch_mark_reduce(const uint8_t* mark, const int mcd[3], const int cells[3], int mshift,
+                               unsigned long long* out, cudaStream_t stream) {
+    mark_reduce_kernel<<<148 * 4, 256, 0, stream>>>(mark, mcd[0], mcd[1], mcd[2], cells[0], cells[1], cells[2], mshift,
+                                                    out);
     return cudaGetLastError();
 }
 

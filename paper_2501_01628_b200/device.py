@@ -163,6 +163,13 @@ class DeviceBrick:
         _lib.check(rc, "dprt_brick_download")
         return out
 
+    @property
+    def macro_shift(self) -> int:
+        """log2 of the macrocell edge in cells (2 or 3, by brick size; dprt_brick_macro_shift)."""
+        v = ctypes.c_int32()
+        _lib.check(_lib.lib().dprt_brick_macro_shift(self.handle, ctypes.byref(v)), "dprt_brick_macro_shift")
+        return int(v.value)
+
     def footprint(self, cam: CameraSpec, width: int, height: int):
         rect = (ctypes.c_int32 * 4)()
         c = camera_struct(cam)

@@ -69,6 +69,8 @@ def test_march_stats_needed_macrocells_match_host_restatement(cuda_device):
     desc = BrickDesc.whole(f, 1)
     b = dev.DeviceBrick(desc, cuda_device).generate(f)
     st = dev.march_stats(b, cam, dtf, 1.0, 2.0, W, H, skip=False)
+    ms = b.macro_shift
+    assert ms == 2  # a small brick: 4^3 macrocells
     ca = oracle.camera_array(cam.position, cam.view_dir, cam.up, cam.fov_y, cam.aspect)
     dirs = oracle.primary_dirs(ca, W, H).reshape(-1, 3)
     lo_w, hi_w = desc.box_world().lo, desc.box_world().hi
@@ -79,7 +81,7 @@ def test_march_stats_needed_macrocells_match_host_restatement(cuda_device):
         for k in range(k0, k0 + n):
             t = k * 1.0
             p = [cam.position[a] + t * d[a] for a in range(3)]
-            c = [min(max(int(np.floor(p[a])), 0), sd[a] - 2) >> 3 for a in range(3)]
+            c = [min(max(int(np.floor(p[a])), 0), sd[a] - 2) >> ms for a in range(3)]
             marked.add(tuple(c))
     # f32 positions may round across a macrocell face: allow a handful of boundary differences
     assert abs(st["macrocells"] - len(marked)) <= max(2, len(marked) // 50)
