@@ -50,7 +50,7 @@ constexpr int kTileX = 16;         // marcher CTA screen tile: 16 x 16 pixels, w
 constexpr int kTileY = 16;
 constexpr int kMaxTf = 1024;       // transfer-function entries held in shared memory
 #ifndef DPRT_SKIP_CAP
-#define DPRT_SKIP_CAP 15
+#define DPRT_SKIP_CAP 31
 #endif
 constexpr int kSkipCap = DPRT_SKIP_CAP;  // Chebyshev skip distances are capped at this many macrocells
 #ifndef DPRT_SKIP_OCTANT

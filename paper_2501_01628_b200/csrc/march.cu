@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kTileX * kTileY, DPRT_MARCH_MINBLOCKS) march_k
 // jumps every lane over the empty slabs at once or lets each lane shade its samples in the slab.  No
 // per-sample skip test, lanes stay in step, and the 32 rays read the same L1 lines.
 #ifndef DPRT_BEAM_UNROLL
-#define DPRT_BEAM_UNROLL 3  // 3 since the per-lane probe loop (c2 0.2236 -> 0.2163 ms; it was 4 before, 3 lost then)
+#define DPRT_BEAM_UNROLL 4  // re-swept after every traversal change (4 -> 3 with the probe loop, 3 -> 4 with 4^3 macrocells)
 #endif
 constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 
