@@ -440,6 +440,26 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
     owned_box(b, a.blo, a.bhi);
     a.half_w = cam->half_w;
     a.half_h = cam->half_h;
+    {
+        double ext = 0.0, dist = 0.0;
+        for (int i = 0; i < 3; ++i) {
+            ext += (a.bhi[i] - a.blo[i]) * (a.bhi[i] - a.blo[i]);
+            const double c = 0.5 * (a.blo[i] + a.bhi[i]) - cam->pos[i];
+            dist += c * c;
+        }
+        const double margin = 1e-3 * (1.0 + sqrt(ext) + sqrt(dist));
+        for (int i = 0; i < 3; ++i) {
+            a.mt_f[i] = (float)cam->fwd[i];
+            a.mt_r[i] = (float)cam->right[i];
+            a.mt_u[i] = (float)cam->up[i];
+            a.mt_lo[i] = (float)(a.blo[i] - cam->pos[i] - margin);
+            a.mt_hi[i] = (float)(a.bhi[i] - cam->pos[i] + margin);
+        }
+        a.mt_hw = (float)cam->half_w;
+        a.mt_hh = (float)cam->half_h;
+        a.mt_iw = (float)(1.0 / W);
+        a.mt_ih = (float)(1.0 / H);
+    }
     a.dt = p->dt;
     {
         int ex;
@@ -681,6 +701,26 @@ int dprt_kat_primary_dirs(int device, const DprtCamera* cam, int W, int H, doubl
     }
     a.half_w = cam->half_w;
     a.half_h = cam->half_h;
+    {
+        double ext = 0.0, dist = 0.0;
+        for (int i = 0; i < 3; ++i) {
+            ext += (a.bhi[i] - a.blo[i]) * (a.bhi[i] - a.blo[i]);
+            const double c = 0.5 * (a.blo[i] + a.bhi[i]) - cam->pos[i];
+            dist += c * c;
+        }
+        const double margin = 1e-3 * (1.0 + sqrt(ext) + sqrt(dist));
+        for (int i = 0; i < 3; ++i) {
+            a.mt_f[i] = (float)cam->fwd[i];
+            a.mt_r[i] = (float)cam->right[i];
+            a.mt_u[i] = (float)cam->up[i];
+            a.mt_lo[i] = (float)(a.blo[i] - cam->pos[i] - margin);
+            a.mt_hi[i] = (float)(a.bhi[i] - cam->pos[i] + margin);
+        }
+        a.mt_hw = (float)cam->half_w;
+        a.mt_hh = (float)cam->half_h;
+        a.mt_iw = (float)(1.0 / W);
+        a.mt_ih = (float)(1.0 / H);
+    }
     a.W = W;
     a.H = H;
     double* buf = nullptr;

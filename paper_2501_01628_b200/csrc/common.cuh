@@ -113,6 +113,10 @@ struct MarchArgs {
     const uint8_t* __restrict__ skipd;  // the symmetric grid; octant o's at skipd + (1 + o) * skip_n
     long long skip_n;                   // macrocells per grid
     int mshift;                         // the brick's macrocell shift (DeviceBrick::mshift)
+    // conservative f32 miss pre-test (DPRT_MISS_TEST): camera basis and the owned box relative to the eye,
+    // expanded by a margin far above f32 rounding; a ray missing that box misses the exact one
+    float mt_f[3], mt_r[3], mt_u[3], mt_lo[3], mt_hi[3];
+    float mt_hw, mt_hh, mt_iw, mt_ih;
     const uint8_t* __restrict__ subm;   // per macrocell: non-empty 4^3 sub-blocks (DPRT_SUBBLOCK)
     int mcd[3];
     int skip;

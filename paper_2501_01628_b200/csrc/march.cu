@@ -384,6 +384,9 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 #define DPRT_BEAM_W 4
 #endif
 constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
+#ifndef DPRT_MISS_TEST
+#define DPRT_MISS_TEST 0  // 1: warps whose rays all miss skip the f64 setup (measured +0.4 % c2, +1 % config 3)
+#endif
 #ifndef DPRT_PROBE_LOOP
 #define DPRT_PROBE_LOOP 1  // per-lane probe loops over consecutive empty cubes (0: one jump per warp iteration)
 #endif
@@ -617,6 +620,31 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
         int nn = 0, pix = 0;
         float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
         const bool inside = px < a.rect[2] && py < a.rect[3];
+#if DPRT_MISS_TEST
+        // conservative f32 pre-test against the owned box expanded by a margin: a warp all of whose rays miss
+        // it needs no exact f64 setup (their exact sample counts are 0); any other warp runs the exact setup
+        bool maybe = false;
+        if (inside) {
+            const float sxf = (((float)px + 0.5f) * a.mt_iw * 2.f - 1.f) * a.mt_hw;
+            const float syf = (1.f - ((float)py + 0.5f) * a.mt_ih * 2.f) * a.mt_hh;
+            float t0 = 0.f, t1 = 3.0e38f;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const float di = fmaf(syf, a.mt_u[i], fmaf(sxf, a.mt_r[i], a.mt_f[i]));
+                const float inv = 1.f / di;  // IEEE: a zero component gives +-inf, an inside slab then no bound
+                const float ta = a.mt_lo[i] * inv, tb = a.mt_hi[i] * inv;
+                t0 = fmaxf(t0, fminf(ta, tb));
+                t1 = fminf(t1, fmaxf(ta, tb));
+            }
+            maybe = !(t1 < t0);
+        }
+        if (!__any_sync(FULL, maybe)) {
+            if (inside) {
+                pix = py * a.W + px;
+                if (!kMark && a.samples) a.samples[pix - a.pix0] = 0u;
+            }
+        } else
+#endif
         if (inside) {
             // exact f64 ray setup for this lane's pixel, fused
             pix = py * a.W + px;
