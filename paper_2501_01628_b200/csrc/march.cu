@@ -408,6 +408,9 @@ constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW
 #endif
 #endif
 constexpr int kSlabShift = DPRT_SLAB_SHIFT;
+#ifndef DPRT_SLAB_SHIFT_DEEP
+#define DPRT_SLAB_SHIFT_DEEP DPRT_MACRO_SHIFT  // large bricks: 8-cell slabs (all 8 config-3 ranks: critical path -2 %)
+#endif
 
 // Tile-queue order: 1 = rows of tiles centre-out (default), 2 = rows and the tiles within a
 // row centre-out, 0 = row-major.  The queue then ends with the short rays at the footprint's top and bottom
@@ -584,6 +587,8 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
     const uint8_t* __restrict__ skipd = a.skipd;
     const int mcd0 = a.mcd[0], mcd1 = a.mcd[1];
     const int ms = kMS ? kMS : a.mshift;  // macrocell shift of this brick (4^3 or 8^3 cells)
+    constexpr bool kDeepCfg = kUnroll == kDeepUnroll && kMinBlocks == kDeepBlocks;
+    constexpr int kSS = (DPRT_BEAM_PROBE && kDeepCfg) ? DPRT_SLAB_SHIFT_DEEP : kSlabShift;  // slab thickness
     const float tns = a.tf_ns, tno = a.tf_no, top = (float)(a.n_tf - 1), ert = a.ert;
     const float4* __restrict__ s_dtf = s_tf + a.n_tf;
 #if DPRT_COUNTERS
@@ -820,14 +825,14 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
 #endif
             // current slab: the nearest (in the march direction) slab holding a sampling lane's next sample
             int ksl = 0;
-            if (samp) ksl = fl2cell(fmaf((float)j, sa, pa), cha) >> kSlabShift;
+            if (samp) ksl = fl2cell(fmaf((float)j, sa, pa), cha) >> kSS;
             const int key = samp ? (pos ? ksl : -ksl) : 0x7fffffff;
             const int kmin = __reduce_min_sync(FULL, key);
             const int K = pos ? kmin : -kmin;
             // this lane's samples in slab K: j .. jend-1 (first sample past the slab's far face)
             int jend = j;
             if (samp) {
-                const float face = (float)((pos ? K + 1 : K) << kSlabShift);
+                const float face = (float)((pos ? K + 1 : K) << kSS);
                 const float je = (face - pa) * isa;
                 jend = je < (float)nn ? max((int)ceilf(je), j + 1) : nn;  // >= 1 sample: progress
                 if (ksl != K) jend = j;  // this ray is not in slab K yet
