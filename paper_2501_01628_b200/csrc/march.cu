@@ -384,6 +384,9 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 #define DPRT_BEAM_W 4
 #endif
 constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
+#ifndef DPRT_BEAM_W_DEEP
+#define DPRT_BEAM_W_DEEP DPRT_BEAM_W  // the large-brick configuration's beam width
+#endif
 #ifndef DPRT_MISS_TEST
 #define DPRT_MISS_TEST 0  // 1: warps whose rays all miss skip the f64 setup (measured +0.4 % c2, +1 % config 3)
 #endif
@@ -574,7 +577,9 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
     const unsigned FULL = 0xffffffffu;
     const int lane = tid & 31;
     const int rw = a.rect[2] - a.rect[0], rh = a.rect[3] - a.rect[1];
-    const int tiles_x = (rw + kBeamW - 1) / kBeamW, tiles_y = (rh + kBeamH - 1) / kBeamH;
+    constexpr bool kDeepBeam = kUnroll == kDeepUnroll && kMinBlocks == kDeepBlocks;
+    constexpr int kBW = kDeepBeam ? DPRT_BEAM_W_DEEP : kBeamW, kBH = 32 / kBW;  // this configuration's beam
+    const int tiles_x = (rw + kBW - 1) / kBW, tiles_y = (rh + kBH - 1) / kBH;
     const int ntiles = tiles_x * tiles_y;
     const int chx = a.chi[0], chy = a.chi[1], chz = a.chi[2];
     const float4* __restrict__ qorg = a.qorg;
@@ -620,8 +625,8 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
 #else
         const int trow = tile / tiles_x, tcol = tile % tiles_x;
 #endif
-        const int px = a.rect[0] + tcol * kBeamW + (lane % kBeamW);
-        const int py = a.rect[1] + trow * kBeamH + (lane / kBeamW);
+        const int px = a.rect[0] + tcol * kBW + (lane % kBW);
+        const int py = a.rect[1] + trow * kBH + (lane / kBW);
         int nn = 0, pix = 0;
         float p0[3] = {0.f, 0.f, 0.f}, st[3] = {0.f, 0.f, 0.f};
         const bool inside = px < a.rect[2] && py < a.rect[3];
