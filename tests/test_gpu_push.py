@@ -125,7 +125,12 @@ def test_push_compositor_class_sequential_emulation(cuda_device):
     P, W, H = 4, 144, 104
     s = c1(P=P, W=W, H=H)
     d = cuda_device
-    comps = run_collective(P, lambda ep: P2PPushCompositor(ep, W, H, d, _emulated=True), device=d)
+    def make(ep):
+        c = P2PPushCompositor(ep, W, H, d, _emulated=True)
+        c._ensure_rgba()  # collective: the float RGBA gather target (keep_float frames)
+        return c
+
+    comps = run_collective(P, make, device=d)
     assert all(c.ok for c in comps)
     bricks = [dev.DeviceBrick(s.dec.brick(r), d).generate(s.field) for r in range(P)]
     dtf = dev.DeviceTF(s.tf, d)
@@ -138,17 +143,22 @@ def test_push_compositor_class_sequential_emulation(cuda_device):
         for r in range(P):
             row_start, dst, fl, counter, epoch = comps[r].march_targets()
             dev.march_push(bricks[r], cam, dtf, s.dt, s.ert, W, H, row_start, dst, fl, counter, epoch, band_clear=True)
-        outs = {r: comps[r].composite(order, s.background, bands=bands) for r in list(range(1, P)) + [0]}
+        kf = cam is cams[-1]  # the last frame also gathers the float RGBA (keep_float) into rank 0
+        outs = {r: comps[r].composite(order, s.background, keep_float=kf, bands=bands) for r in list(range(1, P)) + [0]}
         assert all(outs[r].rgb8 is None for r in range(1, P))
         got = outs[0].rgb8.cpu().numpy().copy()
+        got_rgba = outs[0].rgba.cpu().numpy().copy() if kf else None
         parts = []
         for r in range(P):
             part = torch.empty(H * W * 4, dtype=torch.float32, device=d)
             dev.march(bricks[r], cam, dtf, s.dt, s.ert, part, W, H)
             parts.append(part)
         ref = torch.empty(H * W * 3, dtype=torch.uint8, device=d)
-        dev.composite([parts[o] for o in order], s.background, rgb8=ref)
+        ref_rgba = torch.empty(H * W * 4, dtype=torch.float32, device=d)
+        dev.composite([parts[o] for o in order], s.background, rgb8=ref, rgba=ref_rgba)
         assert np.array_equal(got, ref.view(H, W, 3).cpu().numpy())
+        if kf:
+            assert np.array_equal(got_rgba, ref_rgba.cpu().numpy())
         assert comps[1].last_bytes > 0
     torch.cuda.synchronize()
     for c in comps:
