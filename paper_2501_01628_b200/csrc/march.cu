@@ -736,9 +736,10 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             if (lane == 0) ++c_shade;  // [0]: warp slab iterations (probe + slab step)
 #endif
 #if DPRT_BEAM_PROBE
-            // per-lane probe: a lane whose next sample sits in an empty macrocell jumps over the empty
-            // Chebyshev cube around it on its own (exact); only lanes in non-empty macrocells go on to
-            // the slab step, which then needs no beam-wide emptiness test
+            // per-lane probe: a lane whose next sample sits in an empty macrocell jumps on its own to the exit
+            // of the empty box its octant's skip distance guarantees ahead of it (exact: the skipped samples
+            // add zeros); only lanes in non-empty macrocells go on to the slab step, which then needs no
+            // beam-wide emptiness test
             bool samp = live;
 #if DPRT_PROBE_LOOP
             // ... and keeps jumping until its next sample sits in a non-empty macrocell (then it shades in
@@ -793,7 +794,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 if (dist > 0) {
 #endif
 #if DPRT_JUMP_BRANCHFREE
-                    // exit of the empty cube along each axis, branch-free: an axis the ray does not move along
+                    // exit of the empty box along each axis, branch-free: an axis the ray does not move along
                     // has ist = 0 and so gives je = 0, which only shortens the jump to one sample (still exact;
                     // rays with an exactly zero direction component are rare)
                     const float jx = ((float)((st[0] > 0.f ? mx + dist : mx - dist + 1) << ms) - p0[0]) * ist[0];
