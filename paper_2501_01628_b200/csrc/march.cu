@@ -948,6 +948,13 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                         } else {
 #if DPRT_QUAD_OCTET
                             load_octet(qorg + 2 * (long long)qi, qa[u], qb[u]);
+#elif DPRT_TIMING_PAIR == 1
+                            // timing only (wrong image): the far face read from the adjacent slot
+                            qa[u] = __ldg(qorg + qi);
+                            qb[u] = __ldg(qorg + qi + 1);
+#elif DPRT_TIMING_PAIR == 2
+                            // timing only (wrong image): both faces from one aligned 32-byte slot
+                            load_octet(qbase + ((qk + (unsigned)qi) & ~1u), qa[u], qb[u]);
 #else
                             qa[u] = __ldg(qorg + qi);
                             qb[u] = __ldg(qorg1 + qi);
