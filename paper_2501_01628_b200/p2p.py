@@ -43,9 +43,11 @@ class P2PCompositor:
         except Exception:  # noqa: BLE001 - reported through self.ok
             self.ok = False
         self.peer_partials = ep.share_pointers(self.index, self.partial.ptr if self.partial else 0)
-        self.root_frame = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)[0]
+        self._root_frames = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)
+        self.root_frame = self._root_frames[0]
         self.ok = self.ok and all(self.peer_partials) and self.root_frame != 0
         self.root_rgba = 0
+        self._root_rgbas = None
         self.last_bytes = 0
 
     @classmethod
@@ -65,7 +67,8 @@ class P2PCompositor:
             return
         if self.ep.rank == 0:
             self.frame_rgba = dev.DeviceBuffer(self.device, self.W * self.H * 4)
-        self.root_rgba = self.ep.share_pointers(self.index, self.frame_rgba.ptr if self.frame_rgba else 0)[0]
+        self._root_rgbas = self.ep.share_pointers(self.index, self.frame_rgba.ptr if self.frame_rgba else 0)
+        self.root_rgba = self._root_rgbas[0]
 
     def composite(self, partial: torch.Tensor, order: Sequence[int], background, keep_float: bool = False,
                   bands=None) -> CompositeOutput:
@@ -107,7 +110,9 @@ class P2PCompositor:
         return CompositeOutput(frame, self.frame_rgba.tensor if keep_float else None)
 
     def close(self) -> None:
-        self.ep.unshare_pointers(self.index, self.peer_partials)
+        for ptrs in (self.peer_partials, self._root_frames, self._root_rgbas):
+            if ptrs:
+                self.ep.unshare_pointers(self.index, ptrs)
         for buf in (self.partial, self.frame, self.frame_rgba):
             if buf is not None:
                 buf.close()
@@ -225,9 +230,11 @@ class P2PPushCompositor:
         self.distinct = len(set(ids)) == len(ids) or _emulated
         self.peer_inbox = ep.share_pointers(self.index, self.inbox.ptr if self.inbox else 0)
         self.peer_flags = ep.share_pointers(self.index, self.flags.ptr if self.flags else 0)
-        self.root_frame = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)[0]
+        self._root_frames = ep.share_pointers(self.index, self.frame.ptr if self.frame else 0)
+        self.root_frame = self._root_frames[0]
         self.ok = self.ok and self.distinct and all(self.peer_inbox) and all(self.peer_flags) and self.root_frame != 0
         self.root_rgba = 0
+        self._root_rgbas = None
         self.last_bytes = 0
 
     @classmethod
@@ -247,7 +254,8 @@ class P2PPushCompositor:
             return
         if self.ep.rank == 0:
             self.frame_rgba = dev.DeviceBuffer(self.device, self.W * self.H * 4)
-        self.root_rgba = self.ep.share_pointers(self.index, self.frame_rgba.ptr if self.frame_rgba else 0)[0]
+        self._root_rgbas = self.ep.share_pointers(self.index, self.frame_rgba.ptr if self.frame_rgba else 0)
+        self.root_rgba = self._root_rgbas[0]
 
     def march_targets(self):
         """Start a frame: (row_start, dst pointers, flag pointers, counter pointer, epoch) for dprt_march_push."""
@@ -287,7 +295,7 @@ class P2PPushCompositor:
         return CompositeOutput(frame, self.frame_rgba.tensor if keep_float else None)
 
     def close(self) -> None:
-        for ptrs in (getattr(self, "peer_inbox", None), getattr(self, "peer_flags", None)):
+        for ptrs in (self.peer_inbox, self.peer_flags, self._root_frames, self._root_rgbas):
             if ptrs:
                 self.ep.unshare_pointers(self.index, ptrs)
         for buf in (self.inbox, self.flags, self.frame, self.frame_rgba):
