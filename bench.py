@@ -820,6 +820,57 @@ def push_leg(wl: "Workload", rank: int, device, steps: int = 10) -> dict:
             "clocks": clocks.summary()}
 
 
+def push_frames_leg(renderer, cams, W: int, H: int, opts, steps: int, warmup: int, stream, device) -> dict:
+    """N > 1, every rank on its own GPU: the same frames rendered with the fused march + exchange
+    (composite='p2p_push': the march writes its row blocks into their owners' inboxes over
+    NVLink, no per-frame collective), timed like ``value`` (CUDA events on the rank's stream, max over
+    ranks).  Reported beside ``value``, never instead of it.  The outcome is combined over a gloo group: a
+    rank whose flag wait failed (its CUDA context is then gone) still reports, and cannot hang its peers
+    inside an NCCL collective."""
+    import dataclasses
+
+    import torch
+    import torch.distributed as dist
+
+    g = dist.new_group(backend="gloo")
+    ms, err = float("inf"), ""
+    try:
+        po = dataclasses.replace(opts, composite="p2p_push")
+        for k in range(warmup):
+            renderer.render(cams[k % len(cams)], W, H, po, verify=False)
+        torch.cuda.synchronize(device)
+        dist.barrier(group=g)
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k in range(steps):
+            renderer.render(cams[k % len(cams)], W, H, po, verify=False)
+        end.record(stream)
+        torch.cuda.synchronize(device)
+        ms = start.elapsed_time(end) / steps
+    except Exception as ex:  # reported in the line; the main measurement above stands
+        err = f"{type(ex).__name__}: {ex}"[:400]
+    lost = 0.0
+    if err:
+        try:  # does this rank's CUDA context still work?
+            torch.cuda.synchronize(device)
+            torch.zeros(1, device=device).item()
+        except Exception:  # noqa: BLE001
+            lost = 1.0
+    t = torch.tensor([ms, 0.0 if not err else 1.0, lost], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=g)
+    errs = [None] * dist.get_world_size()
+    dist.all_gather_object(errs, err, group=g)
+    out = {"composite": "p2p_push", "ms_per_step_max_over_ranks": None, "value": None,
+           "how": "renderer.render(..., composite='p2p_push') x steps after warmup, CUDA events, max over ranks"}
+    if t[1] == 0:
+        out["ms_per_step_max_over_ranks"] = float(t[0])
+        out["value"] = 1000.0 / float(t[0])
+    else:
+        out["errors"] = {r: e for r, e in enumerate(errs) if e}
+        out["cuda_context_lost"] = bool(t[2])
+    return out
+
+
 def c4_orbit_leg(device, steps: int = 5, every: int = 6) -> dict:
     """Config 4 on one GPU: the lander-like field's 8 uneven mass-balanced bricks all resident, every
     ``every``-th frame of the 36-frame orbit; per frame every rank's march timed alone (the sort-last frame
@@ -1206,15 +1257,25 @@ def run_ours(args):
     # TF upload and the skip-distance rebuild run inside the timed loop), pixels mapped on rank 0
     api = api_e2e(ep, device, wl, args)
 
+    # ---- N > 1: the fused march + exchange (p2p_push) on the same frames, last (a failed flag wait ends
+    # this process's CUDA context; everything measured above is already on the host)
+    comp_mode = renderer.compositor.mode if R > 1 else "single (fused into the march)"
+    push_frames = None
+    push_env = os.environ.get("DPRT_BENCH_PUSH", "1")
+    if R > 1 and push_env != "0" and (not shared or push_env == "force"):
+        log("[bench] fused march + exchange (p2p_push) frames")
+        push_frames = push_frames_leg(renderer, cams, W, H, opts, args.steps, max(args.warmup, 3), stream, device)
+    context_lost = bool(push_frames and push_frames.get("cuda_context_lost"))
+
     cpu = None
     extras = {}
     if rank == 0 and R == 1 and not args.no_cpu_baseline and cfg in ("c1", "c2", "c3"):
         log("[bench] timing the CPU oracle on a row sample")
         cpu = cpu_baseline_rows(brick.download(), wl)
-    comp_mode = renderer.compositor.mode if R > 1 else "single (fused into the march)"
-    brick.close()
-    del renderer, brick
-    torch.cuda.empty_cache()
+    if not context_lost:
+        brick.close()
+        del renderer, brick
+        torch.cuda.empty_cache()
     if R == 1 and cfg == "c2" and not args.no_extras:
         # config 3 (the north-star target) on this one GPU: every rank's brick of the 2048^3 field marched
         # alone under clocks, even 2x2x2 and mass-balanced kd splits, + its CPU baseline
@@ -1276,11 +1337,17 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "backend": backend if R > 1 else "single",
         }
+        if push_frames is not None:
+            line["p2p_push_frames"] = push_frames
         if shared:
             line["measurement"] = False
             line["note"] = f"{R} ranks shared {torch.cuda.device_count()} GPU(s) over gloo: functional run only"
         line.update(extras)
         print(json.dumps(line), flush=True)
+    if context_lost:  # NCCL teardown on a lost context can block: the line is out, leave now
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
     if R > 1:
         dist.destroy_process_group()
 

@@ -88,7 +88,9 @@ def test_exchange_modes_across_processes(cuda_device, oracle_lib, mode, R):
 def test_bench_multi_rank_code_path(tmp_path, fragments):
     """bench.py's N > 1 leg (weak-scaled bricks, compositor roofline, e2e, max over ranks) run as two
     torchrun processes on this box's one GPU with the gloo control plane (DPRT_BENCH_BACKEND=gloo): a
-    functional check of the code the 8-GPU scaling run executes, not a measurement."""
+    functional check of the code the 8-GPU scaling run executes, not a measurement.  The p2p_push frames
+    leg is forced on: with both ranks on one GPU it must fail cleanly on every rank (the push compositor
+    refuses ranks sharing a GPU) and be reported in the line without disturbing the rest of it."""
     import json
     import os
     import subprocess
@@ -96,7 +98,7 @@ def test_bench_multi_rank_code_path(tmp_path, fragments):
     from pathlib import Path
 
     root = Path(__file__).resolve().parent.parent
-    env = dict(os.environ, DPRT_BENCH_BACKEND="gloo")
+    env = dict(os.environ, DPRT_BENCH_BACKEND="gloo", DPRT_BENCH_PUSH="force")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", str(root / "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--fragments", fragments]
@@ -108,3 +110,6 @@ def test_bench_multi_rank_code_path(tmp_path, fragments):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["compositor_roofline"]["mode"] in ("p2p", "direct_send")
     assert line["config"]["bricks"] == 2 and line["run"]["fragments"] == fragments
+    push = line["p2p_push_frames"]
+    assert push["value"] is None and set(push["errors"]) == {"0", "1"} and not push["cuda_context_lost"]
+    assert all("TransportError" in e for e in push["errors"].values())
