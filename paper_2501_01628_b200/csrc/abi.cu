@@ -465,6 +465,23 @@ static int march_impl(const DprtBrick* b, const DprtCamera* cam, const DprtMarch
         int ex;
         a.inv_dt_pow2 = (frexp(p->dt, &ex) == 0.5) ? 1.0 / p->dt : 0.0;  // exact inverse of a power of two
     }
+    a.fs_iw2 = 2.0 / W;
+    a.fs_ih2 = 2.0 / H;
+    for (int i = 0; i < 3; ++i) {
+        a.fs_L[i] = a.blo[i] - cam->pos[i];  // == __dsub_rn(lo, o) of the exact path
+        a.fs_H[i] = a.bhi[i] - cam->pos[i];
+    }
+    a.fs_idt = 1.0 / p->dt;
+    a.fs_S = 1.0 + fabs(cam->half_w) + fabs(cam->half_h);
+    a.fs_ok = a.blo[0] <= a.bhi[0] && a.blo[1] <= a.bhi[1] && a.blo[2] <= a.bhi[2] && isfinite(a.fs_S);
+    {  // the fast setup's error bound needs |f + sx r + sy u| >= 1: an orthonormal camera basis
+        const double* v[3] = {cam->fwd, cam->right, cam->up};
+        for (int i = 0; i < 3; ++i)
+            for (int j = i; j < 3; ++j) {
+                const double g = v[i][0] * v[j][0] + v[i][1] * v[j][1] + v[i][2] * v[j][2];
+                if (!(fabs(g - (i == j ? 1.0 : 0.0)) <= 1e-9)) a.fs_ok = 0;
+            }
+    }
     a.sy = (long long)b->sd[0];
     a.sz = (long long)b->sd[0] * b->sd[1];
     a.vox = b->vox;

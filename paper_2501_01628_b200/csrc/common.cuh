@@ -57,6 +57,9 @@ constexpr int kSkipCap = DPRT_SKIP_CAP;  // Chebyshev skip distances are capped 
 #define DPRT_SKIP_OCTANT 1  // the beam marcher's per-lane probe jumps by one-sided (octant) distances
 #endif
 constexpr int kSkipGrids = 9;  // symmetric + 8 octants
+#ifndef DPRT_SETUP_FAST
+#define DPRT_SETUP_FAST 0  // beam marcher: f64 ray setup with Newton-refined rcp / rsqrt, the exact setup only for
+#endif                     // lanes whose lattice range it cannot prove (march.cu fast_range)
 #ifndef DPRT_SUBBLOCK
 #define DPRT_SUBBLOCK 0  // 1 / 2: the probe also skips empty 4^3 sub-blocks of non-empty macrocells (measured:
 #endif                   // 9 % fewer shaded samples on c2 but 0.7 % slower, config 3 2-4 % slower; not adopted)
@@ -118,6 +121,10 @@ struct MarchArgs {
     float mt_f[3], mt_r[3], mt_u[3], mt_lo[3], mt_hi[3];
     float mt_hw, mt_hh, mt_iw, mt_ih;
     const uint8_t* __restrict__ subm;   // per macrocell: non-empty 4^3 sub-blocks (DPRT_SUBBLOCK)
+    // fast ray setup (DPRT_SETUP_FAST): 2/W, 2/H, the owned box relative to the eye (the exact path's own
+    // f64 differences), 1/dt, the direction-component scale 1 + half_w + half_h; fs_ok = 0 -> exact only
+    double fs_iw2, fs_ih2, fs_L[3], fs_H[3], fs_idt, fs_S;
+    int fs_ok;
     int mcd[3];
     int skip;
     int band_clear;  // clear only the footprint's row band of the partial (DPRT_MARCH_BAND_CLEAR)

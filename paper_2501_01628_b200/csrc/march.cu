@@ -97,6 +97,84 @@ __device__ __forceinline__ int64_t lattice_range(const MarchArgs& a, const doubl
     return kb > ka ? kb - ka : 0;
 }
 
+#if DPRT_SETUP_FAST
+// Fast ray setup.  The same ray as primary_dir + lattice_range, in f64 with FMA, a Newton-refined approximate
+// rsqrt for the normalisation and Newton-refined reciprocals for the slab divisions -- no correctly rounded
+// division or square root (each a MUFU + 7 DFMA + a slow-path test).  Its values differ from the exact
+// setup's by a few units in the last place, scaled up for a direction component d_i by S / |d_i| (the
+// cancellation in f + sx r + sy u, S = 1 + half_w + half_h).  Each slab bound t carries that error bound e;
+// the lattice range [ceil(max(t0, 0) / dt), ceil(t1 / dt)) is taken only when no lattice point lies within
+// the widened interval of either end, so it equals the exact one; otherwise (a near-zero direction
+// component, an end within ~1e-12 of a lattice point, an empty box) the caller runs the exact setup.
+// Returns false for "not proven".  d[] (start position and step of the f32 march) is accurate to ~1e-15.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    return y * fma(-h * y, y, 1.5);
+}
+
+// ceil(u) for every u in [lo, hi], or INT64_MIN if the interval holds a lattice point in its interior
+__device__ __forceinline__ int64_t ceil_if_unique(double lo, double hi) {
+    const double c = ceil(lo);
+    return hi <= c ? (int64_t)c : INT64_MIN;
+}
+
+__device__ __forceinline__ bool fast_range(const MarchArgs& a, int px, int py, double d[3], int64_t* k0,
+                                           int64_t* n) {
+    const double sx = fma((double)px + 0.5, a.fs_iw2, -1.0) * a.half_w;
+    const double sy = fma(-((double)py + 0.5), a.fs_ih2, 1.0) * a.half_h;
+    double D[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) D[i] = fma(sy, a.u[i], fma(sx, a.r[i], a.f[i]));
+    const double rn = rsqrt_nr(fma(D[0], D[0], fma(D[1], D[1], D[2] * D[2])));
+    // |D| >= 1 (f is a unit vector orthogonal to r and u), so the absolute error of d_i is ~ 2^-50 S
+    // per-axis relative bound of t against the exact setup's t: 2^-42 (S / |d_i| + 1) -- the analysis gives
+    // 2^-46 S / |d_i| (D: a few roundings of terms <= S each way; |D| >= 1) + 2^-50 (rcp, products, t / dt)
+    constexpr double kRel = 0x1p-42;
+    double t0lo = -INFINITY, t0hi = -INFINITY, t1lo = INFINITY, t1hi = INFINITY;
+    bool ok = a.fs_ok != 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        d[i] = D[i] * rn;
+        const double ad = fabs(d[i]);
+        ok = ok && ad > 1e-6;
+        const double inv = rcp_nr(d[i]);
+        const double ta = a.fs_L[i] * inv, tb = a.fs_H[i] * inv;
+        const double tmn = fmin(ta, tb), tmx = fmax(ta, tb);
+        const double rel = kRel * (a.fs_S / ad + 1.0);
+        const double emn = fabs(tmn) * rel, emx = fabs(tmx) * rel;
+        t0lo = fmax(t0lo, tmn - emn);
+        t0hi = fmax(t0hi, tmn + emn);
+        t1lo = fmin(t1lo, tmx - emx);
+        t1hi = fmin(t1hi, tmx + emx);
+    }
+    if (!ok) return false;
+    // the exact path's t / dt (one more rounding; or an exact power-of-two scaling) lies in the widened range
+    const double idt = a.fs_idt;
+    const double u0lo = fmax(t0lo, 0.0) * idt, u0hi = fmax(t0hi, 0.0) * idt;
+    const double u1lo = t1lo * idt, u1hi = t1hi * idt;
+    constexpr double kW = 0x1p-50;
+    const int64_t ka = ceil_if_unique(u0lo - fabs(u0lo) * kW, u0hi + fabs(u0hi) * kW);
+    const int64_t kb = ceil_if_unique(u1lo - fabs(u1lo) * kW, u1hi + fabs(u1hi) * kW);
+    if (ka == INT64_MIN || kb == INT64_MIN) return false;
+    *k0 = ka;
+    *n = kb > ka ? kb - ka : 0;
+    return true;
+}
+#endif
+
 // Known-answer kernels: the marcher's own device functions applied to caller-supplied rays, so the
 // reference's golden vectors (camera rays, slab intervals) are checked on the GPU code itself.
 __global__ void kat_slab_kernel(const double* __restrict__ o, const double* __restrict__ d,
@@ -660,8 +738,16 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             pix = py * a.W + px;
             double d[3];
             int64_t k0 = 0;
+#if DPRT_SETUP_FAST
+            int64_t n = 0;
+            if (!fast_range(a, px, py, d, &k0, &n)) {
+                primary_dir(a, px, py, d);
+                n = lattice_range(a, d, &k0);
+            }
+#else
             primary_dir(a, px, py, d);
             const int64_t n = lattice_range(a, d, &k0);
+#endif
             if (!kMark && a.samples) a.samples[pix - a.pix0] = (uint32_t)n;
             if (n > 0) {
                 const double t0 = __dmul_rn((double)k0, a.dt);
