@@ -871,6 +871,45 @@ def push_frames_leg(renderer, cams, W: int, H: int, opts, steps: int, warmup: in
     return out
 
 
+def c3_one_rank_leg(device, steps: int = 20, warmup: int = 3) -> dict:
+    """The N > 1 workload family (config-3 family: 1024^3 cells per rank at 3840x2160) at ONE rank -- one
+    1024^3 brick, the single-rank fused frame, two frames in flight like ``value`` -- so that the N > 1 lines
+    (weak scaling of this family) have a same-workload N = 1 reference; the N = 1 ``value`` itself is
+    BASELINE's config 2."""
+    import torch
+
+    from paper_2501_01628_b200 import device as dev
+    from paper_2501_01628_b200.engine import RenderOptions, VolumeRenderer
+    from paper_2501_01628_b200.transport import SoloEndpoint
+
+    wl = build_workload("c3", 1, "even")
+    brick = dev.DeviceBrick(wl.dec.brick(0), device).generate(wl.field)
+    renderer = VolumeRenderer(SoloEndpoint(device), brick, wl.dec, wl.tf, BACKGROUND)
+    opts = RenderOptions(dt=DT, ert=ERT, frames_in_flight=2)
+    stream = torch.cuda.current_stream(device)
+    for _ in range(warmup):
+        renderer.render(wl.cams[0], wl.W, wl.H, opts, verify=False)
+    renderer.join(stream)
+    torch.cuda.synchronize(device)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device.index) as clocks:
+        start.record(stream)
+        for _ in range(steps):
+            renderer.render(wl.cams[0], wl.W, wl.H, opts, verify=False)
+        renderer.join(stream)
+        end.record(stream)
+        torch.cuda.synchronize(device)
+    ms = start.elapsed_time(end) / steps
+    brick.close()
+    del renderer, brick
+    torch.cuda.empty_cache()
+    return {"workload": wl.text, "value": 1000.0 / ms, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "frames_in_flight": 2, "config": wl.config(1), "clocks": clocks.summary(),
+            "note": "same-workload N = 1 reference for the N > 1 lines (weak scaling of the config-3 family); "
+                    "value_N / value_1 across the driver's N = 1 (config 2) and N > 1 lines compares different "
+                    "workloads"}
+
+
 def c4_orbit_leg(device, steps: int = 5, every: int = 6) -> dict:
     """Config 4 on one GPU: the lander-like field's 8 uneven mass-balanced bricks all resident, every
     ``every``-th frame of the 36-frame orbit; per frame every rank's march timed alone (the sort-last frame
@@ -1282,6 +1321,8 @@ def run_ours(args):
         log("[bench] config 3 per-rank leg (8 bricks of 2048^3 at 3840x2160)")
         extras["c3_per_rank"] = {s: per_rank_leg("c3", s, device, 10, 3, cpu=(s == "even") and not args.no_cpu_baseline)
                                  for s in ("even", "mass")}
+        log("[bench] config-3 family at one rank (the N > 1 lines' weak-scaling reference)")
+        extras["c3_family_one_rank"] = c3_one_rank_leg(device)
         log("[bench] config 4 orbit leg and config 5 blend leg")
         extras["c4_orbit"] = c4_orbit_leg(device)
         extras["c5_blend"] = c5_blend_leg(device)

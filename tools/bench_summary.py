@@ -60,6 +60,11 @@ if "c3_per_rank" in d:
     if ev.get("reference_gather"):
         L.append(f"The reference's own gather_to_root + _assemble_tiles (4K, 8 ranks, `baseline/_ref`): "
                  f"{ev['reference_gather']['ms']:.1f} ms.\n")
+if "c3_family_one_rank" in d:
+    o = d["c3_family_one_rank"]
+    L.append(f"## config-3 family at one rank (one 1024³ brick, 3840×2160; the N > 1 lines' weak-scaling reference)\n\n"
+             f"{o['value']:.0f} frames/s ({o['ms_per_step']:.4f} ms/frame, two in flight); clocks "
+             f"{o['clocks']['sm_mhz']} MHz {o['clocks']['reasons']}.\n")
 if "c4_orbit" in d:
     c4 = d["c4_orbit"]
     L.append(f"## config 4 (8 uneven bricks, orbit frames 0, 6, …, 30)\n\nmean slowest-rank march "
