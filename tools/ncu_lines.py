@@ -31,6 +31,7 @@ data = [r for r in rows[hdr_i + 1:] if len(r) == len(h)]
 addrs = [int(r[ix["Address"]], 16) for r in data]
 base = min(addrs)
 
+# ranges are line spans of march.cu (lines of other files -- headers, inlined library code -- are listed below)
 with tempfile.TemporaryDirectory() as td:
     subprocess.run(["cuobjdump", "-xelf", "all", str(Path(lib).resolve())], cwd=td, capture_output=True, check=True)
     off2line = {}
@@ -40,11 +41,11 @@ with tempfile.TemporaryDirectory() as td:
         if sec < 0:
             continue
         end = dis.find("//---------------------", sec)
-        line = 0
+        line = ("?", 0)
         for l in dis[sec:end if end > 0 else None].splitlines():
-            m = re.search(r'//## File ".*", line (\d+)', l)
+            m = re.search(r'//## File "(.*)", line (\d+)', l)
             if m:
-                line = int(m.group(1))
+                line = (Path(m.group(1)).name, int(m.group(2)))
                 continue
             m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", l)
             if m:
@@ -54,15 +55,15 @@ with tempfile.TemporaryDirectory() as td:
 inst = collections.Counter()
 stall = collections.Counter()
 for r, a in zip(data, addrs):
-    ln = off2line.get(a - base, -1)
+    ln = off2line.get(a - base, ("?", -1))
     inst[ln] += float(r[ix["Instructions Executed"]] or 0)
     stall[ln] += float(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
 T, S = sum(inst.values()), sum(stall.values())
 print(f"total warp instructions {T:.4g}, stall samples {S:.0f}, lines mapped {len(inst)}")
 if ranges:
     for name, a, b in ranges:
-        i = sum(v for k, v in inst.items() if a <= k <= b)
-        s = sum(v for k, v in stall.items() if a <= k <= b)
+        i = sum(v for k, v in inst.items() if k[0] == "march.cu" and a <= k[1] <= b)
+        s = sum(v for k, v in stall.items() if k[0] == "march.cu" and a <= k[1] <= b)
         print(f"{name:24s} lines {a}-{b}: {i / T * 100:5.1f} % instr, {s / S * 100:5.1f} % stall samples")
 for ln in sorted(inst, key=lambda k: -inst[k])[:40]:
-    print(f"line {ln:5d}: {inst[ln] / T * 100:5.1f} % instr  {stall[ln] / S * 100:5.1f} % stall")
+    print(f"{ln[0]}:{ln[1]:<5d} {inst[ln] / T * 100:5.1f} % instr  {stall[ln] / S * 100:5.1f} % stall")
