@@ -203,6 +203,7 @@ class ClockSampler:
         self._stop = threading.Event()
         self._poll = None
         self.error = None
+        self._mark = 0
 
     def _nvml_handle(self):
         import pynvml
@@ -256,6 +257,10 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def mark(self) -> None:
+        """The timed region starts now: the NVML summary covers only the samples from here on."""
+        self._mark = len(self.nvml)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -292,11 +297,12 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(n)
         bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
-        if self.nvml:
-            for _, _, r in self.nvml:
+        nv = self.nvml[self._mark:] or self.nvml[-1:]
+        if nv:
+            for _, _, r in nv:
                 reasons.update(n for n, b in bits.items() if r & b)
-            return {"sm_mhz": statistics.median(c for c, _, _ in self.nvml), "sm_max_mhz": float(self.nvml[0][1]),
-                    "reasons": sorted(reasons), "samples": len(self.nvml), "source": "nvml 1 ms poll + nvidia-smi",
+            return {"sm_mhz": statistics.median(c for c, _, _ in nv), "sm_max_mhz": float(nv[0][1]),
+                    "reasons": sorted(reasons), "samples": len(nv), "source": "nvml 1 ms poll + nvidia-smi",
                     "smi_samples": len(sm)}
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
@@ -498,6 +504,34 @@ def resolve_config(cfg: str, R: int) -> str:
     if cfg == "auto":
         return "c2" if R == 1 else "c3"
     return cfg
+
+
+def spin_up(step, n: int, device, R: int = 1, min_s: float = 0.2) -> int:
+    """The W warm-up steps, then more until the GPU has been busy for ``min_s``: an idle GPU lowers its SM
+    clock and the first milliseconds after idle run slower (measured on c2: the first 20-frame region after
+    0.5 s idle +6 %, later regions not), so a timed region that follows set-up or another leg's host work
+    would otherwise start below the clock a sustained run holds.  The extra count is derived from the
+    slowest rank's W-step time, so every rank runs the same number of (collective) steps.  ``step(k)``."""
+    import torch
+    import torch.distributed as dist
+
+    for k in range(n):  # W steps (first-frame set-up included)
+        step(k)
+    torch.cuda.synchronize(device)
+    m = max(n, 4)  # steady-state step time
+    t0 = time.perf_counter()
+    for k in range(n, n + m):
+        step(k)
+    torch.cuda.synchronize(device)
+    per = (time.perf_counter() - t0) / m
+    if R > 1:
+        t = torch.tensor([per], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per = float(t.item())
+    extra = min(int(math.ceil(min_s / max(per, 1e-5))), 20000)
+    for k in range(n + m, n + m + extra):
+        step(k)
+    return n + m + extra
 
 
 def events_ms(fn, steps: int, stream) -> float:
@@ -1191,15 +1225,15 @@ def run_ours(args):
         renderer.render(cams[k_step[0] % len(cams)], W, H, opts, verify=False)
         k_step[0] += 1
 
-    # ---- device-resident throughput (value)
-    for _ in range(args.warmup):
-        step()
-    renderer.join(stream)
-    barrier()
-    k_step[0] = 0
+    # ---- device-resident throughput (value); the clock sampler starts first, so its own start-up (NVML,
+    # nvidia-smi) overlaps the warm-up rather than the timed region
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(device.index) as clocks:
+        warm = spin_up(lambda k: step(), args.warmup, device, R)
+        renderer.join(stream)
         barrier()
+        k_step[0] = 0
+        clocks.mark()
         start.record(stream)
         for _ in range(args.steps):
             step()
@@ -1283,8 +1317,7 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for k in range(args.warmup):
-        e2e_step(k)
+    spin_up(e2e_step, args.warmup, device, R)
     drain()
     d2h0 = renderer.d2h_bytes
     e2e_fps = args.steps / timed_host(e2e_step, args.steps)
@@ -1363,7 +1396,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": wl.config(R),
-            "run": {"composite": comp_mode,
+            "run": {"warmup_steps_run": warm,
+                    "warmup_rule": "W steps, then more until the GPU has been busy 0.2 s (spin_up: no timed region "
+                                   "starts at an idle-lowered clock)",
+                    "composite": comp_mode,
                     "fragments": args.fragments, "frames_in_flight": fif, "empty_space_skipping": skip},
             "roofline": roof,
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -1468,8 +1504,7 @@ def api_e2e(ep, device, wl: Workload, args) -> dict:
     d2h0 = [0]
 
     def timed() -> float:
-        for k in range(args.warmup):
-            step(k)
+        spin_up(step, args.warmup, device, ep.R)
         frame.wait()
         if ep.R > 1:
             dist.barrier()
