@@ -307,6 +307,27 @@ __device__ __forceinline__ void quad_bounds_check(const MarchArgs& a, long long 
 #endif
 }
 
+// DPRT_BOUNDS_CHECK builds: every skip-distance load and every output store of the beam marcher traps
+// outside its buffer (a debug build for the parity suite; compiled out otherwise)
+__device__ __forceinline__ void skip_bounds_check(const MarchArgs& a, long long mci) {
+#if DPRT_BOUNDS_CHECK
+    if (mci < 0 || mci >= a.skip_n) __trap();
+#else
+    (void)a;
+    (void)mci;
+#endif
+}
+
+__device__ __forceinline__ void pix_bounds_check(const MarchArgs& a, long long pix) {
+#if DPRT_BOUNDS_CHECK
+    if (pix < 0 || pix >= (long long)a.W * a.H) __trap();
+    if (!a.rgb8 && (pix - a.pix0 < 0 || pix - a.pix0 >= a.npix_buf) && (a.out || a.out16 || a.samples)) __trap();
+#else
+    (void)a;
+    (void)pix;
+#endif
+}
+
 // TF lookup and front-to-back premultiplied blend (§2.7) of one sample value.  Shared memory
 // holds the entries (s_tf) and, in a second array, next - entry (s_dtf; 16-byte strides keep neighbouring
 // lanes' LDS.128 on distinct banks); the last entry's difference is zero, so x = n - 1 needs no clamp.
@@ -522,6 +543,9 @@ __device__ __forceinline__ void store_partial(const MarchArgs& a, const uint8_t*
     if constexpr (kPush) {
         const int b = s_blk[y];
         const long long e = pix - (long long)a.push_row[b] * a.W;
+#if DPRT_BOUNDS_CHECK
+        if (b < 0 || b >= a.push_P || e < 0 || e >= (long long)(a.push_row[b + 1] - a.push_row[b]) * a.W) __trap();
+#endif
         if (a.half_out) {
             const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
             reinterpret_cast<uint2*>(a.push_dst[b])[e] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
@@ -532,6 +556,9 @@ __device__ __forceinline__ void store_partial(const MarchArgs& a, const uint8_t*
     } else {
         (void)y;
         (void)s_blk;
+#if DPRT_BOUNDS_CHECK
+        if (pix - a.pix0 < 0 || pix - a.pix0 >= a.npix_buf) __trap();
+#endif
         if (a.half_out) {
             const __half2 rg = __floats2half2_rn(C0, C1), ba = __floats2half2_rn(C2, A);
             a.out16[pix - a.pix0] = make_uint2(*reinterpret_cast<const unsigned*>(&rg),
@@ -554,6 +581,9 @@ __device__ void fill_outside_rect(const MarchArgs& a, const uint8_t* s_blk, int 
     const uint32_t cb = (uint32_t)floorf(fminf(fmaxf(a.bg[2], 0.f), 1.f) * 255.f + 0.5f);
     const int W = a.W, qpr = (W + 3) / 4;  // 4-pixel groups per row (no index division: rows per block)
     for (int y = y0 + unit; y < y1; y += nunits) {
+#if DPRT_BOUNDS_CHECK
+        if (y < 0 || y >= a.H) __trap();
+#endif
         const bool row_out = y < a.rect[1] || y >= a.rect[3];
         for (int q = t; q < qpr; q += nt) {
             const int x0 = 4 * q;
@@ -593,6 +623,7 @@ __device__ void fill_outside_rect(const MarchArgs& a, const uint8_t* s_blk, int 
 template <bool kPush>
 __device__ __forceinline__ void write_clear(const MarchArgs& a, const uint8_t* s_blk, int pix, int py) {
     if (a.rgb8) {
+        pix_bounds_check(a, pix);
         uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
 #pragma unroll
         for (int c = 0; c < 3; ++c) dst[c] = (uint8_t)floorf(fminf(fmaxf(a.bg[c], 0.f), 1.f) * 255.f + 0.5f);
@@ -748,6 +779,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
             primary_dir(a, px, py, d);
             const int64_t n = lattice_range(a, d, &k0);
 #endif
+            pix_bounds_check(a, pix);
             if (!kMark && a.samples) a.samples[pix - a.pix0] = (uint32_t)n;
             if (n > 0) {
                 const double t0 = __dmul_rn((double)k0, a.dt);
@@ -846,6 +878,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
 #if DPRT_SUBBLOCK == 2
                 const unsigned smask = __ldg(a.subm + mci);  // issued with (not after) the distance load
 #endif
+                skip_bounds_check(a, mci);
                 const int dist = pf >= 0 ? pf : (int)__ldg(skipl + mci);
                 pf = -1;
 #else
@@ -939,6 +972,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                     const int ex = fl2cell(fmaf(fe, st[0], p0[0]), chx) >> ms;
                     const int ey = fl2cell(fmaf(fe, st[1], p0[1]), chy) >> ms;
                     const int ez = fl2cell(fmaf(fe, st[2], p0[2]), chz) >> ms;
+                    skip_bounds_check(a, (ez * mcd1 + ey) * mcd0 + ex);
                     pf = (int)__ldg(skipl + (ez * mcd1 + ey) * mcd0 + ex);
                 }
 #endif
@@ -1164,6 +1198,7 @@ __global__ void __launch_bounds__(kBeamBlock, kMinBlocks) march_beam_kernel(cons
                 // single-rank frame: the over-background + tone map of the compositor, fused
                 // (engine.py:500-502); a miss inside the footprint is the background itself
                 const float one = 1.f - A;
+                pix_bounds_check(a, pix);
                 uint8_t* dst = a.rgb8 + 3 * (size_t)pix;
                 dst[0] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[0], C0), 0.f), 1.f) * 255.f + 0.5f);
                 dst[1] = (uint8_t)floorf(fminf(fmaxf(fmaf(one, a.bg[1], C1), 0.f), 1.f) * 255.f + 0.5f);
