@@ -36,6 +36,42 @@ def _bands(dec, cam, W, H):
                                             (8, 128, 96, True, False)])
 def test_push_frames_equal_local_march_and_composite(cuda_device, P, W, H, clip, half):
     s = c1(P=P, W=W, H=H)
+    bb = s.field.bounds()
+    cams = [s.cam] + [orbit_camera(bb.center(), 1.3 * bb.diagonal(), math.radians(35.0 * k), math.radians(15.0),
+                                   45.0, W / H) for k in range(1, 4)]
+    _push_vs_local(cuda_device, s, cams, P, W, H, clip, half)
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_push_frames_with_offscreen_bricks_and_an_eye_inside(cuda_device, P):
+    """Cameras for which some bricks have no footprint at all (narrow view of one corner: their pushes are
+    background-only and whole row blocks blend nothing but the background) and one inside a brick."""
+    from paper_2501_01628_b200.geom import CameraSpec
+
+    W, H = 150, 110
+    s = c1(P=P, W=W, H=H)
+    lo, hi = s.field.bounds().lo, s.field.bounds().hi
+
+    def at(fx, fy, fz):  # a point in field-relative coordinates
+        return tuple(lo[i] + f * (hi[i] - lo[i]) for i, f in enumerate((fx, fy, fz)))
+
+    inside = at(0.3, 0.3, 0.3)
+    centre = s.field.bounds().center()
+
+    def look(pos, tgt, fov):
+        v = tuple(t - p for t, p in zip(tgt, pos))
+        n = math.sqrt(sum(c * c for c in v))
+        return CameraSpec(pos, tuple(c / n for c in v), (0.0, 1.0, 0.0), fov, W / H)
+
+    # axis-parallel narrow views down one corner column of the field: bricks away from it project nowhere
+    cams = [look(at(0.1, 0.1, -1.5), at(0.1, 0.1, 0.5), 10.0), look(at(-1.5, 0.9, 0.85), at(0.5, 0.9, 0.85), 6.0),
+            look(inside, centre, 60.0), look(inside, tuple(2 * p - c for p, c in zip(inside, centre)), 75.0)]
+    bands = [[tuple(dev.desc_footprint(s.dec.brick(r), c, W, H)[1::2]) for r in range(P)] for c in cams[:2]]
+    assert any(b[1] <= b[0] for bl in bands for b in bl), "the narrow views should leave some brick off-screen"
+    _push_vs_local(cuda_device, s, cams, P, W, H, True, False)
+
+
+def _push_vs_local(cuda_device, s, cams, P, W, H, clip, half):
     d = cuda_device
     fdt = torch.float16 if half else torch.float32
     L = PushLayout(P, W, H, 8 if half else 16)
@@ -46,9 +82,6 @@ def test_push_frames_equal_local_march_and_composite(cuda_device, P, W, H, clip,
     frame = torch.zeros((H, W, 3), dtype=torch.uint8, device=d)
     ib = [t.data_ptr() for t in inbox]
     fb = [t.data_ptr() for t in flags]
-    bb = s.field.bounds()
-    cams = [s.cam] + [orbit_camera(bb.center(), 1.3 * bb.diagonal(), math.radians(35.0 * k), math.radians(15.0),
-                                   45.0, W / H) for k in range(1, 4)]
     for epoch, cam in enumerate(cams, start=1):
         order = s.dec.visibility_order(cam.position)
         bands = _bands(s.dec, cam, W, H) if clip else None
