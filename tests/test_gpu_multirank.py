@@ -82,6 +82,69 @@ def test_band_clipped_exchange_is_bit_identical(cuda_device, mode, R, W, H):
         assert sum(r[1][2] for r in res) < sum(r[0][2] for r in res)
 
 
+def _narrow_cameras(s, W, H):
+    """Axis-parallel narrow views down one corner column of the field (bricks away from it have no screen
+    footprint) and a wide view from inside a brick."""
+    import math
+
+    from paper_2501_01628_b200.geom import CameraSpec
+
+    lo, hi = s.field.bounds().lo, s.field.bounds().hi
+
+    def at(fx, fy, fz):
+        return tuple(lo[i] + f * (hi[i] - lo[i]) for i, f in enumerate((fx, fy, fz)))
+
+    def look(pos, tgt, fov):
+        v = tuple(t - p for t, p in zip(tgt, pos))
+        n = math.sqrt(sum(c * c for c in v))
+        return CameraSpec(pos, tuple(c / n for c in v), (0.0, 1.0, 0.0), fov, W / H)
+
+    return [look(at(0.1, 0.1, -1.5), at(0.1, 0.1, 0.5), 10.0), look(at(-1.5, 0.9, 0.85), at(0.5, 0.9, 0.85), 6.0),
+            look(at(0.3, 0.3, 0.3), s.field.bounds().center(), 60.0)]
+
+
+@pytest.mark.parametrize("mode,R", [("direct_send", 4), ("p2p", 4), ("binary_swap", 4), ("cycle", 4),
+                                    ("direct_send", 8), ("p2p", 8), ("binary_swap", 8)])
+def test_frames_with_offscreen_bricks_match_oracle(cuda_device, oracle_lib, mode, R):
+    """Every exchange schedule when some bricks project nowhere on screen (empty footprints: no rows to
+    send, fragments that are clear everywhere, row blocks blending only background) and with the eye inside
+    a brick: rank 0's frame against the oracle composite, sample ownership exact on every rank."""
+    W, H = 150, 110
+    s = c1(P=R, W=W, H=H)
+    cams = _narrow_cameras(s, W, H)
+    assert any(dev.desc_footprint(s.dec.brick(r), cams[0], W, H)[3] <= dev.desc_footprint(s.dec.brick(r), cams[0], W, H)[1]
+               for r in range(R))
+    vox = oracle.generate_field(s.field.dims, s.field.blobs)
+    refs = []
+    for cam in cams:
+        ref, rs = oracle_partials(vox, s.dec, cam, s.tf, s.dt, s.ert, W, H)
+        order = s.dec.visibility_order(cam.position)
+        refs.append((oracle.composite(ref, order, s.background), rs, order))
+
+    def body(ep):
+        b = dev.DeviceBrick(s.dec.brick(ep.rank), cuda_device).generate(s.field)
+        vr = VolumeRenderer(ep, b, s.dec, s.tf, s.background)
+        out = []
+        for k, cam in enumerate(cams):
+            res = vr.render(cam, W, H, RenderOptions(composite=mode, keep_float=True, collect_samples=True,
+                                                     frame_index=k))
+            torch.cuda.synchronize()
+            out.append((res.image, None if res.rgb8 is None else res.rgb8.cpu().numpy(),
+                        res.samples.cpu().numpy().astype(np.uint32), res.order))
+        return out
+
+    results = run_collective(R, body, device=cuda_device)
+    for k, (img_ref, rs, order) in enumerate(refs):
+        for r in range(R):
+            image, rgb8, samples, got_order = results[r][k]
+            assert np.array_equal(samples, rs[r]), f"camera {k} rank {r} ownership"
+            assert got_order == order
+            if r == 0:
+                assert np.abs(image - img_ref).max() <= RGBA_ATOL
+                q = rgb8.astype(np.int16) - oracle.tone_map_rgb8(img_ref).astype(np.int16)
+                assert np.abs(q).max() <= RGB8_MAX_LSB
+
+
 def test_disable_compositing_shows_only_root_brick(cuda_device, oracle_lib):
     """Negative test (engine.py:172 analog): without compositing the frame is rank 0's brick alone."""
     s = c1(P=2, W=96, H=96)
