@@ -71,6 +71,21 @@ def test_push_frames_with_offscreen_bricks_and_an_eye_inside(cuda_device, P):
     _push_vs_local(cuda_device, s, cams, P, W, H, True, False)
 
 
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("DPRT_PUSH_FUZZ_CASES", "12"))))
+def test_push_fuzz(cuda_device, seed):
+    """Seeded random push scenes: P in 2..8, odd frame sizes (row blocks of unequal height), random orbit
+    cameras incl. close-ups, band clipping on / off, fp16 fragments; byte-identical to march + composite."""
+    rng = np.random.default_rng(5000 + seed)
+    P = int(rng.integers(2, 9))
+    W, H = int(rng.integers(24, 200)), int(rng.integers(P, 160))
+    s = c1(P=P, W=W, H=H)
+    bb = s.field.bounds()
+    cams = [orbit_camera(bb.center(), float(rng.uniform(0.4, 1.6)) * bb.diagonal(),
+                         math.radians(float(rng.uniform(0, 360))), math.radians(float(rng.uniform(-60, 60))),
+                         float(rng.uniform(20, 80)), W / H) for _ in range(3)]
+    _push_vs_local(cuda_device, s, cams, P, W, H, bool(rng.integers(0, 2)), bool(rng.integers(0, 4) == 0))
+
+
 def _push_vs_local(cuda_device, s, cams, P, W, H, clip, half):
     d = cuda_device
     fdt = torch.float16 if half else torch.float32
