@@ -482,7 +482,7 @@ constexpr int kBeamUnroll = DPRT_BEAM_UNROLL;
 #ifndef DPRT_BEAM_W
 #define DPRT_BEAM_W 4
 #endif
-constexpr int kBeamW = DPRT_BEAM_W, kBeamH = 32 / DPRT_BEAM_W;  // beam = kBeamW x kBeamH pixels
+constexpr int kBeamW = DPRT_BEAM_W;  // beam = kBeamW x (32 / kBeamW) pixels
 #ifndef DPRT_BEAM_W_DEEP
 #define DPRT_BEAM_W_DEEP DPRT_BEAM_W  // the large-brick configuration's beam width
 #endif
